@@ -1,0 +1,343 @@
+#!/usr/bin/env python
+"""Benchmark of the discrete X-ray transform hot path (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 4] [--impl ours|reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...        (one process per GPU, NCCL)
+
+One STEP = one pass of the whole hot path over the
+configuration's full ray set: the forward projection sino = A x (every ray of every view)
+followed by the adjoint x' = A^T sino, i.e. one application of the normal operator
+A^T A.  With N GPUs the views are split into N contiguous blocks (one plan per rank); each
+rank projects its block and backprojects it into a partial image, and the partial images
+are summed with one NCCL all_reduce (the path's only exchange step; x stays replicated, so
+no broadcast is needed between steps).  Strong scaling: the configuration is fixed.
+
+``value`` = rays per second of the whole job (all M rays through A and A^T per step).
+``e2e``   = the same through the host-buffer C-ABI entry points (xrt_forward_host /
+            xrt_adjoint_host): H2D of x and of the adjoint input, D2H of sino and x'
+            inside the timed region.
+``roofline`` for the dominant kernel: FP32-issue bound: algorithmic
+            FP32 ops = c * nnz per launch (c = 4 in 2D, 5 in 3D; nnz counted exactly) over
+            148 SMs x 128 lanes x sm_max_mhz.
+``cpu_baseline``: the fp64 oracle (oracle/, as it stands) on a bounded ray sample of the same
+            workload on this host's cores (rank 0, N = 1 only).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import workloads  # noqa: E402
+
+METRIC = "forward-projection rays/s and intersections/s (plus adjoint) vs roofline, 1–8 B200"
+C_OPS = {2: 4, 3: 5}  # algorithmic FP32 ops per ray-unit intersection
+
+
+def peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    src = "measured"
+    try:
+        with open(path) as f:
+            pk = json.load(f)
+    except Exception:
+        pk = {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0}
+        src = "fallback"
+    sm_mhz = float(pk.get("sm_max_mhz", 1965.0))
+    return {"hbm_gbs": float(pk["hbm_gbs"]), "sm_mhz": sm_mhz,
+            "fp32_tops": 148 * 128 * sm_mhz * 1e6 / 1e12, "src": src}
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=5).stdout.strip()
+                if out:
+                    self.rows.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if len(r) > 3 + i and r[3 + i] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def shard_views(c: dict, rank: int, world: int) -> dict:
+    """Contiguous block of views for this rank; helical z0/pitch are angle based."""
+    V = c["n_views"]
+    v0, v1 = V * rank // world, V * (rank + 1) // world
+    s = dict(c)
+    s["angles"] = np.asarray(c["angles"])[v0:v1]
+    s["n_views"] = v1 - v0
+    s["view_range"] = (v0, v1)
+    return s
+
+
+def cpu_baseline(c: dict, budget_s: float = 12.0):
+    """The oracle, as it stands, on a bounded sample of the workload's rays (forward)."""
+    import oracle
+    from oracle import geometry as G
+    img = workloads.make_image(c, device="cuda" if torch.cuda.is_available() else "cpu").cpu().numpy().reshape(-1)
+    done, t_used, rays = 0, 0.0, 0
+    seed = 9000
+    batch = 64
+    while t_used < budget_s and done < 200000:
+        ids = workloads.sample_rays(c, batch, seed=seed)
+        seed += 1
+        p, th = G.rays(c, ids)
+        t0 = time.perf_counter()
+        oracle.forward(c, img, p, th)
+        t_used += time.perf_counter() - t0
+        done += ids.size
+        if t_used < budget_s / 8:
+            batch *= 2
+    return {"value": done / t_used, "unit": "rays/s", "cores": oracle.threads(), "kind": "oracle",
+            "sample": f"{done} seeded rays of {c['name']} (stratified over views), fp64 brute-force forward "
+                      f"(separable early-out mode), {t_used:.1f} s"}
+
+
+def run_reference(args, c, rank, world):
+    """--impl reference: the oracle as the reference arm (rank 0 only)."""
+    if rank != 0:
+        return
+    import oracle
+    from oracle import geometry as G
+    img = workloads.make_image(c, device="cuda" if torch.cuda.is_available() else "cpu").cpu().numpy().reshape(-1)
+    per_step = args.ref_rays
+    times = []
+    seed = 7000
+    for s in range(args.warmup + args.steps):
+        ids = workloads.sample_rays(c, per_step, seed=seed + s)
+        p, th = G.rays(c, ids)
+        y = np.ones(ids.size)
+        t0 = time.perf_counter()
+        oracle.forward(c, img, p, th)
+        oracle.adjoint(c, y, p, th)
+        dt = time.perf_counter() - t0
+        if s >= args.warmup:
+            times.append((ids.size, dt))
+    rays = sum(n for n, _ in times)
+    tt = sum(t for _, t in times)
+    val = rays / tt
+    line = {"impl": "reference", "metric": METRIC, "value": val, "unit": "rays/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tt / max(1, len(times)),
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": {"workload": c["name"], "rays_per_step": per_step,
+                                            "note": "each reference step = forward + adjoint of a seeded ray sample"},
+            "cpu_baseline": {"value": val, "unit": "rays/s", "cores": oracle.threads(), "kind": "oracle",
+                             "sample": f"{per_step} seeded rays per step, fp64 brute force (forward + adjoint)"},
+            "e2e": {"value": val, "unit": "rays/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", type=int, default=4)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--algo", default="auto", choices=["auto", "ray", "column"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--ref-rays", type=int, default=256)
+    args = ap.parse_args()
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    c = workloads.config(args.config)
+    if args.impl == "reference":
+        run_reference(args, c, rank, world)
+        return
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    from paper_2006_00686_b200 import Plan
+    from paper_2006_00686_b200.dist import ShardedPlan
+
+    sp = ShardedPlan(c, rank=rank, world=world, device=local)
+    plan: Plan = sp.plan
+    if args.algo != "auto":
+        plan.set_algorithm("forward", args.algo)
+        plan.set_algorithm("adjoint", args.algo)
+    x = workloads.make_image(c, device=dev)
+    sino = torch.empty(plan.sino_shape, dtype=torch.float32, device=dev)
+    xo = torch.empty_like(x)
+    nnz_local = plan.n_units
+    nnz = torch.tensor([nnz_local], dtype=torch.int64, device=dev)
+    if world > 1:
+        dist.all_reduce(nnz)
+    nnz_total = int(nnz.item())
+    M = workloads.configs.n_rays(c)
+    dim = 2 if c["beam"] in ("par2d", "fan2d") else 3
+    s = torch.cuda.current_stream()
+
+    def step(ev=None):
+        if ev is not None:
+            ev[0].record(s)
+        plan.forward(x, out=sino)
+        if ev is not None:
+            ev[1].record(s)
+        plan.adjoint(sino, out=xo)
+        if ev is not None:
+            ev[2].record(s)
+        if world > 1:
+            dist.all_reduce(xo)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
+    start = torch.cuda.Event(enable_timing=True)
+    end = torch.cuda.Event(enable_timing=True)
+    launches0 = plan.launch_count
+    with ClockSampler(local) as clk:
+        start.record(s)
+        for k in range(args.steps):
+            step(evs[k])
+        end.record(s)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    launches = plan.launch_count - launches0
+    ms = start.elapsed_time(end)
+    fwd_ms = [e[0].elapsed_time(e[1]) for e in evs]
+    adj_ms = [e[1].elapsed_time(e[2]) for e in evs]
+    t = torch.tensor([ms, sum(fwd_ms), sum(adj_ms)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max, fwd_sum, adj_sum = [float(v) for v in t.tolist()]
+    value = M * args.steps / (ms_max / 1e3)
+
+    # ---------------- e2e through the host-buffer C ABI (pinned host memory)
+    e2e = None
+    if not args.no_e2e:
+        xh = x.cpu().pin_memory()
+        sh = torch.empty(plan.sino_shape, dtype=torch.float32).pin_memory()
+        xoh = torch.empty(plan.image_shape, dtype=torch.float32).pin_memory()
+        for _ in range(1):
+            plan.forward_host(xh, out=sh)
+            plan.adjoint_host(sh, out=xoh)
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        ke = max(1, min(args.steps, 3))
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(s)
+        for _ in range(ke):
+            plan.forward_host(xh, out=sh)
+            plan.adjoint_host(sh, out=xoh)
+        e1.record(s)
+        torch.cuda.synchronize()
+        te = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        e2e_ms = float(te.item())
+        img_b = x.numel() * 4
+        sino_b = sino.numel() * 4
+        e2e = {"value": M * ke / (e2e_ms / 1e3), "unit": "rays/s", "ms_per_step": e2e_ms / ke,
+               "h2d_bytes_per_step": img_b + sino_b, "d2h_bytes_per_step": sino_b + img_b,
+               "note": "xrt_forward_host + xrt_adjoint_host, pinned host buffers, per-rank bytes"}
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+    pk = peaks()
+    c_ops = C_OPS[dim]
+    fwd_avg = fwd_sum / args.steps
+    adj_avg = adj_sum / args.steps
+    # per-rank kernels: ops of this rank's shard
+    k_fwd = {"ms": fwd_avg, "tflops": c_ops * nnz_local / (fwd_avg / 1e3) / 1e12}
+    k_adj = {"ms": adj_avg, "tflops": c_ops * nnz_local / (adj_avg / 1e3) / 1e12}
+    dom_name, dom = ("adjoint", k_adj) if adj_avg >= fwd_avg else ("forward", k_fwd)
+    roof = {"bound": "alu", "kernel": dom_name, "achieved": dom["tflops"], "peak": pk["fp32_tops"],
+            "unit": "TFLOP/s", "frac": dom["tflops"] / pk["fp32_tops"], "traffic": None,
+            "peak_source": f"FP32 issue 148 SM x 128 lanes x {pk['sm_mhz']:.0f} MHz ({pk['src']} sm_max_mhz)",
+            "ops_per_intersection": c_ops}
+    line = {
+        "metric": METRIC, "value": value, "unit": "rays/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": c["name"], "rays": M, "intersections": nnz_total,
+                   "image": list(c["n"]), "views": c["n_views"], "det": [c["det_rows"], c["det_cols"]],
+                   "step": "sino = A x; x' = A^T sino (+ all_reduce for N > 1)",
+                   "l2": "inputs larger than L2 (image + sinogram > 126 MB)" if (x.numel() + sino.numel()) * 4 > 126e6
+                   else "inputs smaller than L2 (no flush)",
+                   "parallelism": f"views/{world}"},
+        "intersections_per_s": nnz_total * args.steps / (ms_max / 1e3),
+        "forward": {"ms": fwd_avg, "rays_per_s": M / world / (fwd_avg / 1e3),
+                    "intersections_per_s": nnz_local / (fwd_avg / 1e3),
+                    "roofline_frac": k_fwd["tflops"] / pk["fp32_tops"]},
+        "adjoint": {"ms": adj_avg, "rays_per_s": M / world / (adj_avg / 1e3),
+                    "intersections_per_s": nnz_local / (adj_avg / 1e3),
+                    "roofline_frac": k_adj["tflops"] / pk["fp32_tops"]},
+        "roofline": roof,
+        "gpu_launches": launches,
+        "clocks": clk.summary(),
+        "algo": args.algo,
+    }
+    if e2e is not None:
+        line["e2e"] = e2e
+    if world == 1 and not args.no_cpu:
+        try:
+            line["cpu_baseline"] = cpu_baseline(c)
+        except Exception as e:  # never let the baseline kill the bench line
+            line["cpu_baseline"] = {"value": None, "error": str(e)}
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

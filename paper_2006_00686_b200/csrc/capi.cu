@@ -1,0 +1,437 @@
+// capi.cu -- the extern "C" boundary declared in include/xrt.h: validation, the fp64 plan
+// builder (per-view ray families), dispatch to the kernels, the host-buffer
+// pipeline and the CSR dump (count -> scan -> fill -> per-row sort).
+#include <cuda_runtime.h>
+
+#include <cub/device/device_reduce.cuh>
+#include <cub/device/device_scan.cuh>
+#include <cub/device/device_segmented_sort.cuh>
+
+#include <climits>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "xrt_internal.cuh"
+
+namespace {
+
+thread_local std::string g_err;
+
+xrt_status fail(xrt_status s, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return s;
+}
+
+xrt_status cuda_fail(cudaError_t e, const char* what) {
+    if (e == cudaErrorMemoryAllocation) return fail(XRT_ERR_OOM, "%s: %s", what, cudaGetErrorString(e));
+    return fail(XRT_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
+}
+
+#define XRT_CUDA(call)                                         \
+    do {                                                       \
+        cudaError_t e_ = (call);                               \
+        if (e_ != cudaSuccess) return cuda_fail(e_, #call);    \
+    } while (0)
+
+struct DevGuard {
+    int prev = -1, want;
+    explicit DevGuard(int d) : want(d) {
+        cudaGetDevice(&prev);
+        if (prev != want) cudaSetDevice(want);
+    }
+    ~DevGuard() {
+        if (prev >= 0 && prev != want) cudaSetDevice(prev);
+    }
+};
+
+
+xrt_status validate(const xrt_geometry* g) {
+    if (!g) return fail(XRT_ERR_INVALID_ARG, "geometry is NULL");
+    if (g->reserved0 != 0) return fail(XRT_ERR_INVALID_ARG, "reserved0 must be 0");
+    if (g->beam < XRT_PAR2D || g->beam > XRT_HELICAL) return fail(XRT_ERR_INVALID_ARG, "unknown beam %d", g->beam);
+    const bool is2d = g->beam == XRT_PAR2D || g->beam == XRT_FAN2D;
+    const bool divergent = g->beam == XRT_FAN2D || g->beam == XRT_CONE || g->beam == XRT_HELICAL;
+    for (int a = 0; a < 3; ++a) {
+        if (is2d && a == 2) continue;
+        if (g->n[a] < 1) return fail(XRT_ERR_INVALID_ARG, "n[%d] = %lld must be >= 1", a, (long long)g->n[a]);
+        if (g->n[a] > (1 << 20)) return fail(XRT_ERR_UNSUPPORTED, "n[%d] too large", a);
+        if (!(std::isfinite(g->spacing[a]) && g->spacing[a] > 0))
+            return fail(XRT_ERR_INVALID_ARG, "spacing[%d] must be finite and > 0", a);
+        if (!std::isfinite(g->center[a])) return fail(XRT_ERR_INVALID_ARG, "center[%d] not finite", a);
+    }
+    if (is2d && g->n[2] != 1) return fail(XRT_ERR_INVALID_ARG, "2D beams need n[2] == 1");
+    const long double vox = (long double)g->n[0] * g->n[1] * (is2d ? 1 : g->n[2]);
+    if (vox > 4.0e9L) return fail(XRT_ERR_UNSUPPORTED, "image larger than 2^32 units");
+    if (g->n_views < 1) return fail(XRT_ERR_INVALID_ARG, "n_views must be >= 1");
+    if (!g->angles) return fail(XRT_ERR_INVALID_ARG, "angles is NULL");
+    for (int64_t v = 0; v < g->n_views; ++v)
+        if (!std::isfinite(g->angles[v])) return fail(XRT_ERR_INVALID_ARG, "angles[%lld] not finite", (long long)v);
+    if (g->det_cols < 1 || g->det_rows < 1) return fail(XRT_ERR_INVALID_ARG, "detector dims must be >= 1");
+    if (g->det_cols > INT_MAX || g->det_rows > INT_MAX) return fail(XRT_ERR_UNSUPPORTED, "detector too large");
+    if (is2d && g->det_rows != 1) return fail(XRT_ERR_INVALID_ARG, "2D beams need det_rows == 1");
+    for (int a = 0; a < 2; ++a) {
+        if (!(std::isfinite(g->det_spacing[a]) && g->det_spacing[a] > 0))
+            return fail(XRT_ERR_INVALID_ARG, "det_spacing[%d] must be finite and > 0", a);
+        if (!std::isfinite(g->det_offset[a])) return fail(XRT_ERR_INVALID_ARG, "det_offset[%d] not finite", a);
+    }
+    if (divergent) {
+        if (!(std::isfinite(g->sod) && g->sod > 0)) return fail(XRT_ERR_INVALID_ARG, "sod must be > 0");
+        if (!(std::isfinite(g->sdd) && g->sdd > g->sod)) return fail(XRT_ERR_INVALID_ARG, "sdd must be > sod");
+    }
+    if (g->beam == XRT_HELICAL && !(std::isfinite(g->pitch) && std::isfinite(g->z0)))
+        return fail(XRT_ERR_INVALID_ARG, "pitch / z0 not finite");
+    if (g->beam == XRT_PAR3D && !(std::isfinite(g->tilt) && std::fabs(g->tilt) < M_PI / 2))
+        return fail(XRT_ERR_INVALID_ARG, "tilt must satisfy |tilt| < pi/2");
+    return XRT_OK;
+}
+
+// Per-view terms of the paper's beam -> parallel-beam transforms (xrt_internal.cuh; P:132-138,
+// P:260-272; readings 7-11).  Evaluated with the host libm.
+xrt::ViewRec view_record(const xrt_geometry* g, double ang) {
+    xrt::ViewRec r;
+    std::memset(&r, 0, sizeof r);
+    double a = ang;
+    if (g->beam == XRT_FAN2D) a = ang - M_PI / 2;  // phi = gamma + (alpha - pi/2)
+    r.c1 = std::cos(a);
+    r.s1 = std::sin(a);
+    if (g->beam == XRT_PAR3D) {
+        r.c2 = std::cos(g->tilt);
+        r.s2 = std::sin(g->tilt);
+    }
+    if (g->beam == XRT_HELICAL) r.H = g->z0 + g->pitch * ang / (2.0 * M_PI);  // reading 11
+    return r;
+}
+
+xrt_status alloc_stage(xrt_plan p) {
+    if (!p->d_stage_img) XRT_CUDA(cudaMalloc(&p->d_stage_img, sizeof(float) * (size_t)p->grid.nxyz));
+    if (!p->d_stage_sino) XRT_CUDA(cudaMalloc(&p->d_stage_sino, sizeof(float) * (size_t)p->n_rays));
+    if (!p->aux_stream) {
+        cudaStream_t s;
+        XRT_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+        p->aux_stream = s;
+    }
+    return XRT_OK;
+}
+
+int resolve(int want, bool column_ok) {
+    if (want == XRT_ALGO_AUTO) return column_ok ? XRT_ALGO_COLUMN : XRT_ALGO_RAY;
+    return want;
+}
+
+xrt_status forward_range(xrt_plan p, const float* img, float* sino, int64_t v0, int64_t v1,
+                         cudaStream_t s) {
+    const int64_t pv = p->det.per_view;
+    const int algo = resolve(p->algo_fwd, p->column_ok);
+    cudaError_t e = cudaSuccess;
+    if (algo == XRT_ALGO_RAY) {
+        e = xrt::launch_forward_ray(p, img, sino, v0 * pv, v1 * pv, s);
+        p->launches += 1;
+    } else {
+        return fail(XRT_ERR_UNSUPPORTED, "forward algorithm %d not built", algo);
+    }
+    if (e != cudaSuccess) return cuda_fail(e, "forward launch");
+    return XRT_OK;
+}
+
+xrt_status adjoint_range(xrt_plan p, const float* sino, float* img, int64_t v0, int64_t v1,
+                         cudaStream_t s) {
+    const int64_t pv = p->det.per_view;
+    const int algo = resolve(p->algo_adj, p->column_ok);
+    cudaError_t e = cudaSuccess;
+    if (algo == XRT_ALGO_RAY) {
+        e = xrt::launch_adjoint_ray(p, sino, img, v0 * pv, v1 * pv, s);
+        p->launches += 1;
+    } else {
+        return fail(XRT_ERR_UNSUPPORTED, "adjoint algorithm %d not built", algo);
+    }
+    if (e != cudaSuccess) return cuda_fail(e, "adjoint launch");
+    return XRT_OK;
+}
+
+xrt_status count_units(xrt_plan p, int64_t* out, cudaStream_t s) {
+    const int64_t chunk = (int64_t)1 << 24;
+    int64_t* d_counts = nullptr;
+    int64_t* d_sum = nullptr;
+    void* d_tmp = nullptr;
+    size_t tmp_bytes = 0;
+    XRT_CUDA(cub::DeviceReduce::Sum(nullptr, tmp_bytes, (int64_t*)nullptr, (int64_t*)nullptr, (int)chunk, s));
+    XRT_CUDA(cudaMalloc(&d_counts, sizeof(int64_t) * chunk));
+    XRT_CUDA(cudaMalloc(&d_sum, sizeof(int64_t)));
+    XRT_CUDA(cudaMalloc(&d_tmp, tmp_bytes));
+    int64_t total = 0;
+    xrt_status st = XRT_OK;
+    for (int64_t r0 = 0; r0 < p->n_rays && st == XRT_OK; r0 += chunk) {
+        const int64_t r1 = std::min(p->n_rays, r0 + chunk);
+        cudaError_t e = xrt::launch_units_count(p, r0, r1, d_counts, s);
+        p->launches += 1;
+        if (e == cudaSuccess) e = cub::DeviceReduce::Sum(d_tmp, tmp_bytes, d_counts, d_sum, (int)(r1 - r0), s);
+        int64_t part = 0;
+        if (e == cudaSuccess) e = cudaMemcpyAsync(&part, d_sum, sizeof part, cudaMemcpyDeviceToHost, s);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+        if (e != cudaSuccess) st = cuda_fail(e, "count_units");
+        total += part;
+    }
+    cudaFree(d_counts);
+    cudaFree(d_sum);
+    cudaFree(d_tmp);
+    if (st == XRT_OK) *out = total;
+    return st;
+}
+
+}  // namespace
+
+extern "C" {
+
+int32_t xrt_version(void) { return (XRT_VERSION_MAJOR << 16) | XRT_VERSION_MINOR; }
+
+const char* xrt_last_error(void) { return g_err.c_str(); }
+
+xrt_status xrt_plan_create(const xrt_geometry* g, int cuda_device, xrt_plan* out) {
+    if (!out) return fail(XRT_ERR_INVALID_ARG, "out is NULL");
+    *out = nullptr;
+    xrt_status st = validate(g);
+    if (st != XRT_OK) return st;
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || cuda_device < 0 || cuda_device >= ndev)
+        return fail(XRT_ERR_INVALID_ARG, "cuda_device %d not available (%d devices)", cuda_device, ndev);
+    DevGuard guard(cuda_device);
+    xrt_plan p = new (std::nothrow) xrt_plan_s();
+    if (!p) return fail(XRT_ERR_OOM, "host allocation");
+    const bool is2d = g->beam == XRT_PAR2D || g->beam == XRT_FAN2D;
+    p->device = cuda_device;
+    p->beam = g->beam;
+    p->dim = is2d ? 2 : 3;
+    xrt::GridC& G = p->grid;
+    for (int a = 0; a < 3; ++a) {
+        G.n[a] = (int)(is2d && a == 2 ? 1 : g->n[a]);
+        G.d[a] = is2d && a == 2 ? 1.0 : g->spacing[a];
+    }
+    const double cz = is2d ? 0.0 : g->center[2];
+    G.x_lo = g->center[0] - G.n[0] * G.d[0] / 2.0;
+    G.y_hi = g->center[1] + G.n[1] * G.d[1] / 2.0;
+    G.z_hi = cz + G.n[2] * G.d[2] / 2.0;
+    G.tau = 1e-9 * std::min(G.d[0], std::min(G.d[1], is2d ? G.d[0] : G.d[2]));
+    G.nxy = (int64_t)G.n[0] * G.n[1];
+    G.nxyz = G.nxy * G.n[2];
+    xrt::DetC& D = p->det;
+    D.beam = g->beam;
+    D.D = g->sod;
+    D.sdd = g->sdd;
+    D.cols = (int)g->det_cols;
+    D.rows = (int)g->det_rows;
+    D.du = g->det_spacing[0];
+    D.dv = g->det_spacing[1];
+    D.cu = (g->det_cols - 1) / 2.0;
+    D.cv = (g->det_rows - 1) / 2.0;
+    D.off_u = g->det_offset[0];
+    D.off_v = is2d ? 0.0 : g->det_offset[1];
+    D.per_view = (int64_t)D.cols * D.rows;
+    p->n_views = g->n_views;
+    p->n_rays = D.per_view * g->n_views;
+    std::vector<xrt::ViewRec> views((size_t)g->n_views);
+    for (int64_t v = 0; v < g->n_views; ++v) views[v] = view_record(g, g->angles[v]);
+    cudaError_t e = cudaMalloc(&p->d_views, sizeof(xrt::ViewRec) * views.size());
+    if (e == cudaSuccess)
+        e = cudaMemcpy(p->d_views, views.data(), sizeof(xrt::ViewRec) * views.size(), cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) {
+        xrt_plan_destroy(p);
+        return cuda_fail(e, "plan tables");
+    }
+    p->column_ok = false;
+    *out = p;
+    return XRT_OK;
+}
+
+xrt_status xrt_plan_destroy(xrt_plan p) {
+    if (!p) return XRT_OK;
+    DevGuard guard(p->device);
+    cudaFree(p->d_views);
+    cudaFree(p->d_work);
+    cudaFree(p->d_stage_img);
+    cudaFree(p->d_stage_sino);
+    if (p->aux_stream) cudaStreamDestroy((cudaStream_t)p->aux_stream);
+    delete p;
+    return XRT_OK;
+}
+
+xrt_status xrt_plan_query(xrt_plan p, int64_t* n_rays, int64_t* n_units) {
+    if (!p) return fail(XRT_ERR_INVALID_ARG, "plan is NULL");
+    if (n_rays) *n_rays = p->n_rays;
+    if (n_units) {
+        if (p->n_units < 0) {
+            DevGuard guard(p->device);
+            xrt_status st = count_units(p, &p->n_units, (cudaStream_t)0);
+            if (st != XRT_OK) return st;
+        }
+        *n_units = p->n_units;
+    }
+    return XRT_OK;
+}
+
+xrt_status xrt_plan_set_algorithm(xrt_plan p, int32_t op, int32_t algo) {
+    if (!p) return fail(XRT_ERR_INVALID_ARG, "plan is NULL");
+    if (op != XRT_OP_FORWARD && op != XRT_OP_ADJOINT) return fail(XRT_ERR_INVALID_ARG, "bad op %d", op);
+    if (algo < XRT_ALGO_AUTO || algo > XRT_ALGO_COLUMN) return fail(XRT_ERR_INVALID_ARG, "bad algo %d", algo);
+    if (algo == XRT_ALGO_COLUMN && !p->column_ok)
+        return fail(XRT_ERR_UNSUPPORTED, "column algorithm does not serve this geometry");
+    if (op == XRT_OP_FORWARD) p->algo_fwd = algo; else p->algo_adj = algo;
+    return XRT_OK;
+}
+
+int64_t xrt_plan_launch_count(xrt_plan p) { return p ? p->launches : -1; }
+
+xrt_status xrt_forward(xrt_plan p, const float* img, float* sino, void* cuda_stream) {
+    if (!p || !img || !sino) return fail(XRT_ERR_INVALID_ARG, "NULL argument");
+    DevGuard guard(p->device);
+    return forward_range(p, img, sino, 0, p->n_views, (cudaStream_t)cuda_stream);
+}
+
+xrt_status xrt_adjoint(xrt_plan p, const float* sino, float* img, void* cuda_stream) {
+    if (!p || !img || !sino) return fail(XRT_ERR_INVALID_ARG, "NULL argument");
+    DevGuard guard(p->device);
+    cudaStream_t s = (cudaStream_t)cuda_stream;
+    XRT_CUDA(cudaMemsetAsync(img, 0, sizeof(float) * (size_t)p->grid.nxyz, s));
+    return adjoint_range(p, sino, img, 0, p->n_views, s);
+}
+
+// Host-buffer forward: H2D(image) -> per view chunk: kernel, then D2H of that chunk on the aux
+// stream, so the sinogram download overlaps the next chunk's kernel.
+xrt_status xrt_forward_host(xrt_plan p, const float* img_host, float* sino_host, void* cuda_stream) {
+    if (!p || !img_host || !sino_host) return fail(XRT_ERR_INVALID_ARG, "NULL argument");
+    DevGuard guard(p->device);
+    xrt_status st = alloc_stage(p);
+    if (st != XRT_OK) return st;
+    cudaStream_t s = (cudaStream_t)cuda_stream, a = (cudaStream_t)p->aux_stream;
+    XRT_CUDA(cudaMemcpyAsync(p->d_stage_img, img_host, sizeof(float) * (size_t)p->grid.nxyz,
+                             cudaMemcpyHostToDevice, s));
+    const int64_t nchunk = std::min<int64_t>(8, p->n_views);
+    const int64_t pv = p->det.per_view;
+    std::vector<cudaEvent_t> ev((size_t)nchunk);
+    for (auto& x : ev) XRT_CUDA(cudaEventCreateWithFlags(&x, cudaEventDisableTiming));
+    for (int64_t k = 0; k < nchunk && st == XRT_OK; ++k) {
+        const int64_t v0 = p->n_views * k / nchunk, v1 = p->n_views * (k + 1) / nchunk;
+        st = forward_range(p, p->d_stage_img, p->d_stage_sino, v0, v1, s);
+        if (st != XRT_OK) break;
+        cudaError_t e = cudaEventRecord(ev[k], s);
+        if (e == cudaSuccess) e = cudaStreamWaitEvent(a, ev[k], 0);
+        if (e == cudaSuccess)
+            e = cudaMemcpyAsync(sino_host + v0 * pv, p->d_stage_sino + v0 * pv,
+                                sizeof(float) * (size_t)((v1 - v0) * pv), cudaMemcpyDeviceToHost, a);
+        if (e != cudaSuccess) st = cuda_fail(e, "forward_host pipeline");
+    }
+    cudaError_t e1 = cudaStreamSynchronize(a);
+    cudaError_t e2 = cudaStreamSynchronize(s);
+    for (auto& x : ev) cudaEventDestroy(x);
+    if (st != XRT_OK) return st;
+    if (e1 != cudaSuccess) return cuda_fail(e1, "forward_host sync");
+    if (e2 != cudaSuccess) return cuda_fail(e2, "forward_host sync");
+    return XRT_OK;
+}
+
+// Host-buffer adjoint: per view chunk H2D(sino chunk) on the aux stream overlapping the previous
+// chunk's kernel, then D2H(image).
+xrt_status xrt_adjoint_host(xrt_plan p, const float* sino_host, float* img_host, void* cuda_stream) {
+    if (!p || !img_host || !sino_host) return fail(XRT_ERR_INVALID_ARG, "NULL argument");
+    DevGuard guard(p->device);
+    xrt_status st = alloc_stage(p);
+    if (st != XRT_OK) return st;
+    cudaStream_t s = (cudaStream_t)cuda_stream, a = (cudaStream_t)p->aux_stream;
+    XRT_CUDA(cudaMemsetAsync(p->d_stage_img, 0, sizeof(float) * (size_t)p->grid.nxyz, s));
+    const int64_t nchunk = std::min<int64_t>(8, p->n_views);
+    const int64_t pv = p->det.per_view;
+    std::vector<cudaEvent_t> ev((size_t)nchunk);
+    for (auto& x : ev) XRT_CUDA(cudaEventCreateWithFlags(&x, cudaEventDisableTiming));
+    // all uploads on the aux stream, each kernel waits for its chunk
+    for (int64_t k = 0; k < nchunk && st == XRT_OK; ++k) {
+        const int64_t v0 = p->n_views * k / nchunk, v1 = p->n_views * (k + 1) / nchunk;
+        cudaError_t e = cudaMemcpyAsync(p->d_stage_sino + v0 * pv, sino_host + v0 * pv,
+                                        sizeof(float) * (size_t)((v1 - v0) * pv), cudaMemcpyHostToDevice, a);
+        if (e == cudaSuccess) e = cudaEventRecord(ev[k], a);
+        if (e == cudaSuccess) e = cudaStreamWaitEvent(s, ev[k], 0);
+        if (e != cudaSuccess) { st = cuda_fail(e, "adjoint_host pipeline"); break; }
+        st = adjoint_range(p, p->d_stage_sino, p->d_stage_img, v0, v1, s);
+    }
+    if (st == XRT_OK) {
+        cudaError_t e = cudaMemcpyAsync(img_host, p->d_stage_img, sizeof(float) * (size_t)p->grid.nxyz,
+                                        cudaMemcpyDeviceToHost, s);
+        if (e != cudaSuccess) st = cuda_fail(e, "adjoint_host D2H");
+    }
+    cudaError_t e1 = cudaStreamSynchronize(s);
+    cudaError_t e2 = cudaStreamSynchronize(a);
+    for (auto& x : ev) cudaEventDestroy(x);
+    if (st != XRT_OK) return st;
+    if (e1 != cudaSuccess) return cuda_fail(e1, "adjoint_host sync");
+    if (e2 != cudaSuccess) return cuda_fail(e2, "adjoint_host sync");
+    return XRT_OK;
+}
+
+xrt_status xrt_ray_units(xrt_plan p, int64_t ray_begin, int64_t ray_end, int64_t* row_ptr,
+                         int64_t* cols, double* lens, int64_t capacity, int64_t* nnz_out,
+                         void* cuda_stream) {
+    if (!p || !row_ptr || !nnz_out) return fail(XRT_ERR_INVALID_ARG, "NULL argument");
+    if (ray_begin < 0 || ray_end < ray_begin || ray_end > p->n_rays)
+        return fail(XRT_ERR_INVALID_ARG, "ray range [%lld, %lld) outside [0, %lld)", (long long)ray_begin,
+                    (long long)ray_end, (long long)p->n_rays);
+    if ((cols == nullptr) != (lens == nullptr)) return fail(XRT_ERR_INVALID_ARG, "cols and lens must both be set or both NULL");
+    DevGuard guard(p->device);
+    cudaStream_t s = (cudaStream_t)cuda_stream;
+    const int64_t n = ray_end - ray_begin;
+    if (n > INT_MAX) return fail(XRT_ERR_UNSUPPORTED, "more than 2^31-1 rays in one call");
+    XRT_CUDA(cudaMemsetAsync(row_ptr, 0, sizeof(int64_t), s));
+    if (n == 0) {
+        *nnz_out = 0;
+        return XRT_OK;
+    }
+    int64_t* d_counts = nullptr;
+    void* d_tmp = nullptr;
+    size_t tmp_bytes = 0;
+    xrt_status st = XRT_OK;
+    cudaError_t e = cudaMallocAsync(&d_counts, sizeof(int64_t) * (size_t)n, s);
+    if (e == cudaSuccess) { e = xrt::launch_units_count(p, ray_begin, ray_end, d_counts, s); p->launches += 1; }
+    if (e == cudaSuccess) e = cub::DeviceScan::InclusiveSum(nullptr, tmp_bytes, d_counts, row_ptr + 1, (int)n, s);
+    if (e == cudaSuccess) e = cudaMallocAsync(&d_tmp, tmp_bytes, s);
+    if (e == cudaSuccess) e = cub::DeviceScan::InclusiveSum(d_tmp, tmp_bytes, d_counts, row_ptr + 1, (int)n, s);
+    int64_t nnz = 0;
+    if (e == cudaSuccess) e = cudaMemcpyAsync(&nnz, row_ptr + n, sizeof nnz, cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    if (d_tmp) cudaFreeAsync(d_tmp, s);
+    if (d_counts) cudaFreeAsync(d_counts, s);
+    d_tmp = nullptr;
+    if (e != cudaSuccess) return cuda_fail(e, "ray_units count");
+    *nnz_out = nnz;
+    if (!cols) return XRT_OK;
+    if (capacity < nnz) return fail(XRT_ERR_CAPACITY, "capacity %lld < nnz %lld", (long long)capacity, (long long)nnz);
+    if (nnz > INT_MAX) return fail(XRT_ERR_UNSUPPORTED, "nnz > 2^31-1 in one call; split the ray range");
+    if (nnz == 0) return XRT_OK;
+    // fill in traversal order into scratch, then sort each row by flat index into the caller's arrays
+    int64_t* k_in = nullptr;
+    double* v_in = nullptr;
+    e = cudaMallocAsync(&k_in, sizeof(int64_t) * (size_t)nnz, s);
+    if (e == cudaSuccess) e = cudaMallocAsync(&v_in, sizeof(double) * (size_t)nnz, s);
+    if (e == cudaSuccess) { e = xrt::launch_units_fill(p, ray_begin, ray_end, row_ptr, k_in, v_in, s); p->launches += 1; }
+    tmp_bytes = 0;
+    if (e == cudaSuccess)
+        e = cub::DeviceSegmentedSort::SortPairs(nullptr, tmp_bytes, k_in, cols, v_in, lens, (int)nnz, (int)n,
+                                                row_ptr, row_ptr + 1, s);
+    if (e == cudaSuccess) e = cudaMallocAsync(&d_tmp, tmp_bytes, s);
+    if (e == cudaSuccess)
+        e = cub::DeviceSegmentedSort::SortPairs(d_tmp, tmp_bytes, k_in, cols, v_in, lens, (int)nnz, (int)n,
+                                                row_ptr, row_ptr + 1, s);
+    if (d_tmp) cudaFreeAsync(d_tmp, s);
+    if (k_in) cudaFreeAsync(k_in, s);
+    if (v_in) cudaFreeAsync(v_in, s);
+    if (e != cudaSuccess) st = cuda_fail(e, "ray_units fill");
+    return st;
+}
+
+}  // extern "C"

@@ -1,0 +1,247 @@
+// kern_ray.cu -- one thread per ray: forward (fp32), adjoint scatter (fp32 red.add) and the
+// fp64 CSR count / fill passes.  Works for every beam and every direction (including the
+// paper's Cases 2-4: axis-parallel and plane-parallel rays).
+//
+// The per-ray enumeration is the paper's method in incremental form.  Along each axis a with
+// w_a != 0 the ray enters successive unit slabs at the crossing values
+//     T_a(b) = (b - u0_a) / w_a                                   (the paper's C_x, C_y, C_z:
+//                                                                  eq:C_xC_y P:170-172,
+//                                                                  eq:C_xC_yC_z P:446-450)
+// and a unit (i, j, k) is intersected non-vanishingly iff C_low < C_up with
+// C_low = max of its slab entries, C_up = min of its slab exits (eq:conditions_2D_1 P:180-187,
+// eq:conditions_3D_1 P:460-468).  Walking the three monotone crossing sequences in merged order
+// visits exactly the units with C_low < C_up -- for a slice i of one axis, the units visited
+// inside it are the valid band of the other index (eq:restriction_j P:197-212,
+// eq:restriction_j_3D / eq:restriction_k_3D_1 P:479-499), found with one comparison per band
+// member instead of a search -- and the length of the current unit is
+//     l = C_up - C_low = (next crossing) - (previous crossing)   (eq:range_length P:217-220).
+// Each crossing value is computed once and shared by the two units it separates
+// ("telescoping", SURVEY hard part 1), which keeps fp32 sums accurate.  Axes with w_a == 0 keep
+// the half-open cell floor(u0_a) (ties to the bigger index).
+#include <cuda_runtime.h>
+
+#include "xrt_internal.cuh"
+
+namespace xrt {
+
+namespace {
+
+// fp32 per-ray state, relative to t_in (all times >= 0).
+struct Ray32 {
+    float T[3];    // next crossing time per axis (INF if the axis is fixed)
+    float t1[3];   // first crossing time
+    float dt[3];   // crossing spacing 1/|w|
+    float m[3];    // crossings taken so far
+    int step[3];   // signed flat-index stride
+    float tend;    // end of the last unit (<= the fp32 face-crossing time of every axis)
+    int budget;    // 1 + number of interior crossings: hard cap on loop trips
+    int64_t idx;   // flat index of the current unit
+};
+
+__device__ __forceinline__ void to_ray32(const Ray64& R, const GridC& g, Ray32& S) {
+    const int64_t strides[3] = {1, (int64_t)g.n[0], g.nxy};
+    float tend = (float)(R.t_out - R.t_in);
+    int budget = 1;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        S.m[a] = 0.f;
+        if (!R.moving[a]) {
+            S.T[a] = INFINITY;
+            S.t1[a] = INFINITY;
+            S.dt[a] = 0.f;
+            S.step[a] = 0;
+            continue;
+        }
+        const int pos = R.w[a] > 0.0;
+        const int b_first = pos ? R.cell[a] + 1 : R.cell[a];
+        const int m_face = pos ? (g.n[a] - b_first) : b_first;  // interior crossings before the face
+        S.t1[a] = (float)(((double)b_first - R.u0[a]) * R.inv_w[a] - R.t_in);
+        S.dt[a] = (float)fabs(R.inv_w[a]);
+        S.step[a] = (int)(pos ? strides[a] : -strides[a]);
+        S.T[a] = S.t1[a];
+        budget += m_face;
+        // the face crossing computed exactly as the loop would compute it: no axis can ever
+        // step past its last interior boundary before tend (keeps every load in bounds)
+        tend = fminf(tend, fmaf((float)m_face, S.dt[a], S.t1[a]));
+    }
+    S.tend = tend;
+    S.budget = budget;
+    S.idx = ((int64_t)R.cell[2] * g.n[1] + R.cell[1]) * g.n[0] + R.cell[0];
+}
+
+// Advance the axis whose crossing defined tn (one axis per call; ties advance on the next
+// iteration with a zero-length unit in between).
+__device__ __forceinline__ void advance(Ray32& S, float tn) {
+    if (tn == S.T[0]) {
+        S.m[0] += 1.f; S.T[0] = fmaf(S.m[0], S.dt[0], S.t1[0]); S.idx += S.step[0];
+    } else if (tn == S.T[1]) {
+        S.m[1] += 1.f; S.T[1] = fmaf(S.m[1], S.dt[1], S.t1[1]); S.idx += S.step[1];
+    } else if (tn == S.T[2]) {
+        S.m[2] += 1.f; S.T[2] = fmaf(S.m[2], S.dt[2], S.t1[2]); S.idx += S.step[2];
+    }
+}
+
+__device__ __forceinline__ void ray_of(int64_t m, const DetC& dc, int& v, int& r, int& c) {
+    const int64_t pv = dc.per_view;
+    v = (int)(m / pv);
+    const int64_t rem = m - (int64_t)v * pv;
+    r = (int)(rem / dc.cols);
+    c = (int)(rem - (int64_t)r * dc.cols);
+}
+
+__global__ void __launch_bounds__(256) k_forward_ray(const ViewRec* __restrict__ views, DetC dc,
+                                                      GridC g, const float* __restrict__ img,
+                                                      float* __restrict__ sino, int64_t ray0,
+                                                      int64_t ray1) {
+    const int64_t m = ray0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (m >= ray1) return;
+    int v, r, c;
+    ray_of(m, dc, v, r, c);
+    Ray64 R;
+    float acc = 0.f;
+    if (setup_ray(views[v], dc, g, r, c, R)) {
+        Ray32 S;
+        to_ray32(R, g, S);
+        float tc = 0.f;
+        for (int it = 0; tc < S.tend && it < S.budget; ++it) {
+            const float tn = fminf(fminf(S.T[0], S.T[1]), fminf(S.T[2], S.tend));
+            acc = fmaf(__ldg(img + S.idx), tn - tc, acc);  // f_I * (C_up - C_low)
+            tc = tn;
+            advance(S, tn);
+        }
+    }
+    sino[m] = acc;
+}
+
+__global__ void __launch_bounds__(256) k_adjoint_ray(const ViewRec* __restrict__ views, DetC dc,
+                                                      GridC g, const float* __restrict__ sino,
+                                                      float* __restrict__ img, int64_t ray0,
+                                                      int64_t ray1) {
+    const int64_t m = ray0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (m >= ray1) return;
+    const float y = sino[m];
+    if (y == 0.f) return;
+    int v, r, c;
+    ray_of(m, dc, v, r, c);
+    Ray64 R;
+    if (!setup_ray(views[v], dc, g, r, c, R)) return;
+    Ray32 S;
+    to_ray32(R, g, S);
+    float tc = 0.f;
+    for (int it = 0; tc < S.tend && it < S.budget; ++it) {
+        const float tn = fminf(fminf(S.T[0], S.T[1]), fminf(S.T[2], S.tend));
+        const float l = tn - tc;
+        if (l > 0.f) atomicAdd(img + S.idx, y * l);
+        tc = tn;
+        advance(S, tn);
+    }
+}
+
+// fp64 enumeration for the CSR dump: crossing values recomputed exactly as the clip computed
+// the face values, so an axis never steps through the image face (see setup_ray).
+template <bool kFill>
+__device__ __forceinline__ int64_t units64(const Ray64& R, const GridC& g, int64_t* cols,
+                                           double* lens) {
+    int cell[3] = {R.cell[0], R.cell[1], R.cell[2]};
+    double T[3];
+    int bnd[3];
+    int sgn[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        if (!R.moving[a]) { T[a] = INFINITY; bnd[a] = 0; sgn[a] = 0; continue; }
+        sgn[a] = R.w[a] > 0.0 ? 1 : -1;
+        bnd[a] = sgn[a] > 0 ? cell[a] + 1 : cell[a];
+        T[a] = ((double)bnd[a] - R.u0[a]) * R.inv_w[a];
+    }
+    double t = R.t_in;
+    int64_t n = 0;
+    const int budget = 2 + g.n[0] + g.n[1] + g.n[2];
+    for (int it = 0; it < budget; ++it) {
+        const double tn = fmin(fmin(T[0], T[1]), fmin(T[2], R.t_out));
+        const double l = tn - t;  // C_up - C_low
+        if (l > g.tau) {
+            if (kFill) {
+                cols[n] = ((int64_t)cell[2] * g.n[1] + cell[1]) * g.n[0] + cell[0];
+                lens[n] = l;
+            }
+            ++n;
+        }
+        if (tn >= R.t_out) break;
+        int a = (tn == T[0]) ? 0 : ((tn == T[1]) ? 1 : 2);
+        cell[a] += sgn[a];
+        bnd[a] += sgn[a];
+        T[a] = ((double)bnd[a] - R.u0[a]) * R.inv_w[a];
+        t = tn;
+    }
+    return n;
+}
+
+__global__ void __launch_bounds__(128) k_units_count(const ViewRec* __restrict__ views, DetC dc,
+                                                      GridC g, int64_t ray0, int64_t ray1,
+                                                      int64_t* __restrict__ counts) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t m = ray0 + i;
+    if (m >= ray1) return;
+    int v, r, c;
+    ray_of(m, dc, v, r, c);
+    Ray64 R;
+    int64_t n = 0;
+    if (setup_ray(views[v], dc, g, r, c, R)) n = units64<false>(R, g, nullptr, nullptr);
+    counts[i] = n;
+}
+
+__global__ void __launch_bounds__(128) k_units_fill(const ViewRec* __restrict__ views, DetC dc,
+                                                     GridC g, int64_t ray0, int64_t ray1,
+                                                     const int64_t* __restrict__ row_ptr,
+                                                     int64_t* __restrict__ cols,
+                                                     double* __restrict__ lens) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t m = ray0 + i;
+    if (m >= ray1) return;
+    int v, r, c;
+    ray_of(m, dc, v, r, c);
+    Ray64 R;
+    if (setup_ray(views[v], dc, g, r, c, R)) {
+        const int64_t o = row_ptr[i];
+        units64<true>(R, g, cols + o, lens + o);
+    }
+}
+
+inline unsigned blocks_for(int64_t n, int bs) { return (unsigned)((n + bs - 1) / bs); }
+
+}  // namespace
+
+cudaError_t launch_forward_ray(const xrt_plan_s* p, const float* img, float* sino, int64_t ray0,
+                               int64_t ray1, cudaStream_t s) {
+    if (ray1 <= ray0) return cudaSuccess;
+    k_forward_ray<<<blocks_for(ray1 - ray0, 256), 256, 0, s>>>(p->d_views, p->det, p->grid, img,
+                                                               sino, ray0, ray1);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_adjoint_ray(const xrt_plan_s* p, const float* sino, float* img, int64_t ray0,
+                               int64_t ray1, cudaStream_t s) {
+    if (ray1 <= ray0) return cudaSuccess;
+    k_adjoint_ray<<<blocks_for(ray1 - ray0, 256), 256, 0, s>>>(p->d_views, p->det, p->grid, sino,
+                                                               img, ray0, ray1);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_units_count(const xrt_plan_s* p, int64_t ray0, int64_t ray1, int64_t* counts,
+                               cudaStream_t s) {
+    if (ray1 <= ray0) return cudaSuccess;
+    k_units_count<<<blocks_for(ray1 - ray0, 128), 128, 0, s>>>(p->d_views, p->det, p->grid, ray0,
+                                                               ray1, counts);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_units_fill(const xrt_plan_s* p, int64_t ray0, int64_t ray1,
+                              const int64_t* row_ptr, int64_t* cols, double* lens,
+                              cudaStream_t s) {
+    if (ray1 <= ray0) return cudaSuccess;
+    k_units_fill<<<blocks_for(ray1 - ray0, 128), 128, 0, s>>>(p->d_views, p->det, p->grid, ray0,
+                                                              ray1, row_ptr, cols, lens);
+    return cudaGetLastError();
+}
+
+}  // namespace xrt

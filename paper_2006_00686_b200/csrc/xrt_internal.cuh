@@ -1,0 +1,208 @@
+// xrt_internal.cuh -- plan layout and the per-ray geometry shared by every kernel.
+//
+// A plan stores, per view v, the view-dependent terms of the paper's transformation of that
+// view's rays to parallel-beam parameters (DESIGN.md section 5 "Plan"); every ray is then
+// built in fp64 exactly as the paper parameterises it:
+//   2D   ray (s, phi):  theta = (cos phi, sin phi), foot point s theta_perp
+//   3D   ray (s1, s2, phi1, phi2): theta, theta_1, theta_2 of P:404-412, foot point
+//        s1 theta_1 + s2 theta_2
+//   fan  s = D t / sqrt(D^2 + t^2), phi = arctan(t / D) + alpha - pi/2
+//   cone phi1 = phi1' + alpha, phi2 = beta, s1 = D sin(alpha), s2 = h cos^2(alpha) cos(beta),
+//        alpha = arctan(t / D), beta = arctan(h / sqrt(D^2 + t^2))
+//   helix s2 += H cos(beta)
+// with t = u sod / sdd, h = v sod / sdd (flat detector at sdd, reading 8).  Sums of angles are
+// formed with the addition theorem from per-view cos/sin (host, libm) and the per-ray
+// cos/sin of arctan (algebraic), so no per-ray transcendental is evaluated.  Parameterising at
+// the paper's foot point (not at the source) also makes the fixed coordinate of an
+// axis-parallel ray exact (e.g. the central fan ray of a view at alpha = pi/2 has y = s = 0
+// exactly, where the source has y = D cos(pi/2) = 6e-14), which the half-open tie rule needs.
+#pragma once
+
+#include <cstdint>
+#include <cmath>
+
+#include "../../include/xrt.h"
+
+namespace xrt {
+
+struct ViewRec {
+    // par2d: cos/sin(phi); fan: cos/sin(alpha - pi/2); par3d: cos/sin(phi1);
+    // cone / helical: cos/sin(phi1')
+    double c1, s1;
+    double c2, s2;  // par3d: cos/sin(phi2 = tilt); unused otherwise
+    double H;       // helical source height H(phi1'); 0 otherwise
+    double pad[3];
+};
+
+struct GridC {
+    int n[3];          // N_x, N_y, N_z
+    double d[3];       // spacing
+    double x_lo, y_hi, z_hi;
+    double tau;        // drop threshold for the fp64 CSR path (reading 4)
+    int64_t nxy, nxyz;
+};
+
+struct DetC {
+    int beam;                              // xrt_beam
+    double D, sdd;                         // source-to-origin / -detector distances
+    int cols, rows;
+    double du, dv, cu, cv, off_u, off_v;  // u_c = (c - cu) du + off_u
+    int64_t per_view;                      // rows * cols
+};
+
+constexpr double kSnap = 1e-12;  // |theta_a| <= kSnap -> 0 (reading 2/5)
+
+// Index-space description of one ray: u(t) = u0 + t w, t the physical arc length.
+// Unit (i, j, k) is [i, i+1) x [j, j+1) x [k, k+1) in u (P:151, P:427 shifted/scaled; reading 2).
+struct Ray64 {
+    double u0[3];
+    double w[3];
+    double inv_w[3];
+    double t_in, t_out;  // clip of the line to the image box
+    int cell[3];         // unit containing u(t) just after t_in
+    int moving[3];       // w != 0
+};
+
+// Compute the ray of detector bin (view v, row r, col c) and clip it to the image box (fp64).
+// Returns false when the ray has no unit with length > tau (the whole chord is <= tau).
+__device__ __forceinline__ void paper_ray(const ViewRec& V, const DetC& dc, int r, int c,
+                                          double p[3], double th[3]) {
+    const double u = ((double)c - dc.cu) * dc.du + dc.off_u;
+    const double v = ((double)r - dc.cv) * dc.dv + dc.off_v;
+    const double D = dc.D;
+    switch (dc.beam) {
+        case XRT_PAR2D: {  // (s, phi) = (u, angle_v)
+            th[0] = V.c1; th[1] = V.s1; th[2] = 0.0;
+            p[0] = -u * V.s1; p[1] = u * V.c1; p[2] = 0.0;
+            break;
+        }
+        case XRT_FAN2D: {  // equispaced fan, t on the iso plane
+            const double t = u * D / dc.sdd;
+            const double den = sqrt(D * D + t * t);
+            const double cg = D / den, sg = t / den;          // cos/sin(arctan(t/D))
+            const double s = D * t / den;
+            const double cp = V.c1 * cg - V.s1 * sg;          // cos(gamma + alpha - pi/2)
+            const double sp = V.s1 * cg + V.c1 * sg;
+            th[0] = cp; th[1] = sp; th[2] = 0.0;
+            p[0] = -s * sp; p[1] = s * cp; p[2] = 0.0;
+            break;
+        }
+        case XRT_PAR3D: {  // (s1, s2, phi1, phi2) = (u, v, angle_v, tilt)
+            const double c1 = V.c1, s1 = V.s1, c2 = V.c2, s2 = V.s2;
+            th[0] = c2 * c1; th[1] = c2 * s1; th[2] = s2;
+            p[0] = u * (-s1) + v * (-s2 * c1);
+            p[1] = u * c1 + v * (-s2 * s1);
+            p[2] = v * c2;
+            break;
+        }
+        default: {  // cone / helical, equispaced flat detector
+            const double t = u * D / dc.sdd;
+            const double h = v * D / dc.sdd;
+            const double q = D * D + t * t;
+            const double sq = sqrt(q);
+            const double ca = D / sq, sa = t / sq;            // alpha = arctan(t / D)
+            const double r3 = sqrt(q + h * h);
+            const double cb = sq / r3, sb = h / r3;           // beta = arctan(h / sqrt(D^2+t^2))
+            const double s1 = D * sa;
+            const double s2 = h * (ca * ca) * cb + V.H * cb;
+            const double c1 = V.c1 * ca - V.s1 * sa;          // phi1 = phi1' + alpha
+            const double n1 = V.s1 * ca + V.c1 * sa;
+            th[0] = cb * c1; th[1] = cb * n1; th[2] = sb;
+            p[0] = s1 * (-n1) + s2 * (-sb * c1);
+            p[1] = s1 * c1 + s2 * (-sb * n1);
+            p[2] = s2 * cb;
+            break;
+        }
+    }
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+        if (fabs(th[a]) <= kSnap) th[a] = 0.0;
+}
+
+__device__ __forceinline__ bool setup_ray(const ViewRec& V, const DetC& dc, const GridC& g,
+                                          int r, int c, Ray64& R) {
+    double o[3], th[3];
+    paper_ray(V, dc, r, c, o, th);
+    // index-space frame (P:140-151 / P:416-427 with spacing and centre: reading 2, 13, 14)
+    R.u0[0] = (o[0] - g.x_lo) / g.d[0];
+    R.u0[1] = (g.y_hi - o[1]) / g.d[1];
+    R.u0[2] = (g.z_hi - o[2]) / g.d[2];
+    R.w[0] = th[0] / g.d[0];
+    R.w[1] = -th[1] / g.d[1];
+    R.w[2] = -th[2] / g.d[2];
+    double t_in = -INFINITY, t_out = INFINITY;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        if (R.w[a] == 0.0) {
+            // fixed axis: inside slab c iff c <= u0 < c + 1 (half-open)
+            if (!(R.u0[a] >= 0.0 && R.u0[a] < (double)g.n[a])) return false;
+            R.moving[a] = 0;
+            R.inv_w[a] = 0.0;
+            R.cell[a] = (int)floor(R.u0[a]);
+        } else {
+            R.moving[a] = 1;
+            R.inv_w[a] = 1.0 / R.w[a];
+            const double t0 = (0.0 - R.u0[a]) * R.inv_w[a];
+            const double t1 = ((double)g.n[a] - R.u0[a]) * R.inv_w[a];
+            t_in = fmax(t_in, fmin(t0, t1));
+            t_out = fmin(t_out, fmax(t0, t1));
+        }
+    }
+    if (!(t_out - t_in > g.tau)) return false;
+    R.t_in = t_in;
+    R.t_out = t_out;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        if (!R.moving[a]) continue;
+        const int N = g.n[a];
+        int cc = (int)floor(R.u0[a] + t_in * R.w[a]);
+        cc = cc < 0 ? 0 : (cc > N - 1 ? N - 1 : cc);
+        // make the entry cell consistent with the crossing times T(b) = (b - u0) / w
+        if (R.w[a] > 0.0) {
+            if (cc + 1 <= N - 1 && ((double)(cc + 1) - R.u0[a]) * R.inv_w[a] <= t_in) cc += 1;
+            else if (cc >= 1 && ((double)cc - R.u0[a]) * R.inv_w[a] > t_in) cc -= 1;
+        } else {
+            if (cc >= 1 && ((double)cc - R.u0[a]) * R.inv_w[a] <= t_in) cc -= 1;
+            else if (cc + 1 <= N - 1 && ((double)(cc + 1) - R.u0[a]) * R.inv_w[a] > t_in) cc += 1;
+        }
+        R.cell[a] = cc;
+    }
+    return true;
+}
+
+}  // namespace xrt
+
+// ---------------------------------------------------------------------------------- host side
+struct xrt_plan_s {
+    int device = 0;
+    int beam = 0;
+    int dim = 3;
+    xrt::GridC grid{};
+    xrt::DetC det{};
+    int64_t n_views = 0;
+    int64_t n_rays = 0;
+    int64_t n_units = -1;
+    xrt::ViewRec* d_views = nullptr;   // device [n_views]
+    float* d_work = nullptr;           // device workspace (image-sized)
+    int64_t work_elems = 0;
+    // host-pipeline staging (allocated on first *_host call)
+    float* d_stage_img = nullptr;
+    float* d_stage_sino = nullptr;
+    void* aux_stream = nullptr;
+    int algo_fwd = XRT_ALGO_AUTO;
+    int algo_adj = XRT_ALGO_AUTO;
+    bool column_ok = false;            // geometry admits the column-shared kernels
+    int64_t launches = 0;
+};
+
+namespace xrt {
+// kernels (kern_ray.cu)
+cudaError_t launch_forward_ray(const xrt_plan_s* p, const float* img, float* sino, int64_t ray0,
+                               int64_t ray1, cudaStream_t s);
+cudaError_t launch_adjoint_ray(const xrt_plan_s* p, const float* sino, float* img, int64_t ray0,
+                               int64_t ray1, cudaStream_t s);
+cudaError_t launch_units_count(const xrt_plan_s* p, int64_t ray0, int64_t ray1, int64_t* counts,
+                               cudaStream_t s);
+cudaError_t launch_units_fill(const xrt_plan_s* p, int64_t ray0, int64_t ray1,
+                              const int64_t* row_ptr, int64_t* cols, double* lens, cudaStream_t s);
+}  // namespace xrt

@@ -1,0 +1,161 @@
+"""Thin Python binding of the C ABI (include/xrt.h): same names, argument marshalling only.
+
+Every step of the X-ray transform runs in libxrt.so's CUDA kernels; torch provides
+device memory and streams.  Geometry dicts use the field names of ``xrt_geometry``
+(see ``workloads/configs.py`` for the five BASELINE configurations).
+"""
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._lib import check
+
+
+def _geometry_struct(g: dict) -> tuple[_lib.XrtGeometry, np.ndarray]:
+    angles = np.ascontiguousarray(np.asarray(g["angles"], dtype=np.float64))
+    s = _lib.XrtGeometry()
+    s.beam = _lib.BEAMS[g["beam"]] if isinstance(g["beam"], str) else int(g["beam"])
+    s.reserved0 = 0
+    for a in range(3):
+        s.n[a] = int(g["n"][a])
+        s.spacing[a] = float(g["spacing"][a])
+        s.center[a] = float(g.get("center", (0.0, 0.0, 0.0))[a])
+    s.n_views = int(angles.shape[0])
+    s.angles = angles.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
+    s.det_cols = int(g["det_cols"])
+    s.det_rows = int(g.get("det_rows", 1))
+    for a in range(2):
+        s.det_spacing[a] = float(g["det_spacing"][a])
+        s.det_offset[a] = float(g.get("det_offset", (0.0, 0.0))[a])
+    s.sod = float(g.get("sod", 0.0))
+    s.sdd = float(g.get("sdd", 0.0))
+    s.pitch = float(g.get("pitch", 0.0))
+    s.z0 = float(g.get("z0", 0.0))
+    s.tilt = float(g.get("tilt", 0.0))
+    return s, angles
+
+
+def _stream_handle(stream) -> int:
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return int(stream.cuda_stream)
+
+
+class Plan:
+    """xrt_plan: a validated acquisition geometry with its device tables on one GPU."""
+
+    def __init__(self, geometry: dict, device: int | None = None):
+        lib = _lib.load()
+        if device is None:
+            device = torch.cuda.current_device()
+        self.device = int(device)
+        self.geometry = dict(geometry)
+        s, self._angles = _geometry_struct(geometry)
+        h = ctypes.c_void_p()
+        check(lib.xrt_plan_create(ctypes.byref(s), self.device, ctypes.byref(h)))
+        self._h = h
+        self._lib = lib
+        n = ctypes.c_int64()
+        check(lib.xrt_plan_query(h, ctypes.byref(n), None))
+        self.n_rays = int(n.value)
+        self.n_views = int(s.n_views)
+        self.det_rows, self.det_cols = int(s.det_rows), int(s.det_cols)
+        is2d = s.beam in (0, 1)
+        self.image_shape = (1 if is2d else int(s.n[2]), int(s.n[1]), int(s.n[0]))
+        self.sino_shape = (self.n_views, self.det_rows, self.det_cols)
+
+    # -------------------------------------------------------------- lifetime
+    def close(self):
+        if getattr(self, "_h", None):
+            self._lib.xrt_plan_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # -------------------------------------------------------------- queries
+    @property
+    def n_units(self) -> int:
+        """Exact nnz of the projection matrix (fp64 enumeration; synchronous, cached)."""
+        n = ctypes.c_int64()
+        check(self._lib.xrt_plan_query(self._h, None, ctypes.byref(n)))
+        return int(n.value)
+
+    @property
+    def launch_count(self) -> int:
+        return int(self._lib.xrt_plan_launch_count(self._h))
+
+    def set_algorithm(self, op: str, algo: str) -> None:
+        o = {"forward": _lib.OP_FORWARD, "adjoint": _lib.OP_ADJOINT}[op]
+        check(self._lib.xrt_plan_set_algorithm(self._h, o, _lib.ALGOS[algo]))
+
+    # -------------------------------------------------------------- operators
+    def _check_dev(self, t: torch.Tensor, shape, name):
+        if not (t.is_cuda and t.dtype == torch.float32 and t.is_contiguous()):
+            raise ValueError(f"{name} must be a contiguous float32 CUDA tensor")
+        if t.device.index != self.device:
+            raise ValueError(f"{name} is on cuda:{t.device.index}, plan on cuda:{self.device}")
+        if t.numel() != int(np.prod(shape)):
+            raise ValueError(f"{name} has {t.numel()} elements, expected {shape}")
+
+    def forward(self, img: torch.Tensor, out: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+        """xrt_forward: sino[m] = sum_I img[I] l_I(ray m)."""
+        self._check_dev(img, self.image_shape, "img")
+        if out is None:
+            out = torch.empty(self.sino_shape, dtype=torch.float32, device=img.device)
+        self._check_dev(out, self.sino_shape, "sino")
+        check(self._lib.xrt_forward(self._h, img.data_ptr(), out.data_ptr(), _stream_handle(stream)))
+        return out
+
+    def adjoint(self, sino: torch.Tensor, out: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+        """xrt_adjoint: img[I] = sum_m sino[m] l_I(ray m)."""
+        self._check_dev(sino, self.sino_shape, "sino")
+        if out is None:
+            out = torch.empty(self.image_shape, dtype=torch.float32, device=sino.device)
+        self._check_dev(out, self.image_shape, "img")
+        check(self._lib.xrt_adjoint(self._h, sino.data_ptr(), out.data_ptr(), _stream_handle(stream)))
+        return out
+
+    def forward_host(self, img: torch.Tensor, out: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+        """xrt_forward_host: host (ideally pinned) fp32 buffers, copies inside the call."""
+        if img.is_cuda or img.dtype != torch.float32 or not img.is_contiguous():
+            raise ValueError("img must be a contiguous float32 CPU tensor")
+        if out is None:
+            out = torch.empty(self.sino_shape, dtype=torch.float32, pin_memory=True)
+        check(self._lib.xrt_forward_host(self._h, img.data_ptr(), out.data_ptr(), _stream_handle(stream)))
+        return out
+
+    def adjoint_host(self, sino: torch.Tensor, out: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+        if sino.is_cuda or sino.dtype != torch.float32 or not sino.is_contiguous():
+            raise ValueError("sino must be a contiguous float32 CPU tensor")
+        if out is None:
+            out = torch.empty(self.image_shape, dtype=torch.float32, pin_memory=True)
+        check(self._lib.xrt_adjoint_host(self._h, sino.data_ptr(), out.data_ptr(), _stream_handle(stream)))
+        return out
+
+    def ray_units(self, ray_begin: int, ray_end: int, stream=None):
+        """xrt_ray_units (two-phase): CSR (row_ptr, cols, lens) as CUDA tensors (int64, int64, fp64)."""
+        n = int(ray_end) - int(ray_begin)
+        dev = torch.device("cuda", self.device)
+        row_ptr = torch.empty(max(n, 0) + 1, dtype=torch.int64, device=dev)
+        nnz = ctypes.c_int64()
+        sh = _stream_handle(stream)
+        check(self._lib.xrt_ray_units(self._h, int(ray_begin), int(ray_end), row_ptr.data_ptr(), None, None,
+                                      0, ctypes.byref(nnz), sh))
+        cols = torch.empty(max(nnz.value, 1), dtype=torch.int64, device=dev)
+        lens = torch.empty(max(nnz.value, 1), dtype=torch.float64, device=dev)
+        check(self._lib.xrt_ray_units(self._h, int(ray_begin), int(ray_end), row_ptr.data_ptr(), cols.data_ptr(),
+                                      lens.data_ptr(), cols.numel(), ctypes.byref(nnz), sh))
+        return row_ptr, cols[:nnz.value], lens[:nnz.value]
+
+
+def version() -> tuple[int, int]:
+    v = _lib.load().xrt_version()
+    return v >> 16, v & 0xFFFF

@@ -1,0 +1,248 @@
+"""CUDA path (through the C ABI) vs the fp64 oracle on the same seeded inputs.
+
+Bars (BASELINE.json north_star): per-ray unit index sets from xrt_ray_units bit-exact;
+forward within 1e-5 per ray relative to max|sino|; adjoint within 1e-4 relative L2
+(sparse-y parity); dot-product test to 1e-5.
+"""
+import numpy as np
+import pytest
+import torch
+
+import workloads
+from paper_2006_00686_b200 import Plan, XrtError
+from paper_2006_00686_b200 import _lib
+
+import helpers as H
+
+pytestmark = pytest.mark.gpu
+
+ALGOS = ["ray", "column"]
+
+
+def _plan(c, algo=None):
+    p = Plan(c, device=0)
+    if algo is not None:
+        try:
+            p.set_algorithm("forward", algo)
+            p.set_algorithm("adjoint", algo)
+        except XrtError as e:
+            if e.status == _lib.XRT_ERR_UNSUPPORTED:
+                pytest.skip(f"{algo} does not serve {c['beam']}")
+            raise
+    return p
+
+
+_img_cache = {}
+
+
+def _image(c):
+    key = (c["name"], tuple(c["n"]))
+    if key not in _img_cache:
+        _img_cache[key] = workloads.make_image(c, device="cuda")
+    return _img_cache[key]
+
+
+# ------------------------------------------------------------------- CSR (index sets)
+@pytest.mark.parametrize("idx", [1, 2, 3, 4, 5])
+def test_csr_small_every_ray(cuda_ok, idx):
+    c = H.small_config(idx)
+    p = _plan(c)
+    M = p.n_rays
+    ids = H.ray_ids_all(c)
+    # split into a few calls with ragged boundaries
+    cuts = [0, M // 3 + 7, (2 * M) // 3 + 1, M]
+    for a, b in zip(cuts[:-1], cuts[1:]):
+        gpu = p.ray_units(a, b)
+        ref = H.oracle_csr(c, ids[a:b])
+        H.compare_csr(gpu, ref, f"cfg{idx} rays [{a},{b})")
+
+
+@pytest.mark.parametrize("idx", [1, 2, 3, 4, 5])
+def test_csr_full_size_sampled(cuda_ok, idx):
+    c = workloads.config(idx)
+    p = _plan(c)
+    rng = np.random.Generator(np.random.PCG64(100 + idx))
+    M = p.n_rays
+    n_ranges, width = (4, 64) if idx in (1, 2) else (4, 24)
+    for _ in range(n_ranges):
+        a = int(rng.integers(0, M - width))
+        gpu = p.ray_units(a, a + width)
+        ref = H.oracle_csr(c, np.arange(a, a + width))
+        H.compare_csr(gpu, ref, f"cfg{idx} rays [{a},{a + width})")
+
+
+def test_csr_constructed_rays(cuda_ok):
+    for g, expect in H.constructed_plans():
+        p = _plan(g)
+        gpu = p.ray_units(0, p.n_rays)
+        ref = H.oracle_csr(g, H.ray_ids_all(g))
+        H.compare_csr(gpu, ref, f"constructed phi={g['angles'][0]}")
+        rp = gpu[0].cpu().numpy()
+        for b, n in expect.items():
+            assert rp[b + 1] - rp[b] == n, (g["angles"][0], b, n)
+
+
+def test_n_units_matches_csr(cuda_ok):
+    c = H.small_config(4)
+    p = _plan(c)
+    rp, _, _ = p.ray_units(0, p.n_rays)
+    assert int(rp[-1]) == p.n_units
+
+
+def test_ray_units_edges(cuda_ok):
+    import ctypes
+    c = H.small_config(1)
+    p = _plan(c)
+    rp, cols, lens = p.ray_units(5, 5)
+    assert rp.numel() == 1 and int(rp[0]) == 0 and cols.numel() == 0
+    with pytest.raises(XrtError):
+        p.ray_units(0, p.n_rays + 1)
+    with pytest.raises(XrtError):
+        p.ray_units(10, 3)
+    # capacity error leaves nnz_out set
+    row_ptr = torch.empty(11, dtype=torch.int64, device="cuda")
+    small = torch.empty(3, dtype=torch.int64, device="cuda")
+    smallv = torch.empty(3, dtype=torch.float64, device="cuda")
+    nnz = ctypes.c_int64()
+    st = p._lib.xrt_ray_units(p._h, 4000, 4010, row_ptr.data_ptr(), small.data_ptr(), smallv.data_ptr(), 3,
+                              ctypes.byref(nnz), 0)
+    assert st == _lib.XRT_ERR_CAPACITY and nnz.value > 3
+
+
+# ------------------------------------------------------------------- forward
+@pytest.mark.parametrize("algo", ALGOS)
+@pytest.mark.parametrize("idx", [1, 2, 3, 4, 5])
+def test_forward_small_every_ray(cuda_ok, idx, algo):
+    c = H.small_config(idx)
+    p = _plan(c, algo)
+    img = _image(c)
+    sino = p.forward(img)
+    torch.cuda.synchronize()
+    ref = H.oracle_forward(c, img.cpu(), H.ray_ids_all(c))
+    err = H.fwd_err(sino.cpu().numpy().ravel(), ref)
+    assert err <= H.FWD_TOL, err
+
+
+@pytest.mark.parametrize("algo", ALGOS)
+@pytest.mark.parametrize("idx", [1, 2, 3, 4, 5])
+def test_forward_full_size_sampled(cuda_ok, idx, algo):
+    """Full BASELINE size in the launch configuration bench.py times; sampled rays vs oracle."""
+    c = workloads.config(idx)
+    p = _plan(c, algo)
+    img = _image(c)
+    sino = p.forward(img)
+    torch.cuda.synchronize()
+    n = {1: 8640, 2: 1500, 3: 600, 4: 300, 5: 400}[idx]
+    ids = workloads.sample_rays(c, n, seed=200 + idx)
+    ref = H.oracle_forward(c, img.cpu(), ids)
+    got = sino.reshape(-1)[torch.from_numpy(ids).cuda()].cpu().numpy()
+    # normalise by the max of the full GPU sinogram (the oracle only sees a sample)
+    scale = float(sino.abs().max())
+    err = H.fwd_err(got, ref, scale=scale)
+    assert err <= H.FWD_TOL, err
+
+
+@pytest.mark.parametrize("algo", ALGOS)
+def test_forward_constructed_rays(cuda_ok, algo):
+    img = _image(workloads.config(1))
+    for g, _ in H.constructed_plans():
+        p = _plan(g, "ray" if algo == "column" else algo)
+        sino = p.forward(img)
+        ref = H.oracle_forward(g, img.cpu(), H.ray_ids_all(g))
+        assert H.fwd_err(sino.cpu().numpy().ravel(), ref, scale=64.0) <= H.FWD_TOL
+
+
+@pytest.mark.parametrize("algo", ALGOS)
+def test_forward_deterministic_and_linear(cuda_ok, algo):
+    c = H.small_config(4)
+    p = _plan(c, algo)
+    img = _image(c)
+    a = p.forward(img).clone()
+    b = p.forward(img)
+    assert torch.equal(a, b)
+    z = p.forward(torch.zeros_like(img))
+    assert float(z.abs().max()) == 0.0
+    ones = torch.ones_like(img)
+    ch = p.forward(ones)
+    # constant image: every ray value = chord length through the box (<= box diagonal)
+    ext = np.array(c["n"]) * np.array(c["spacing"])
+    assert float(ch.max()) <= float(np.linalg.norm(ext)) + 1e-3
+
+
+# ------------------------------------------------------------------- adjoint
+@pytest.mark.parametrize("algo", ALGOS)
+@pytest.mark.parametrize("idx", [1, 2, 3, 4, 5])
+def test_adjoint_small_sparse_parity(cuda_ok, idx, algo):
+    c = H.small_config(idx)
+    p = _plan(c, algo)
+    M = p.n_rays
+    ids = workloads.sample_rays(c, min(M, 3000), seed=300 + idx)
+    y = np.zeros(M, dtype=np.float32)
+    rng = np.random.Generator(np.random.PCG64(400 + idx))
+    y[ids] = rng.uniform(-1, 1, size=ids.size).astype(np.float32)
+    sino = torch.from_numpy(y).reshape(p.sino_shape).cuda()
+    img = p.adjoint(sino)
+    ref = H.oracle_adjoint(c, y[ids].astype(np.float64), ids)
+    err = H.rel_l2(img.cpu().numpy().ravel(), ref)
+    assert err <= H.ADJ_TOL, err
+
+
+@pytest.mark.parametrize("algo", ALGOS)
+@pytest.mark.parametrize("idx", [2, 4, 5])
+def test_adjoint_full_size_sparse_parity(cuda_ok, idx, algo):
+    c = workloads.config(idx)
+    p = _plan(c, algo)
+    ids = workloads.sample_rays(c, {2: 800, 4: 120, 5: 200}[idx], seed=500 + idx)
+    y = torch.zeros(p.n_rays, dtype=torch.float32, device="cuda")
+    rng = np.random.Generator(np.random.PCG64(600 + idx))
+    yv = rng.uniform(-1, 1, size=ids.size).astype(np.float32)
+    y[torch.from_numpy(ids).cuda()] = torch.from_numpy(yv).cuda()
+    img = p.adjoint(y.reshape(p.sino_shape))
+    ref = H.oracle_adjoint(c, yv.astype(np.float64), ids)
+    err = H.rel_l2(img.cpu().numpy().ravel(), ref)
+    assert err <= H.ADJ_TOL, err
+
+
+@pytest.mark.parametrize("algo", ALGOS)
+@pytest.mark.parametrize("idx", [1, 2, 3, 4, 5])
+def test_dot_product(cuda_ok, idx, algo):
+    c = H.small_config(idx) if idx in (3, 4, 5) else workloads.config(idx)
+    p = _plan(c, algo)
+    x = _image(c)
+    y = workloads.make_sino_input(c, device="cuda")
+    Ax = p.forward(x)
+    Aty = p.adjoint(y)
+    lhs = float((Ax.double() * y.double()).sum())
+    rhs = float((x.double() * Aty.double()).sum())
+    scale = float(Ax.double().norm() * y.double().norm() + x.double().norm() * Aty.double().norm())
+    assert abs(lhs - rhs) <= H.DOT_TOL * scale, (lhs, rhs)
+
+
+# ------------------------------------------------------------------- host-buffer path
+def test_host_path_matches_device(cuda_ok):
+    c = H.small_config(5)
+    p = _plan(c)
+    img = _image(c)
+    dev = p.forward(img)
+    host = p.forward_host(img.cpu().contiguous())
+    assert torch.equal(dev.cpu(), host)
+    y = workloads.make_sino_input(c)
+    a_dev = p.adjoint(y.cuda())
+    a_host = p.adjoint_host(y.contiguous())
+    assert H.rel_l2(a_host.numpy(), a_dev.cpu().numpy()) < 1e-6
+
+
+def test_algorithms_agree(cuda_ok):
+    """RAY and COLUMN enumerate the same units: forward results agree to fp32 rounding."""
+    for idx in (3, 4, 5):
+        c = H.small_config(idx)
+        p = _plan(c)
+        img = _image(c)
+        p.set_algorithm("forward", "ray")
+        a = p.forward(img).clone()
+        try:
+            p.set_algorithm("forward", "column")
+        except XrtError:
+            pytest.skip("column not built")
+        b = p.forward(img)
+        assert H.fwd_err(b.cpu().numpy(), a.cpu().numpy()) < 2e-6
