@@ -112,6 +112,45 @@ xrt::ViewRec view_record(const xrt_geometry* g, double ang) {
     return r;
 }
 
+// z padding (per side) of the column kernels' z-fastest volume: every ray's u_z over the
+// in-plane chord stays inside [-pad, N_z + pad).  Bound: |z| <= |z0| + R tan(beta) with R the
+// largest distance of an image-square point from the z axis (|sigma_abs| <= R).
+int64_t column_zpad(const xrt_geometry* g, const xrt::GridC& G) {
+    const double hx = G.n[0] * G.d[0] / 2 + std::fabs(g->center[0]);
+    const double hy = G.n[1] * G.d[1] / 2 + std::fabs(g->center[1]);
+    const double R = std::sqrt(hx * hx + hy * hy);
+    const double v0 = (0 - (g->det_rows - 1) / 2.0) * g->det_spacing[1] + g->det_offset[1];
+    const double v1 = ((g->det_rows - 1) - (g->det_rows - 1) / 2.0) * g->det_spacing[1] + g->det_offset[1];
+    const double vmax = std::max(std::fabs(v0), std::fabs(v1));
+    double zmax;
+    if (g->beam == XRT_PAR3D) {
+        const double c2 = std::cos(g->tilt), t2 = std::fabs(std::tan(g->tilt));
+        zmax = vmax / c2 + R * t2;
+    } else {
+        const double hmax = vmax * g->sod / g->sdd;
+        double Hmax = 0.0;
+        if (g->beam == XRT_HELICAL)
+            for (int64_t v = 0; v < g->n_views; ++v)
+                Hmax = std::max(Hmax, std::fabs(g->z0 + g->pitch * g->angles[v] / (2.0 * M_PI)));
+        zmax = hmax + Hmax + R * hmax / g->sod;
+    }
+    const double half = G.n[2] * G.d[2] / 2;
+    const double over = (zmax + std::fabs(g->center[2]) - half) / G.d[2];
+    int64_t pad = over > 0 ? (int64_t)std::ceil(over) : 0;
+    return pad + 4;
+}
+
+// The column kernels split an in-plane segment at no more than one z plane: need
+// max segment length (the in-plane unit diagonal) * max |d u_z / d sigma| < 1.
+bool column_single_crossing(const xrt_geometry* g, const xrt::GridC& G) {
+    const double v0 = (0 - (g->det_rows - 1) / 2.0) * g->det_spacing[1] + g->det_offset[1];
+    const double v1 = ((g->det_rows - 1) - (g->det_rows - 1) / 2.0) * g->det_spacing[1] + g->det_offset[1];
+    const double vmax = std::max(std::fabs(v0), std::fabs(v1));
+    const double tanb = g->beam == XRT_PAR3D ? std::fabs(std::tan(g->tilt)) : vmax * g->sod / g->sdd / g->sod;
+    const double diag = std::sqrt(G.d[0] * G.d[0] + G.d[1] * G.d[1]);
+    return diag * tanb / G.d[2] < 0.999;
+}
+
 xrt_status alloc_stage(xrt_plan p) {
     if (!p->d_stage_img) XRT_CUDA(cudaMalloc(&p->d_stage_img, sizeof(float) * (size_t)p->grid.nxyz));
     if (!p->d_stage_sino) XRT_CUDA(cudaMalloc(&p->d_stage_sino, sizeof(float) * (size_t)p->n_rays));
@@ -128,6 +167,16 @@ int resolve(int want, bool column_ok) {
     return want;
 }
 
+// Forward over views [v0, v1).  COLUMN reads the plan's z-fastest copy of the image, which
+// fwd_prepare() builds once per call (img -> work_fwd transpose).
+xrt_status fwd_prepare(xrt_plan p, const float* img, cudaStream_t s) {
+    if (resolve(p->algo_fwd, p->column_ok) != XRT_ALGO_COLUMN) return XRT_OK;
+    cudaError_t e = xrt::launch_to_zfast(p, img, p->d_work_fwd, s);
+    p->launches += 1;
+    if (e != cudaSuccess) return cuda_fail(e, "transpose launch");
+    return XRT_OK;
+}
+
 xrt_status forward_range(xrt_plan p, const float* img, float* sino, int64_t v0, int64_t v1,
                          cudaStream_t s) {
     const int64_t pv = p->det.per_view;
@@ -135,11 +184,22 @@ xrt_status forward_range(xrt_plan p, const float* img, float* sino, int64_t v0, 
     cudaError_t e = cudaSuccess;
     if (algo == XRT_ALGO_RAY) {
         e = xrt::launch_forward_ray(p, img, sino, v0 * pv, v1 * pv, s);
-        p->launches += 1;
+    } else if (algo == XRT_ALGO_COLUMN) {
+        e = xrt::launch_forward_column(p, p->d_work_fwd, sino, v0, v1, s);
     } else {
         return fail(XRT_ERR_UNSUPPORTED, "forward algorithm %d not built", algo);
     }
+    p->launches += 1;
     if (e != cudaSuccess) return cuda_fail(e, "forward launch");
+    return XRT_OK;
+}
+
+// Adjoint: adj_begin() clears the accumulator, adjoint_range() adds views [v0, v1),
+// adj_finish() writes the caller's image (COLUMN: work_adj -> img transpose).
+xrt_status adj_begin(xrt_plan p, float* img, cudaStream_t s) {
+    const bool col = resolve(p->algo_adj, p->column_ok) == XRT_ALGO_COLUMN;
+    if (col) XRT_CUDA(cudaMemsetAsync(p->d_work_adj, 0, sizeof(float) * (size_t)(p->grid.nxy * p->nzp), s));
+    else XRT_CUDA(cudaMemsetAsync(img, 0, sizeof(float) * (size_t)p->grid.nxyz, s));
     return XRT_OK;
 }
 
@@ -150,11 +210,21 @@ xrt_status adjoint_range(xrt_plan p, const float* sino, float* img, int64_t v0, 
     cudaError_t e = cudaSuccess;
     if (algo == XRT_ALGO_RAY) {
         e = xrt::launch_adjoint_ray(p, sino, img, v0 * pv, v1 * pv, s);
-        p->launches += 1;
+    } else if (algo == XRT_ALGO_COLUMN) {
+        e = xrt::launch_adjoint_column(p, sino, p->d_work_adj, v0, v1, s);
     } else {
         return fail(XRT_ERR_UNSUPPORTED, "adjoint algorithm %d not built", algo);
     }
+    p->launches += 1;
     if (e != cudaSuccess) return cuda_fail(e, "adjoint launch");
+    return XRT_OK;
+}
+
+xrt_status adj_finish(xrt_plan p, float* img, cudaStream_t s) {
+    if (resolve(p->algo_adj, p->column_ok) != XRT_ALGO_COLUMN) return XRT_OK;
+    cudaError_t e = xrt::launch_from_zfast(p, p->d_work_adj, img, s);
+    p->launches += 1;
+    if (e != cudaSuccess) return cuda_fail(e, "transpose launch");
     return XRT_OK;
 }
 
@@ -247,7 +317,20 @@ xrt_status xrt_plan_create(const xrt_geometry* g, int cuda_device, xrt_plan* out
         xrt_plan_destroy(p);
         return cuda_fail(e, "plan tables");
     }
-    p->column_ok = false;
+    p->column_ok = (g->beam == XRT_PAR3D || g->beam == XRT_CONE || g->beam == XRT_HELICAL) &&
+                   column_single_crossing(g, G);
+    if (p->column_ok) {
+        p->zpad = column_zpad(g, G);
+        p->nzp = G.n[2] + 2 * p->zpad;
+        const size_t bytes = sizeof(float) * (size_t)(G.nxy * p->nzp);
+        e = cudaMalloc(&p->d_work_fwd, bytes);
+        if (e == cudaSuccess) e = cudaMalloc(&p->d_work_adj, bytes);
+        if (e == cudaSuccess) e = cudaMemset(p->d_work_fwd, 0, bytes);  // zero padding stays zero
+        if (e != cudaSuccess) {
+            xrt_plan_destroy(p);
+            return cuda_fail(e, "plan workspace");
+        }
+    }
     *out = p;
     return XRT_OK;
 }
@@ -256,7 +339,8 @@ xrt_status xrt_plan_destroy(xrt_plan p) {
     if (!p) return XRT_OK;
     DevGuard guard(p->device);
     cudaFree(p->d_views);
-    cudaFree(p->d_work);
+    cudaFree(p->d_work_fwd);
+    cudaFree(p->d_work_adj);
     cudaFree(p->d_stage_img);
     cudaFree(p->d_stage_sino);
     if (p->aux_stream) cudaStreamDestroy((cudaStream_t)p->aux_stream);
@@ -293,15 +377,20 @@ int64_t xrt_plan_launch_count(xrt_plan p) { return p ? p->launches : -1; }
 xrt_status xrt_forward(xrt_plan p, const float* img, float* sino, void* cuda_stream) {
     if (!p || !img || !sino) return fail(XRT_ERR_INVALID_ARG, "NULL argument");
     DevGuard guard(p->device);
-    return forward_range(p, img, sino, 0, p->n_views, (cudaStream_t)cuda_stream);
+    cudaStream_t s = (cudaStream_t)cuda_stream;
+    xrt_status st = fwd_prepare(p, img, s);
+    if (st != XRT_OK) return st;
+    return forward_range(p, img, sino, 0, p->n_views, s);
 }
 
 xrt_status xrt_adjoint(xrt_plan p, const float* sino, float* img, void* cuda_stream) {
     if (!p || !img || !sino) return fail(XRT_ERR_INVALID_ARG, "NULL argument");
     DevGuard guard(p->device);
     cudaStream_t s = (cudaStream_t)cuda_stream;
-    XRT_CUDA(cudaMemsetAsync(img, 0, sizeof(float) * (size_t)p->grid.nxyz, s));
-    return adjoint_range(p, sino, img, 0, p->n_views, s);
+    xrt_status st = adj_begin(p, img, s);
+    if (st == XRT_OK) st = adjoint_range(p, sino, img, 0, p->n_views, s);
+    if (st == XRT_OK) st = adj_finish(p, img, s);
+    return st;
 }
 
 // Host-buffer forward: H2D(image) -> per view chunk: kernel, then D2H of that chunk on the aux
@@ -314,6 +403,8 @@ xrt_status xrt_forward_host(xrt_plan p, const float* img_host, float* sino_host,
     cudaStream_t s = (cudaStream_t)cuda_stream, a = (cudaStream_t)p->aux_stream;
     XRT_CUDA(cudaMemcpyAsync(p->d_stage_img, img_host, sizeof(float) * (size_t)p->grid.nxyz,
                              cudaMemcpyHostToDevice, s));
+    st = fwd_prepare(p, p->d_stage_img, s);
+    if (st != XRT_OK) return st;
     const int64_t nchunk = std::min<int64_t>(8, p->n_views);
     const int64_t pv = p->det.per_view;
     std::vector<cudaEvent_t> ev((size_t)nchunk);
@@ -346,7 +437,8 @@ xrt_status xrt_adjoint_host(xrt_plan p, const float* sino_host, float* img_host,
     xrt_status st = alloc_stage(p);
     if (st != XRT_OK) return st;
     cudaStream_t s = (cudaStream_t)cuda_stream, a = (cudaStream_t)p->aux_stream;
-    XRT_CUDA(cudaMemsetAsync(p->d_stage_img, 0, sizeof(float) * (size_t)p->grid.nxyz, s));
+    st = adj_begin(p, p->d_stage_img, s);
+    if (st != XRT_OK) return st;
     const int64_t nchunk = std::min<int64_t>(8, p->n_views);
     const int64_t pv = p->det.per_view;
     std::vector<cudaEvent_t> ev((size_t)nchunk);
@@ -361,6 +453,7 @@ xrt_status xrt_adjoint_host(xrt_plan p, const float* sino_host, float* img_host,
         if (e != cudaSuccess) { st = cuda_fail(e, "adjoint_host pipeline"); break; }
         st = adjoint_range(p, p->d_stage_sino, p->d_stage_img, v0, v1, s);
     }
+    if (st == XRT_OK) st = adj_finish(p, p->d_stage_img, s);
     if (st == XRT_OK) {
         cudaError_t e = cudaMemcpyAsync(img_host, p->d_stage_img, sizeof(float) * (size_t)p->grid.nxyz,
                                         cudaMemcpyDeviceToHost, s);

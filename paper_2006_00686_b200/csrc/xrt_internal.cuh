@@ -183,8 +183,9 @@ struct xrt_plan_s {
     int64_t n_rays = 0;
     int64_t n_units = -1;
     xrt::ViewRec* d_views = nullptr;   // device [n_views]
-    float* d_work = nullptr;           // device workspace (image-sized)
-    int64_t work_elems = 0;
+    float* d_work_fwd = nullptr;       // z-fastest, z-padded copy of the forward input (COLUMN)
+    float* d_work_adj = nullptr;       // z-fastest, z-padded adjoint accumulator (COLUMN)
+    int64_t zpad = 0, nzp = 0;         // z padding per side and padded column length
     // host-pipeline staging (allocated on first *_host call)
     float* d_stage_img = nullptr;
     float* d_stage_sino = nullptr;
@@ -205,4 +206,11 @@ cudaError_t launch_units_count(const xrt_plan_s* p, int64_t ray0, int64_t ray1, 
                                cudaStream_t s);
 cudaError_t launch_units_fill(const xrt_plan_s* p, int64_t ray0, int64_t ray1,
                               const int64_t* row_ptr, int64_t* cols, double* lens, cudaStream_t s);
+// kernels (kern_column.cu)
+cudaError_t launch_to_zfast(const xrt_plan_s* p, const float* img, float* work, cudaStream_t s);
+cudaError_t launch_from_zfast(const xrt_plan_s* p, const float* work, float* img, cudaStream_t s);
+cudaError_t launch_forward_column(const xrt_plan_s* p, const float* vol_zfast, float* sino,
+                                  int64_t v0, int64_t v1, cudaStream_t s);
+cudaError_t launch_adjoint_column(const xrt_plan_s* p, const float* sino, float* vol_zfast,
+                                  int64_t v0, int64_t v1, cudaStream_t s);
 }  // namespace xrt
