@@ -104,15 +104,6 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.rows)}
 
 
-def shard_views(c: dict, rank: int, world: int) -> dict:
-    """Contiguous block of views for this rank; helical z0/pitch are angle based."""
-    V = c["n_views"]
-    v0, v1 = V * rank // world, V * (rank + 1) // world
-    s = dict(c)
-    s["angles"] = np.asarray(c["angles"])[v0:v1]
-    s["n_views"] = v1 - v0
-    s["view_range"] = (v0, v1)
-    return s
 
 
 def cpu_baseline(c: dict, budget_s: float = 12.0):

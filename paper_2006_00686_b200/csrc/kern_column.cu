@@ -34,6 +34,8 @@
 // thin annulus |s1| ~ const of the image -- a small, L2-resident working set reused by every view.
 #include <cuda_runtime.h>
 
+#include <cstdlib>
+
 #include "xrt_internal.cuh"
 
 namespace xrt {
@@ -62,6 +64,8 @@ struct ColumnPath {
     int cell_a0, step_a;   // major cell of slice 0 and its step (+-1)
     int cell_b0, step_b;   // minor cell at the entry and its step
     int nb_face;      // number of interior minor crossings
+    float idtb;       // 1 / dtb (estimate only; decisions use the fmaf crossing values)
+    int sa, sb;       // flat xy strides of the major / minor axis
     double sig_in;    // absolute sigma of the square entry (fp64)
 };
 
@@ -171,6 +175,9 @@ __device__ __forceinline__ void column_path(const ViewRec& V, const DetC& dc, co
     }
     P.cell_b0 = cellb;
     P.L = L;
+    P.idtb = P.step_b != 0 ? 1.f / P.dtb : 0.f;
+    P.sa = a == 0 ? 1 : g.n[0];
+    P.sb = a == 0 ? g.n[0] : 1;
     // slices = 1 + number of major crossings strictly inside (0, L)
     const float est = (L - P.t0a) / P.dta;
     int m = est < 0.f ? 0 : (est > (float)ma_face ? ma_face : (int)est);
@@ -185,38 +192,32 @@ __device__ __forceinline__ float slice_start(const ColumnPath& P, int n) {
 }
 
 // Segments of major slice n: 1 or 2 in-plane units (cell, sigma_start, sigma_end).  The minor
-// crossings before the slice are counted against the SAME fmaf expression the neighbouring
-// slices use, so every crossing value is produced exactly once (telescoping).
-__device__ __forceinline__ int slice_segments(const ColumnPath& P, int n, int nx, float& s0,
-                                              float& s1, float& s2, int& c0, int& c1) {
-    const float t_lo = slice_start(P, n);
-    const float t_hi = slice_start(P, n + 1);
+// crossings at or before the slice start are counted against the SAME fmaf expression the
+// neighbouring slices use, so every crossing value is produced exactly once (telescoping).
+__device__ __forceinline__ int slice_segments(const ColumnPath& P, int n, float& s0, float& s1,
+                                              float& s2, int& c0, int& c1) {
+    const float t_lo = n == 0 ? 0.f : fminf(fmaf((float)(n - 1), P.dta, P.t0a), P.L);
+    const float t_hi = n + 1 >= P.n_slices ? P.L : fminf(fmaf((float)n, P.dta, P.t0a), P.L);
     const int ca = P.cell_a0 + P.step_a * n;
-    int mb = 0;  // minor crossings at or before t_lo
+    int mb = 0;
+    bool split = false;
+    float tb = 0.f;
     if (P.step_b != 0) {
-        const float est = (t_lo - P.t0b) / P.dtb;
-        int m = est < 0.f ? 0 : (est > (float)P.nb_face ? P.nb_face : (int)est);
-        while (m < P.nb_face && fmaf((float)m, P.dtb, P.t0b) <= t_lo) ++m;
-        while (m > 0 && fmaf((float)(m - 1), P.dtb, P.t0b) > t_lo) --m;
+        // estimate (exact up to one step), then one fix-up step each way
+        int m = __float2int_rd((t_lo - P.t0b) * P.idtb) + 1;
+        m = max(0, min(m, P.nb_face));
+        if (m < P.nb_face && fmaf((float)m, P.dtb, P.t0b) <= t_lo) ++m;
+        if (m > 0 && fmaf((float)(m - 1), P.dtb, P.t0b) > t_lo) --m;
         mb = m;
+        tb = fmaf((float)m, P.dtb, P.t0b);
+        split = m < P.nb_face && tb < t_hi;
     }
-    const int cb = P.cell_b0 + P.step_b * mb;
-    const int sa = P.a == 0 ? 1 : nx;   // flat xy stride of the major axis
-    const int sb = P.a == 0 ? nx : 1;   // ... and of the minor axis
-    c0 = ca * sa + cb * sb;
+    c0 = ca * P.sa + (P.cell_b0 + P.step_b * mb) * P.sb;
     s0 = t_lo;
     s2 = t_hi;
-    if (P.step_b != 0 && mb < P.nb_face) {
-        const float tb = fmaf((float)mb, P.dtb, P.t0b);
-        if (tb < t_hi) {
-            s1 = tb;
-            c1 = c0 + P.step_b * sb;
-            return 2;
-        }
-    }
-    s1 = t_hi;
-    c1 = c0;
-    return 1;
+    s1 = split ? tb : t_hi;
+    c1 = split ? c0 + P.step_b * P.sb : c0;
+    return split ? 2 : 1;
 }
 
 // Per-ray z description along the shared path (sigma from the square entry).
@@ -275,13 +276,29 @@ __global__ void __launch_bounds__(kWarps * 32, 3) k_column(const ViewRec* __rest
                                                          float* __restrict__ volw,
                                                          const float* __restrict__ sino_in,
                                                          float* __restrict__ sino_out, int view0,
-                                                         int nzp, int pad) {
+                                                         int n_views, int n_cgroups, int nzp, int pad,
+                                                         int order) {
     __shared__ Seg s_seg[kWarps][kSegCap];
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
-    const int c = blockIdx.y * kColsPerCta + (warp % kColsPerCta);
-    const int r = (blockIdx.z * kRowWarps + warp / kColsPerCta) * 32 + lane;
-    const int v = view0 + blockIdx.x;
+    // 1D grid; order 0: id = (band * n_cgroups + cgroup) * n_views + view (views fastest)
+    //          order 1: id = (band * n_views + view) * n_cgroups + cgroup (columns fastest)
+    const unsigned bid = blockIdx.x;
+    int vv, cg, band;
+    if (order == 0) {
+        vv = (int)(bid % (unsigned)n_views);
+        const unsigned rest = bid / (unsigned)n_views;
+        cg = (int)(rest % (unsigned)n_cgroups);
+        band = (int)(rest / (unsigned)n_cgroups);
+    } else {
+        cg = (int)(bid % (unsigned)n_cgroups);
+        const unsigned rest = bid / (unsigned)n_cgroups;
+        vv = (int)(rest % (unsigned)n_views);
+        band = (int)(rest / (unsigned)n_views);
+    }
+    const int c = cg * kColsPerCta + (warp % kColsPerCta);
+    const int r = (band * kRowWarps + warp / kColsPerCta) * 32 + lane;
+    const int v = view0 + vv;
     if (c >= dc.cols) return;  // warp-uniform
     const ViewRec V = views[v];
     ColumnPath P;
@@ -298,6 +315,7 @@ __global__ void __launch_bounds__(kWarps * 32, 3) k_column(const ViewRec* __rest
     const unsigned long long base = (unsigned long long)(kAdjoint ? (const float*)volw : vol);
     const unsigned long long cstride = 4ull * (unsigned long long)nzp;
     unsigned kp = (unsigned)Z.kp;
+    (void)0;
     float tz = Z.t0z, mz = 0.f;
     if (__any_sync(0xffffffffu, live)) {
         for (int n0 = 0; n0 < P.n_slices; n0 += kSlices) {
@@ -308,7 +326,7 @@ __global__ void __launch_bounds__(kWarps * 32, 3) k_column(const ViewRec* __rest
                 const int n = n0 + half * 32 + lane;
                 float a0 = 0.f, a1 = 0.f, a2 = 0.f;
                 int c0 = 0, c1 = 0, cnt = 0;
-                if (n < P.n_slices) cnt = slice_segments(P, n, g.n[0], a0, a1, a2, c0, c1);
+                if (n < P.n_slices) cnt = slice_segments(P, n, a0, a1, a2, c0, c1);
                 int incl = cnt;
 #pragma unroll
                 for (int o = 1; o < 32; o <<= 1) {
@@ -331,25 +349,29 @@ __global__ void __launch_bounds__(kWarps * 32, 3) k_column(const ViewRec* __rest
                 // ---- units of each segment: cell k_s, and k_s + dk after the z crossing tz
 #pragma unroll 4
                 for (int s = 0; s < total; ++s) {
-                    const Seg q = seg[s];
+                    const uint4 raw = *reinterpret_cast<const uint4*>(&seg[s]);
+                    Seg q;
+                    q.ptr = ((unsigned long long)raw.y << 32) | raw.x;
+                    q.se = __uint_as_float(raw.z);
+                    q.ds = __uint_as_float(raw.w);
                     const bool cross = tz < q.se;
                     const float l_e = fmaxf(q.se - tz, 0.f);         // C_up - C_low, cell k_e
                     const float l_s = q.ds - l_e;                    // C_up - C_low, cell k_s
-                    const unsigned ke = cross ? kp + Z.dk : kp;
-                    float* a_s = (float*)(q.ptr + 4ull * kp);
-                    float* a_e = (float*)(q.ptr + 4ull * ke);
                     if (kAdjoint) {
-                        atomicAdd(a_s, y * l_s);
-                        if (cross) atomicAdd(a_e, y * l_e);
+                        atomicAdd((float*)(q.ptr + 4ull * kp), y * l_s);
                     } else {
-                        acc_s = fmaf(__ldg(a_s), l_s, acc_s);
-                        acc_e = fmaf(__ldg(a_e), l_e, acc_e);
+                        acc_s = fmaf(__ldg((const float*)(q.ptr + 4ull * kp)), l_s, acc_s);
                     }
                     if (cross) {
+                        kp += Z.dk;
+                        if (kAdjoint) {
+                            atomicAdd((float*)(q.ptr + 4ull * kp), y * l_e);
+                        } else {
+                            acc_e = fmaf(__ldg((const float*)(q.ptr + 4ull * kp)), l_e, acc_e);
+                        }
                         mz += 1.f;
                         tz = fmaf(mz, Z.dtz, Z.t0z);
                     }
-                    kp = ke;
                 }
             }
             __syncwarp();
@@ -388,6 +410,14 @@ inline cudaError_t transpose(const float* in, float* out, int64_t rows, int64_t 
     return cudaGetLastError();
 }
 
+int column_order() {
+    static int o = [] {
+        const char* e = getenv("XRT_COLUMN_ORDER");
+        return e ? atoi(e) : 1;
+    }();
+    return o;
+}
+
 }  // namespace
 
 // image [N_z][N_xy] -> padded z-fastest work [N_xy][NzP] (interior rows pad .. pad + N_z)
@@ -404,10 +434,12 @@ cudaError_t launch_forward_column(const xrt_plan_s* p, const float* vol_zfast, f
                                   int64_t v0, int64_t v1, cudaStream_t s) {
     if (v1 <= v0) return cudaSuccess;
     const int rows_per_cta = kRowWarps * 32;
-    dim3 grid((unsigned)(v1 - v0), (unsigned)((p->det.cols + kColsPerCta - 1) / kColsPerCta),
-              (unsigned)((p->det.rows + rows_per_cta - 1) / rows_per_cta));
-    k_column<false><<<grid, kWarps * 32, 0, s>>>(p->d_views, p->det, p->grid, vol_zfast, nullptr,
-                                                nullptr, sino, (int)v0, (int)p->nzp, (int)p->zpad);
+    const int ncg = (p->det.cols + kColsPerCta - 1) / kColsPerCta;
+    const int nband = (p->det.rows + rows_per_cta - 1) / rows_per_cta;
+    const unsigned nblk = (unsigned)((v1 - v0) * ncg * nband);
+    k_column<false><<<nblk, kWarps * 32, 0, s>>>(p->d_views, p->det, p->grid, vol_zfast, nullptr,
+                                                nullptr, sino, (int)v0,
+        (int)(v1 - v0), ncg, (int)p->nzp, (int)p->zpad, column_order());
     return cudaGetLastError();
 }
 
@@ -415,10 +447,12 @@ cudaError_t launch_adjoint_column(const xrt_plan_s* p, const float* sino, float*
                                   int64_t v0, int64_t v1, cudaStream_t s) {
     if (v1 <= v0) return cudaSuccess;
     const int rows_per_cta = kRowWarps * 32;
-    dim3 grid((unsigned)(v1 - v0), (unsigned)((p->det.cols + kColsPerCta - 1) / kColsPerCta),
-              (unsigned)((p->det.rows + rows_per_cta - 1) / rows_per_cta));
-    k_column<true><<<grid, kWarps * 32, 0, s>>>(p->d_views, p->det, p->grid, nullptr, vol_zfast,
-                                               sino, nullptr, (int)v0, (int)p->nzp, (int)p->zpad);
+    const int ncg = (p->det.cols + kColsPerCta - 1) / kColsPerCta;
+    const int nband = (p->det.rows + rows_per_cta - 1) / rows_per_cta;
+    const unsigned nblk = (unsigned)((v1 - v0) * ncg * nband);
+    k_column<true><<<nblk, kWarps * 32, 0, s>>>(p->d_views, p->det, p->grid, nullptr, vol_zfast,
+                                               sino, nullptr, (int)v0,
+        (int)(v1 - v0), ncg, (int)p->nzp, (int)p->zpad, column_order());
     return cudaGetLastError();
 }
 

@@ -43,7 +43,7 @@ class ShardedPlan:
     """A plan over this rank's view block plus the collectives that make it the full operator."""
 
     def __init__(self, geometry: dict, rank: int | None = None, world: int | None = None,
-                 device: int | None = None, group=None):
+                 device: int | None = None, group=None, plan_factory=None):
         if rank is None:
             rank = dist.get_rank(group) if dist.is_initialized() else 0
         if world is None:
@@ -51,8 +51,10 @@ class ShardedPlan:
         self.rank, self.world, self.group = rank, world, group
         self.geometry = shard_geometry(geometry, rank, world)
         self.view_block = self.geometry["view_block"]
-        from .plan import Plan  # local import: the sharding logic is testable without the library
-        self.plan = Plan(self.geometry, device=device)
+        if plan_factory is None:
+            from .plan import Plan  # local import: the sharding logic is testable without the library
+            plan_factory = Plan
+        self.plan = plan_factory(self.geometry, device=device)
 
     def forward(self, img: torch.Tensor, out: torch.Tensor | None = None, broadcast_src: int | None = None):
         """This rank's sinogram slab [views in block][rows][cols] of A img."""
