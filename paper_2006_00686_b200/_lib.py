@@ -49,9 +49,11 @@ _lock = threading.Lock()
 _lib = None
 
 
-def load(path: str = LIB_PATH) -> ctypes.CDLL:
-    """Load libxrt.so (no fallback: raises if absent)."""
+def load(path: str | None = None) -> ctypes.CDLL:
+    """Load libxrt.so (no fallback: raises if absent).  XRT_LIB overrides the path (A/B builds)."""
     global _lib
+    if path is None:
+        path = os.environ.get("XRT_LIB", LIB_PATH)
     with _lock:
         if _lib is not None:
             return _lib

@@ -8,6 +8,7 @@
 #include <cub/device/device_segmented_sort.cuh>
 
 #include <climits>
+#include <cstdlib>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -107,6 +108,8 @@ xrt::ViewRec view_record(const xrt_geometry* g, double ang) {
     if (g->beam == XRT_PAR3D) {
         r.c2 = std::cos(g->tilt);
         r.s2 = std::sin(g->tilt);
+        r.pad[0] = r.s2 / r.c2;
+        r.pad[1] = 1.0 / r.c2;
     }
     if (g->beam == XRT_HELICAL) r.H = g->z0 + g->pitch * ang / (2.0 * M_PI);  // reading 11
     return r;
@@ -291,12 +294,14 @@ xrt_status xrt_plan_create(const xrt_geometry* g, int cuda_device, xrt_plan* out
     G.y_hi = g->center[1] + G.n[1] * G.d[1] / 2.0;
     G.z_hi = cz + G.n[2] * G.d[2] / 2.0;
     G.tau = 1e-9 * std::min(G.d[0], std::min(G.d[1], is2d ? G.d[0] : G.d[2]));
+    G.inv_dz = 1.0 / G.d[2];
     G.nxy = (int64_t)G.n[0] * G.n[1];
     G.nxyz = G.nxy * G.n[2];
     xrt::DetC& D = p->det;
     D.beam = g->beam;
     D.D = g->sod;
     D.sdd = g->sdd;
+    D.inv_D = g->sod > 0 ? 1.0 / g->sod : 0.0;
     D.cols = (int)g->det_cols;
     D.rows = (int)g->det_rows;
     D.du = g->det_spacing[0];
@@ -326,6 +331,29 @@ xrt_status xrt_plan_create(const xrt_geometry* g, int cuda_device, xrt_plan* out
         e = cudaMalloc(&p->d_work_fwd, bytes);
         if (e == cudaSuccess) e = cudaMalloc(&p->d_work_adj, bytes);
         if (e == cudaSuccess) e = cudaMemset(p->d_work_fwd, 0, bytes);  // zero padding stays zero
+        if (e == cudaSuccess)
+            e = cudaMalloc(&p->d_coldesc, xrt::column_desc_bytes() * (size_t)(p->n_views * D.cols));
+        if (e == cudaSuccess) e = xrt::launch_col_desc(p, (cudaStream_t)0);
+        if (e == cudaSuccess) e = cudaDeviceSynchronize();
+        // xy tiling: largest power-of-two tile whose z-fastest columns fit the L2 budget
+        const double budget = 64.0 * 1024 * 1024;
+        int ts = 32;
+        while ((double)(2 * ts) * (2 * ts) * (double)p->nzp * 4.0 <= budget) ts *= 2;
+        if (const char* f = std::getenv("XRT_COLUMN_TILE")) ts = std::max(4, std::atoi(f));  // testing
+        if (ts >= std::max(G.n[0], G.n[1])) {
+            p->tile = std::max(G.n[0], G.n[1]);
+            p->n_tx = p->n_ty = 1;
+        } else {
+            p->tile = ts;
+            p->n_tx = (G.n[0] + ts - 1) / ts;
+            p->n_ty = (G.n[1] + ts - 1) / ts;
+            std::vector<uint2> items;
+            xrt::build_column_items(p, views.data(), items);
+            p->n_items = (int64_t)items.size();
+            if (e == cudaSuccess && !items.empty()) e = cudaMalloc(&p->d_items, sizeof(uint2) * items.size());
+            if (e == cudaSuccess && !items.empty())
+                e = cudaMemcpy(p->d_items, items.data(), sizeof(uint2) * items.size(), cudaMemcpyHostToDevice);
+        }
         if (e != cudaSuccess) {
             xrt_plan_destroy(p);
             return cuda_fail(e, "plan workspace");
@@ -341,6 +369,8 @@ xrt_status xrt_plan_destroy(xrt_plan p) {
     cudaFree(p->d_views);
     cudaFree(p->d_work_fwd);
     cudaFree(p->d_work_adj);
+    cudaFree(p->d_items);
+    cudaFree(p->d_coldesc);
     cudaFree(p->d_stage_img);
     cudaFree(p->d_stage_sino);
     if (p->aux_stream) cudaStreamDestroy((cudaStream_t)p->aux_stream);
@@ -405,7 +435,8 @@ xrt_status xrt_forward_host(xrt_plan p, const float* img_host, float* sino_host,
                              cudaMemcpyHostToDevice, s));
     st = fwd_prepare(p, p->d_stage_img, s);
     if (st != XRT_OK) return st;
-    const int64_t nchunk = std::min<int64_t>(8, p->n_views);
+    const bool whole = p->d_items && resolve(p->algo_fwd, p->column_ok) == XRT_ALGO_COLUMN;
+    const int64_t nchunk = whole ? 1 : std::min<int64_t>(8, p->n_views);
     const int64_t pv = p->det.per_view;
     std::vector<cudaEvent_t> ev((size_t)nchunk);
     for (auto& x : ev) XRT_CUDA(cudaEventCreateWithFlags(&x, cudaEventDisableTiming));
@@ -439,7 +470,8 @@ xrt_status xrt_adjoint_host(xrt_plan p, const float* sino_host, float* img_host,
     cudaStream_t s = (cudaStream_t)cuda_stream, a = (cudaStream_t)p->aux_stream;
     st = adj_begin(p, p->d_stage_img, s);
     if (st != XRT_OK) return st;
-    const int64_t nchunk = std::min<int64_t>(8, p->n_views);
+    const bool whole = p->d_items && resolve(p->algo_adj, p->column_ok) == XRT_ALGO_COLUMN;
+    const int64_t nchunk = whole ? 1 : std::min<int64_t>(8, p->n_views);
     const int64_t pv = p->det.per_view;
     std::vector<cudaEvent_t> ev((size_t)nchunk);
     for (auto& x : ev) XRT_CUDA(cudaEventCreateWithFlags(&x, cudaEventDisableTiming));

@@ -34,7 +34,9 @@
 // thin annulus |s1| ~ const of the image -- a small, L2-resident working set reused by every view.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdlib>
+#include <vector>
 
 #include "xrt_internal.cuh"
 
@@ -42,11 +44,17 @@ namespace xrt {
 
 namespace {
 
-constexpr int kColsPerCta = 4;
-constexpr int kRowWarps = 2;                     // warps per column (64 rows per CTA)
+#ifndef XRT_COLS_PER_CTA
+#define XRT_COLS_PER_CTA 4
+#endif
+#ifndef XRT_MIN_BLOCKS
+#define XRT_MIN_BLOCKS 3
+#endif
+constexpr int kColsPerCta = XRT_COLS_PER_CTA;   // detector columns per CTA (one warp each)
+constexpr int kRowWarps = 8 / XRT_COLS_PER_CTA;  // warps per column (32 rows each)
 constexpr int kWarps = kColsPerCta * kRowWarps;  // 8 warps = 256 threads
 constexpr int kSlices = 64;                      // major slices per chunk (2 x 32 lanes)
-constexpr int kSegCap = 2 * kSlices + 1;         // segments per chunk + end sentinel
+constexpr int kSegCap = 2 * kSlices;             // segments per chunk
 
 struct __align__(16) Seg {
     unsigned long long ptr;  // address of (cell, padded k = 0) in the z-fastest volume
@@ -67,10 +75,12 @@ struct ColumnPath {
     float idtb;       // 1 / dtb (estimate only; decisions use the fmaf crossing values)
     int sa, sb;       // flat xy strides of the major / minor axis
     double sig_in;    // absolute sigma of the square entry (fp64)
+    double ux0, uy0;  // in-plane index coordinates at sigma_rel = 0 (the square entry)
+    double wx, wy;    // d u / d sigma
 };
 
 // fp64 in-plane line of the column (the paper's per-column parameters), u = detector coordinate.
-__device__ __forceinline__ void column_line(const ViewRec& V, const DetC& dc, int c, double& qx,
+__host__ __device__ __forceinline__ void column_line(const ViewRec& V, const DetC& dc, int c, double& qx,
                                             double& qy, double& ex, double& ey, double& ca_out) {
     const double u = ((double)c - dc.cu) * dc.du + dc.off_u;
     if (dc.beam == XRT_PAR3D) {
@@ -135,6 +145,10 @@ __device__ __forceinline__ void column_path(const ViewRec& V, const DetC& dc, co
     }
     if (!P.hit || !(s_out - s_in > 0.0)) { P.hit = false; P.n_slices = 0; P.L = 0.f; return; }
     P.sig_in = s_in;
+    P.ux0 = ux + s_in * wx;
+    P.uy0 = uy + s_in * wy;
+    P.wx = wx;
+    P.wy = wy;
     const int cx = wx == 0.0 ? (int)floor(ux) : entry_cell(ux, wx, s_in, g.n[0]);
     const int cy = wy == 0.0 ? (int)floor(uy) : entry_cell(uy, wy, s_in, g.n[1]);
     // major axis: the one crossed most often per unit sigma
@@ -191,11 +205,13 @@ __device__ __forceinline__ float slice_start(const ColumnPath& P, int n) {
     return n == 0 ? 0.f : (n >= P.n_slices ? P.L : fminf(fmaf((float)(n - 1), P.dta, P.t0a), P.L));
 }
 
-// Segments of major slice n: 1 or 2 in-plane units (cell, sigma_start, sigma_end).  The minor
-// crossings at or before the slice start are counted against the SAME fmaf expression the
-// neighbouring slices use, so every crossing value is produced exactly once (telescoping).
-__device__ __forceinline__ int slice_segments(const ColumnPath& P, int n, float& s0, float& s1,
-                                              float& s2, int& c0, int& c1) {
+// Segments of major slice n: 1 or 2 in-plane units (cell, sigma_start, sigma_end), keeping only
+// those whose cell lies in the tile [ti0, ti1) x [tj0, tj1).  The minor crossings at or before the
+// slice start are counted against the SAME fmaf expression the neighbouring slices use, so every
+// crossing value is produced exactly once (telescoping, also across tiles).
+__device__ __forceinline__ int slice_segments(const ColumnPath& P, int n, int ti0, int ti1, int tj0,
+                                              int tj1, float& e0s, float& e0e, int& e0c, float& e1s,
+                                              float& e1e, int& e1c) {
     const float t_lo = n == 0 ? 0.f : fminf(fmaf((float)(n - 1), P.dta, P.t0a), P.L);
     const float t_hi = n + 1 >= P.n_slices ? P.L : fminf(fmaf((float)n, P.dta, P.t0a), P.L);
     const int ca = P.cell_a0 + P.step_a * n;
@@ -212,20 +228,97 @@ __device__ __forceinline__ int slice_segments(const ColumnPath& P, int n, float&
         tb = fmaf((float)m, P.dtb, P.t0b);
         split = m < P.nb_face && tb < t_hi;
     }
-    c0 = ca * P.sa + (P.cell_b0 + P.step_b * mb) * P.sb;
-    s0 = t_lo;
-    s2 = t_hi;
-    s1 = split ? tb : t_hi;
-    c1 = split ? c0 + P.step_b * P.sb : c0;
-    return split ? 2 : 1;
+    const int cb0 = P.cell_b0 + P.step_b * mb;
+    const int cb1 = split ? cb0 + P.step_b : cb0;
+    const int ii = P.a == 0 ? ca : cb0, jj0 = P.a == 0 ? cb0 : ca;
+    const bool a_in = P.a == 0 ? (ca >= ti0 && ca < ti1) : (ca >= tj0 && ca < tj1);
+    const bool b0_in = P.a == 0 ? (cb0 >= tj0 && cb0 < tj1) : (cb0 >= ti0 && cb0 < ti1);
+    const bool b1_in = P.a == 0 ? (cb1 >= tj0 && cb1 < tj1) : (cb1 >= ti0 && cb1 < ti1);
+    (void)ii; (void)jj0;
+    const int c0 = ca * P.sa + cb0 * P.sb;
+    const int c1 = ca * P.sa + cb1 * P.sb;
+    const float m1 = split ? tb : t_hi;
+    int cnt = 0;
+    if (a_in && b0_in) { e0s = t_lo; e0e = m1; e0c = c0; cnt = 1; }
+    if (split && a_in && b1_in) {
+        if (cnt == 0) { e0s = tb; e0e = t_hi; e0c = c1; }
+        else { e1s = tb; e1e = t_hi; e1c = c1; }
+        ++cnt;
+    }
+    return cnt;
 }
 
-// Per-ray z description along the shared path (sigma from the square entry).
+// Per-(view, column) path descriptor: the in-plane path (fp32 crossing sequences, cells) and the
+// fp64 terms the per-ray z setup needs.  Depends on the geometry only: built once at plan creation
+// (k_col_desc) instead of by every warp of every band and tile.
+struct __align__(16) ColDesc {
+    float L, t0a, dta, t0b;
+    float dtb, idtb;
+    int n_slices, flags;              // flags: bit0 hit, bit1 major axis (0 = x, 1 = y)
+    int cell_a0, cell_b0, nb_face, steps;  // steps: (step_a + 1) | (step_b + 1) << 2
+    float ux0, uy0, wx, wy;           // in-plane index coordinates at sigma = 0 and d/dsigma (tile clip)
+    double sig_in, ca;                // absolute sigma of the square entry; cos(alpha) of the column
+};
+
+__global__ void k_col_desc(const ViewRec* __restrict__ views, DetC dc, GridC g, int64_t n,
+                           ColDesc* __restrict__ out) {
+    const int64_t id = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (id >= n) return;
+    const int v = (int)(id / dc.cols), c = (int)(id - (int64_t)v * dc.cols);
+    ColumnPath P;
+    double ca;
+    column_path(views[v], dc, g, c, P, ca);
+    ColDesc d;
+    d.L = P.L; d.t0a = P.t0a; d.dta = P.dta; d.t0b = P.t0b; d.dtb = P.dtb; d.idtb = P.idtb;
+    d.n_slices = P.hit ? P.n_slices : 0;
+    d.flags = (P.hit ? 1 : 0) | (P.a << 1);
+    d.cell_a0 = P.cell_a0; d.cell_b0 = P.cell_b0; d.nb_face = P.nb_face;
+    d.steps = (P.step_a + 1) | ((P.step_b + 1) << 2);
+    d.ux0 = (float)P.ux0; d.uy0 = (float)P.uy0; d.wx = (float)P.wx; d.wy = (float)P.wy;
+    d.sig_in = P.sig_in;
+    d.ca = ca;
+    out[id] = d;
+}
+
+__device__ __forceinline__ void load_path(const ColDesc* __restrict__ dsc, int nx, ColumnPath& P,
+                                          double& ca, float& ux0, float& uy0, float& wx, float& wy) {
+    const float4 q0 = __ldg(reinterpret_cast<const float4*>(dsc) + 0);
+    const float4 q1 = __ldg(reinterpret_cast<const float4*>(dsc) + 1);
+    const int4 q2 = __ldg(reinterpret_cast<const int4*>(dsc) + 2);
+    const float4 q3 = __ldg(reinterpret_cast<const float4*>(dsc) + 3);
+    const double2 q4 = __ldg(reinterpret_cast<const double2*>(dsc) + 4);
+    P.L = q0.x; P.t0a = q0.y; P.dta = q0.z; P.t0b = q0.w;
+    P.dtb = q1.x; P.idtb = q1.y;
+    P.n_slices = __float_as_int(q1.z);
+    const int flags = __float_as_int(q1.w);
+    P.hit = flags & 1;
+    P.a = (flags >> 1) & 1;
+    P.cell_a0 = q2.x; P.cell_b0 = q2.y; P.nb_face = q2.z;
+    P.step_a = (q2.w & 3) - 1;
+    P.step_b = ((q2.w >> 2) & 3) - 1;
+    P.sa = P.a == 0 ? 1 : nx;
+    P.sb = P.a == 0 ? nx : 1;
+    ux0 = q3.x; uy0 = q3.y; wx = q3.z; wy = q3.w;
+    P.sig_in = q4.x;
+    ca = q4.y;
+}
+
+// Per-ray z description along the shared path (sigma from the square entry).  The z cell at sigma is
+// kp(sigma) = kp0 + dk * c(sigma), c = number of z-plane crossings tau_m = t0z + m dtz <= sigma, and is
+// evaluated statelessly: x = fmaf(sigma, A, B) = dk * ((sigma - t0z + dtz) / dtz) - dk / 2 has
+// rint(x) = dk * c, read from the mantissa of x + 1.5 * 2^23 (one FADD); x is small (|x| <= L/dtz
+// + 1), so the decision is made in sigma to within rounding of sigma (well conditioned also for
+// rays almost parallel to the z planes).
+constexpr float kMagic = 12582912.0f;          // 1.5 * 2^23: bits(x + kMagic) = 0x4B400000 + rint(x)
+constexpr unsigned kMagicBits = 0x4B400000u;
+
 struct RayZ {
     bool active;      // ray exists (row in range) and the column hits the square
     int kp;           // padded z index (k + pad) of the cell at sigma = 0
     int dk;           // +1 / -1 per z-plane crossing, 0 when z is fixed
     float t0z, dtz;   // z-plane crossings tau_m = t0z + m dtz (INF when fixed)
+    float A, B;       // x(sigma) = fmaf(sigma, A, B), rint(x) = dk * c(sigma)
+    unsigned off;     // kp(sigma) = bits(x + kMagic) + off  (off = kp0 - kMagicBits, mod 2^32)
     float scale;      // 1 / cos(beta): physical length per unit sigma
 };
 
@@ -233,69 +326,87 @@ __device__ __forceinline__ void ray_z(const ViewRec& V, const DetC& dc, const Gr
                                       const ColumnPath& P, double ca, int r, int pad, RayZ& Z) {
     Z.active = false;
     Z.kp = pad; Z.dk = 0; Z.t0z = INFINITY; Z.dtz = 0.f; Z.scale = 1.f;
+    Z.A = 0.f; Z.B = 0.f; Z.off = (unsigned)pad - kMagicBits;
     if (r >= dc.rows || !P.hit) return;
     const double v = ((double)r - dc.cv) * dc.dv + dc.off_v;
-    double tb, z0, cb;  // tan(beta), z at absolute sigma 0, cos(beta)
+    double tb, z0;  // tan(beta), z at absolute sigma 0
     if (dc.beam == XRT_PAR3D) {
         // z(sigma) = s2 / cos(phi2) + sigma tan(phi2), sigma = t cos(phi2) - s2 sin(phi2)
-        cb = V.c2;
-        tb = V.s2 / V.c2;
-        z0 = v / V.c2;
         if (fabs(V.s2) <= kSnap) { tb = 0.0; z0 = v * V.c2; }
+        else { tb = V.pad[0]; z0 = v * V.pad[1]; }      // tan(phi2), 1 / cos(phi2) (plan)
     } else {
-        const double D = dc.D;
-        const double h = v * D / dc.sdd;
-        // tan(beta) = h / sqrt(D^2 + t^2) = h cos(alpha) / D; |theta_xy| = cos(beta)
-        const double tanb = h * ca / D;
-        cb = 1.0 / sqrt(1.0 + tanb * tanb);
-        const double s2 = h * (ca * ca) * cb + V.H * cb;
-        tb = tanb;
-        z0 = s2 / cb;
-        if (fabs(tanb * cb) <= kSnap) { tb = 0.0; z0 = s2; }
+        // tan(beta) = h / sqrt(D^2 + t^2) = h cos(alpha) / D, z(sigma=0) = s2 / cos(beta) = h cos^2
+        // (alpha) + H  (P:636, P:660 divided by cos(beta))
+        const double h = v * dc.D / dc.sdd;
+        tb = h * ca * dc.inv_D;
+        z0 = h * (ca * ca) + V.H;
+        if (fabs(tb) <= kSnap) tb = 0.0;
     }
-    Z.scale = (float)(1.0 / cb);
-    const double uz0 = (g.z_hi - (z0 + P.sig_in * tb)) / g.d[2];   // u_z at sigma = 0
-    const double wz = -tb / g.d[2];
-    double kk = floor(uz0);                                         // half-open cell
-    if (kk < (double)(-pad)) kk = (double)(-pad);
-    if (kk > (double)(g.n[2] + pad - 1)) kk = (double)(g.n[2] + pad - 1);
-    Z.kp = (int)kk + pad;
-    if (wz != 0.0) {
-        const double iw = 1.0 / wz;
-        const double bf = wz > 0.0 ? kk + 1.0 : kk;                 // first plane ahead
-        Z.t0z = (float)((bf - uz0) * iw);
-        Z.dtz = (float)fabs(iw);
-        Z.dk = wz > 0.0 ? 1 : -1;
+    Z.scale = sqrtf(1.f + (float)(tb * tb));           // 1 / cos(beta)
+    if (tb == 0.0) {
+        // fixed z: the half-open cell floor(u0); rays outside the slab read padding
+        double kk = floor((g.z_hi - z0) / g.d[2]);
+        kk = fmin(fmax(kk, (double)(-pad)), (double)(g.n[2] + pad - 1));
+        Z.kp = (int)kk + pad;
+        Z.off = (unsigned)Z.kp - kMagicBits;
+    } else {
+        const double uz0 = (g.z_hi - (z0 + P.sig_in * tb)) * g.inv_dz;   // u_z at sigma = 0
+        const double iw = -g.d[2] * __drcp_rn(tb);                          // 1 / (d u_z / d sigma)
+        double kk = floor(uz0);
+        kk = fmin(fmax(kk, (double)(-pad)), (double)(g.n[2] + pad - 1));
+        Z.kp = (int)kk + pad;
+        const double bf = iw > 0.0 ? kk + 1.0 : kk;                          // first plane ahead
+        const double t0 = (bf - uz0) * iw, dt = fabs(iw);
+        Z.t0z = (float)t0;
+        Z.dtz = (float)dt;
+        Z.dk = iw > 0.0 ? 1 : -1;
+        // c(sigma) = floor((sigma - (t0 - dt)) / dt): x = dk * (sigma - t0 + dt) / dt - dk / 2
+        const double idt = 1.0 / dt;
+        Z.A = (float)(Z.dk * idt);
+        Z.B = (float)(Z.dk * ((dt - t0) * idt - 0.5));
+        Z.off = (unsigned)Z.kp - kMagicBits;
     }
     Z.active = true;
 }
 
+// Work item of the tiled launch: (view, column group, tile); items are sorted by tile so that all
+// views and columns crossing one volume tile run while the tile is L2-resident.
+struct ColumnLaunch {
+    const uint2* items;   // nullptr: untiled, (view, cgroup) from the block id
+    int n_items;
+    int n_views, n_cgroups, n_bands;
+    int tile, n_tx;       // tile side in cells, tiles along x
+    int nzp, pad;
+};
+
 template <bool kAdjoint>
-__global__ void __launch_bounds__(kWarps * 32, 3) k_column(const ViewRec* __restrict__ views, DetC dc,
+__global__ void __launch_bounds__(kWarps * 32, XRT_MIN_BLOCKS) k_column(const ViewRec* __restrict__ views, DetC dc,
                                                          GridC g, const float* __restrict__ vol,
                                                          float* __restrict__ volw,
                                                          const float* __restrict__ sino_in,
                                                          float* __restrict__ sino_out, int view0,
-                                                         int n_views, int n_cgroups, int nzp, int pad,
-                                                         int order) {
+                                                         const ColDesc* __restrict__ desc,
+                                                         ColumnLaunch L) {
     __shared__ Seg s_seg[kWarps][kSegCap];
+    __shared__ float s_first[kWarps];
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
-    // 1D grid; order 0: id = (band * n_cgroups + cgroup) * n_views + view (views fastest)
-    //          order 1: id = (band * n_views + view) * n_cgroups + cgroup (columns fastest)
     const unsigned bid = blockIdx.x;
-    int vv, cg, band;
-    if (order == 0) {
-        vv = (int)(bid % (unsigned)n_views);
-        const unsigned rest = bid / (unsigned)n_views;
-        cg = (int)(rest % (unsigned)n_cgroups);
-        band = (int)(rest / (unsigned)n_cgroups);
+    const int band = (int)(bid % (unsigned)L.n_bands);
+    const unsigned it = bid / (unsigned)L.n_bands;
+    int vv, cg, ti0 = 0, ti1 = g.n[0], tj0 = 0, tj1 = g.n[1];
+    if (L.items) {
+        const uint2 w = L.items[it];
+        vv = (int)w.x;
+        cg = (int)(w.y & 0xffffu);
+        const int t = (int)(w.y >> 16);
+        ti0 = (t % L.n_tx) * L.tile; ti1 = min(ti0 + L.tile, g.n[0]);
+        tj0 = (t / L.n_tx) * L.tile; tj1 = min(tj0 + L.tile, g.n[1]);
     } else {
-        cg = (int)(bid % (unsigned)n_cgroups);
-        const unsigned rest = bid / (unsigned)n_cgroups;
-        vv = (int)(rest % (unsigned)n_views);
-        band = (int)(rest / (unsigned)n_views);
+        cg = (int)(it % (unsigned)L.n_cgroups);
+        vv = (int)(it / (unsigned)L.n_cgroups);
     }
+    const bool tiled = L.items != nullptr;
     const int c = cg * kColsPerCta + (warp % kColsPerCta);
     const int r = (band * kRowWarps + warp / kColsPerCta) * 32 + lane;
     const int v = view0 + vv;
@@ -303,30 +414,52 @@ __global__ void __launch_bounds__(kWarps * 32, 3) k_column(const ViewRec* __rest
     const ViewRec V = views[v];
     ColumnPath P;
     double ca;
-    column_path(V, dc, g, c, P, ca);
+    float pux, puy, pwx, pwy;
+    load_path(desc + ((int64_t)v * dc.cols + c), g.n[0], P, ca, pux, puy, pwx, pwy);
     RayZ Z;
-    ray_z(V, dc, g, P, ca, r, pad, Z);
+    ray_z(V, dc, g, P, ca, r, L.pad, Z);
     const int64_t m = ((int64_t)v * dc.rows + r) * dc.cols + c;
     float y = 0.f;
     if (kAdjoint && Z.active) y = sino_in[m] * Z.scale;
     const bool live = kAdjoint ? (Z.active && y != 0.f) : Z.active;
+    // slice range of the tile: clip the in-plane line to the tile box (fp64), then widen by one
+    // slice each way (segments outside the tile are filtered exactly)
+    int na = 0, nb = P.n_slices;
+    if (tiled && P.hit) {
+        float lo = -INFINITY, hi = INFINITY;
+        if (pwx != 0.f) {
+            const float a0 = (ti0 - pux) / pwx, a1 = (ti1 - pux) / pwx;
+            lo = fmaxf(lo, fminf(a0, a1)); hi = fminf(hi, fmaxf(a0, a1));
+        } else if (!(pux >= ti0 - 1e-3f && pux <= ti1 + 1e-3f)) { hi = -INFINITY; }
+        if (pwy != 0.f) {
+            const float a0 = (tj0 - puy) / pwy, a1 = (tj1 - puy) / pwy;
+            lo = fmaxf(lo, fminf(a0, a1)); hi = fminf(hi, fmaxf(a0, a1));
+        } else if (!(puy >= tj0 - 1e-3f && puy <= tj1 + 1e-3f)) { hi = -INFINITY; }
+        if (!(hi >= lo)) { na = nb = 0; }
+        else {
+            // conservative slice range (segments outside the tile are filtered exactly)
+            const float ida = 1.f / P.dta;
+            na = max(0, __float2int_rd((lo - P.t0a) * ida) - 1);
+            nb = min(P.n_slices, __float2int_rd((hi - P.t0a) * ida) + 3);
+        }
+    }
     float acc_s = 0.f, acc_e = 0.f;
     Seg* seg = s_seg[warp];
     const unsigned long long base = (unsigned long long)(kAdjoint ? (const float*)volw : vol);
-    const unsigned long long cstride = 4ull * (unsigned long long)nzp;
+    const unsigned long long cstride = 4ull * (unsigned long long)L.nzp;
     unsigned kp = (unsigned)Z.kp;
-    (void)0;
     float tz = Z.t0z, mz = 0.f;
-    if (__any_sync(0xffffffffu, live)) {
-        for (int n0 = 0; n0 < P.n_slices; n0 += kSlices) {
-            // ---- warp-cooperative: slices n0 .. n0+63 -> segments in path order
+    bool zinit = !tiled;  // untiled: the z state at sigma = 0 is the initial one
+    if (__any_sync(0xffffffffu, live) && nb > na) {
+        for (int n0 = na; n0 < nb; n0 += kSlices) {
+            // ---- warp-cooperative: slices n0 .. n0+63 -> in-tile segments in path order
             int total = 0;
 #pragma unroll
             for (int half = 0; half < 2; ++half) {
                 const int n = n0 + half * 32 + lane;
-                float a0 = 0.f, a1 = 0.f, a2 = 0.f;
+                float a0s = 0.f, a0e = 0.f, a1s = 0.f, a1e = 0.f;
                 int c0 = 0, c1 = 0, cnt = 0;
-                if (n < P.n_slices) cnt = slice_segments(P, n, a0, a1, a2, c0, c1);
+                if (n < nb) cnt = slice_segments(P, n, ti0, ti1, tj0, tj1, a0s, a0e, c0, a1s, a1e, c1);
                 int incl = cnt;
 #pragma unroll
                 for (int o = 1; o < 32; o <<= 1) {
@@ -335,50 +468,71 @@ __global__ void __launch_bounds__(kWarps * 32, 3) k_column(const ViewRec* __rest
                 }
                 const int b = total + incl - cnt;
                 if (cnt > 0) {
-                    Seg q; q.ptr = base + cstride * (unsigned)c0; q.se = a1; q.ds = a1 - a0;
+                    Seg q; q.ptr = base + cstride * (unsigned)c0; q.se = a0e; q.ds = a0e - a0s;
                     seg[b] = q;
+                    if (b == 0) s_first[warp] = a0s;
                 }
                 if (cnt > 1) {
-                    Seg q; q.ptr = base + cstride * (unsigned)c1; q.se = a2; q.ds = a2 - a1;
+                    Seg q; q.ptr = base + cstride * (unsigned)c1; q.se = a1e; q.ds = a1e - a1s;
                     seg[b + 1] = q;
                 }
                 total += __shfl_sync(0xffffffffu, incl, 31);
             }
             __syncwarp();
+            if (!zinit && total > 0) {
+                // z state at the first in-tile segment: crossings tau_m < sigma_first already taken
+                zinit = true;
+                if (Z.dk != 0) {
+                    const float sf = s_first[warp];
+                    int m0 = (int)ceilf((sf - Z.t0z) / Z.dtz);
+                    m0 = m0 < 0 ? 0 : m0;
+                    if (fmaf((float)m0, Z.dtz, Z.t0z) < sf) ++m0;
+                    if (m0 > 0 && !(fmaf((float)(m0 - 1), Z.dtz, Z.t0z) < sf)) --m0;
+                    kp = (unsigned)(Z.kp + Z.dk * m0);
+                    mz = (float)m0;
+                    tz = fmaf(mz, Z.dtz, Z.t0z);
+                }
+            }
             if (live) {
                 // ---- units of each segment: cell k_s, and k_s + dk after the z crossing tz
 #pragma unroll 4
                 for (int s = 0; s < total; ++s) {
                     const uint4 raw = *reinterpret_cast<const uint4*>(&seg[s]);
-                    Seg q;
-                    q.ptr = ((unsigned long long)raw.y << 32) | raw.x;
-                    q.se = __uint_as_float(raw.z);
-                    q.ds = __uint_as_float(raw.w);
-                    const bool cross = tz < q.se;
-                    const float l_e = fmaxf(q.se - tz, 0.f);         // C_up - C_low, cell k_e
-                    const float l_s = q.ds - l_e;                    // C_up - C_low, cell k_s
+                    const unsigned long long qptr = ((unsigned long long)raw.y << 32) | raw.x;
+                    const float qse = __uint_as_float(raw.z);
+                    const float qds = __uint_as_float(raw.w);
+                    const bool cross = tz < qse;
                     if (kAdjoint) {
-                        atomicAdd((float*)(q.ptr + 4ull * kp), y * l_s);
-                    } else {
-                        acc_s = fmaf(__ldg((const float*)(q.ptr + 4ull * kp)), l_s, acc_s);
-                    }
-                    if (cross) {
-                        kp += Z.dk;
-                        if (kAdjoint) {
-                            atomicAdd((float*)(q.ptr + 4ull * kp), y * l_e);
-                        } else {
-                            acc_e = fmaf(__ldg((const float*)(q.ptr + 4ull * kp)), l_e, acc_e);
+                        const float l_e = fmaxf(qse - tz, 0.f);     // C_up - C_low, cell k_e
+                        atomicAdd((float*)(qptr + 4ull * kp), y * (qds - l_e));
+                        if (cross) {
+                            kp += Z.dk;
+                            atomicAdd((float*)(qptr + 4ull * kp), y * l_e);
+                            mz += 1.f;
+                            tz = fmaf(mz, Z.dtz, Z.t0z);
                         }
-                        mz += 1.f;
-                        tz = fmaf(mz, Z.dtz, Z.t0z);
+                    } else {
+                        // f_s * d_sigma for the whole segment, then move (sigma_e - tau) to k_e
+                        const float fs = __ldg((const float*)(qptr + 4ull * kp));
+                        acc_s = fmaf(fs, qds, acc_s);
+                        if (cross) {
+                            kp += Z.dk;
+                            const float fe = __ldg((const float*)(qptr + 4ull * kp));
+                            acc_e = fmaf(fe - fs, qse - tz, acc_e);
+                            mz += 1.f;
+                            tz = fmaf(mz, Z.dtz, Z.t0z);
+                        }
                     }
                 }
             }
             __syncwarp();
         }
     }
-    const float acc = acc_s + acc_e, acc2 = 0.f;
-    if (!kAdjoint && r < dc.rows) sino_out[m] = (acc + acc2) * Z.scale;
+    if (!kAdjoint && r < dc.rows) {
+        const float out = (acc_s + acc_e) * Z.scale;
+        if (tiled) { if (out != 0.f) atomicAdd(sino_out + m, out); }
+        else sino_out[m] = out;
+    }
 }
 
 // [rows][cols] (row stride in_ld, column offset in_off) -> [cols][rows] (row stride out_ld,
@@ -410,14 +564,6 @@ inline cudaError_t transpose(const float* in, float* out, int64_t rows, int64_t 
     return cudaGetLastError();
 }
 
-int column_order() {
-    static int o = [] {
-        const char* e = getenv("XRT_COLUMN_ORDER");
-        return e ? atoi(e) : 1;
-    }();
-    return o;
-}
-
 }  // namespace
 
 // image [N_z][N_xy] -> padded z-fastest work [N_xy][NzP] (interior rows pad .. pad + N_z)
@@ -430,30 +576,113 @@ cudaError_t launch_from_zfast(const xrt_plan_s* p, const float* work, float* img
     return transpose(work, img, p->grid.nxy, p->grid.n[2], p->nzp, p->zpad, p->grid.nxy, 0, s);
 }
 
+ColumnLaunch make_launch(const xrt_plan_s* p, int64_t v0, int64_t v1, int& nblk) {
+    ColumnLaunch L;
+    const int rows_per_cta = kRowWarps * 32;
+    L.n_views = (int)(v1 - v0);
+    L.n_cgroups = (p->det.cols + kColsPerCta - 1) / kColsPerCta;
+    L.n_bands = (p->det.rows + rows_per_cta - 1) / rows_per_cta;
+    L.nzp = (int)p->nzp;
+    L.pad = (int)p->zpad;
+    L.tile = p->tile;
+    L.n_tx = p->n_tx;
+    if (p->d_items && v0 == 0 && v1 == p->n_views) {
+        L.items = (const uint2*)p->d_items;
+        L.n_items = (int)p->n_items;
+        nblk = L.n_items * L.n_bands;
+    } else if (p->d_items) {
+        // view sub-range of a tiled plan (host pipeline chunks): the items of those views
+        L.items = (const uint2*)p->d_items;
+        L.n_items = (int)p->n_items;
+        nblk = L.n_items * L.n_bands;
+    } else {
+        L.items = nullptr;
+        L.n_items = L.n_views * L.n_cgroups;
+        nblk = L.n_items * L.n_bands;
+    }
+    return L;
+}
+
 cudaError_t launch_forward_column(const xrt_plan_s* p, const float* vol_zfast, float* sino,
                                   int64_t v0, int64_t v1, cudaStream_t s) {
     if (v1 <= v0) return cudaSuccess;
-    const int rows_per_cta = kRowWarps * 32;
-    const int ncg = (p->det.cols + kColsPerCta - 1) / kColsPerCta;
-    const int nband = (p->det.rows + rows_per_cta - 1) / rows_per_cta;
-    const unsigned nblk = (unsigned)((v1 - v0) * ncg * nband);
+    int nblk = 0;
+    ColumnLaunch L = make_launch(p, v0, v1, nblk);
+    if (L.items && !(v0 == 0 && v1 == p->n_views)) return cudaErrorInvalidValue;
+    if (L.items) {
+        cudaError_t e = cudaMemsetAsync(sino, 0, sizeof(float) * (size_t)p->n_rays, s);
+        if (e != cudaSuccess) return e;
+    }
     k_column<false><<<nblk, kWarps * 32, 0, s>>>(p->d_views, p->det, p->grid, vol_zfast, nullptr,
-                                                nullptr, sino, (int)v0,
-        (int)(v1 - v0), ncg, (int)p->nzp, (int)p->zpad, column_order());
+                                                nullptr, sino, (int)v0, (const ColDesc*)p->d_coldesc, L);
     return cudaGetLastError();
 }
 
 cudaError_t launch_adjoint_column(const xrt_plan_s* p, const float* sino, float* vol_zfast,
                                   int64_t v0, int64_t v1, cudaStream_t s) {
     if (v1 <= v0) return cudaSuccess;
-    const int rows_per_cta = kRowWarps * 32;
-    const int ncg = (p->det.cols + kColsPerCta - 1) / kColsPerCta;
-    const int nband = (p->det.rows + rows_per_cta - 1) / rows_per_cta;
-    const unsigned nblk = (unsigned)((v1 - v0) * ncg * nband);
+    int nblk = 0;
+    ColumnLaunch L = make_launch(p, v0, v1, nblk);
+    if (L.items && !(v0 == 0 && v1 == p->n_views)) return cudaErrorInvalidValue;
     k_column<true><<<nblk, kWarps * 32, 0, s>>>(p->d_views, p->det, p->grid, nullptr, vol_zfast,
-                                               sino, nullptr, (int)v0,
-        (int)(v1 - v0), ncg, (int)p->nzp, (int)p->zpad, column_order());
+                                               sino, nullptr, (int)v0, (const ColDesc*)p->d_coldesc, L);
     return cudaGetLastError();
+}
+
+size_t column_desc_bytes() { return sizeof(ColDesc); }
+
+cudaError_t launch_col_desc(const xrt_plan_s* p, cudaStream_t s) {
+    const int64_t n = p->n_views * (int64_t)p->det.cols;
+    k_col_desc<<<(unsigned)((n + 127) / 128), 128, 0, s>>>(p->d_views, p->det, p->grid, n,
+                                                         (ColDesc*)p->d_coldesc);
+    return cudaGetLastError();
+}
+
+// Host: work list of the tiled launch.  For every view and column group, the tiles crossed by
+// any of the group's in-plane lines (walked in fp64 over the tile grid); items sorted by tile.
+int build_column_items(const xrt_plan_s* p, const ViewRec* views_host, std::vector<uint2>& items) {
+    const GridC& g = p->grid;
+    const DetC& dc = p->det;
+    const int ts = p->tile, ntx = p->n_tx, nty = p->n_ty;
+    const int ncg = (dc.cols + kColsPerCta - 1) / kColsPerCta;
+    std::vector<std::vector<uint2>> per_tile((size_t)ntx * nty);
+    std::vector<int> mark((size_t)ntx * nty, -1);
+    for (int64_t v = 0; v < p->n_views; ++v) {
+        for (int cgi = 0; cgi < ncg; ++cgi) {
+            const int stamp = (int)(v * ncg + cgi);
+            for (int c = cgi * kColsPerCta; c < std::min(dc.cols, (cgi + 1) * kColsPerCta); ++c) {
+                double qx, qy, ex, ey, ca;
+                column_line(views_host[v], dc, c, qx, qy, ex, ey, ca);
+                const double ux = (qx - g.x_lo) / g.d[0], uy = (g.y_hi - qy) / g.d[1];
+                const double wx = ex / g.d[0], wy = -ey / g.d[1];
+                // test every tile box (expanded by a margin); tiles are few (<= 64)
+                for (int ty = 0; ty < nty; ++ty)
+                    for (int tx = 0; tx < ntx; ++tx) {
+                        const int t = ty * ntx + tx;
+                        if (mark[t] == stamp) continue;
+                        const double x0 = tx * ts - 1e-3, x1 = std::min(g.n[0], (tx + 1) * ts) + 1e-3;
+                        const double y0 = ty * ts - 1e-3, y1 = std::min(g.n[1], (ty + 1) * ts) + 1e-3;
+                        double lo = -INFINITY, hi = INFINITY;
+                        bool ok = true;
+                        if (wx != 0.0) {
+                            const double a0 = (x0 - ux) / wx, a1 = (x1 - ux) / wx;
+                            lo = std::max(lo, std::min(a0, a1)); hi = std::min(hi, std::max(a0, a1));
+                        } else ok = ux >= x0 && ux <= x1;
+                        if (wy != 0.0) {
+                            const double a0 = (y0 - uy) / wy, a1 = (y1 - uy) / wy;
+                            lo = std::max(lo, std::min(a0, a1)); hi = std::min(hi, std::max(a0, a1));
+                        } else ok = ok && uy >= y0 && uy <= y1;
+                        if (ok && hi >= lo) {
+                            mark[t] = stamp;
+                            per_tile[t].push_back(make_uint2((unsigned)v, (unsigned)cgi | ((unsigned)t << 16)));
+                        }
+                    }
+            }
+        }
+    }
+    items.clear();
+    for (auto& vt : per_tile) items.insert(items.end(), vt.begin(), vt.end());
+    return (int)items.size();
 }
 
 }  // namespace xrt

@@ -31,7 +31,7 @@ struct ViewRec {
     double c1, s1;
     double c2, s2;  // par3d: cos/sin(phi2 = tilt); unused otherwise
     double H;       // helical source height H(phi1'); 0 otherwise
-    double pad[3];
+    double pad[3];  // par3d: pad[0] = tan(phi2), pad[1] = 1 / cos(phi2)
 };
 
 struct GridC {
@@ -39,12 +39,14 @@ struct GridC {
     double d[3];       // spacing
     double x_lo, y_hi, z_hi;
     double tau;        // drop threshold for the fp64 CSR path (reading 4)
+    double inv_dz;     // 1 / d_z
     int64_t nxy, nxyz;
 };
 
 struct DetC {
     int beam;                              // xrt_beam
     double D, sdd;                         // source-to-origin / -detector distances
+    double inv_D;                          // 1 / D
     int cols, rows;
     double du, dv, cu, cv, off_u, off_v;  // u_c = (c - cu) du + off_u
     int64_t per_view;                      // rows * cols
@@ -186,6 +188,10 @@ struct xrt_plan_s {
     float* d_work_fwd = nullptr;       // z-fastest, z-padded copy of the forward input (COLUMN)
     float* d_work_adj = nullptr;       // z-fastest, z-padded adjoint accumulator (COLUMN)
     int64_t zpad = 0, nzp = 0;         // z padding per side and padded column length
+    int tile = 0, n_tx = 1, n_ty = 1;  // xy tiling of the column kernels (L2 residency)
+    void* d_items = nullptr;           // device uint2 work list (tiled) or nullptr
+    void* d_coldesc = nullptr;         // per-(view, column) path descriptors (COLUMN)
+    int64_t n_items = 0;
     // host-pipeline staging (allocated on first *_host call)
     float* d_stage_img = nullptr;
     float* d_stage_sino = nullptr;
@@ -213,4 +219,10 @@ cudaError_t launch_forward_column(const xrt_plan_s* p, const float* vol_zfast, f
                                   int64_t v0, int64_t v1, cudaStream_t s);
 cudaError_t launch_adjoint_column(const xrt_plan_s* p, const float* sino, float* vol_zfast,
                                   int64_t v0, int64_t v1, cudaStream_t s);
+}  // namespace xrt
+#include <vector>
+namespace xrt {
+int build_column_items(const xrt_plan_s* p, const ViewRec* views_host, std::vector<uint2>& items);
+size_t column_desc_bytes();
+cudaError_t launch_col_desc(const xrt_plan_s* p, cudaStream_t s);
 }  // namespace xrt
