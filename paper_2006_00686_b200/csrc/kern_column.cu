@@ -45,16 +45,18 @@ namespace xrt {
 namespace {
 
 #ifndef XRT_COLS_PER_CTA
-#define XRT_COLS_PER_CTA 4
+#define XRT_COLS_PER_CTA 1
+#endif
+#ifndef XRT_CTA_WARPS
+#define XRT_CTA_WARPS 8
 #endif
 #ifndef XRT_MIN_BLOCKS
-#define XRT_MIN_BLOCKS 3
+#define XRT_MIN_BLOCKS 4
 #endif
-constexpr int kColsPerCta = XRT_COLS_PER_CTA;   // detector columns per CTA (one warp each)
-constexpr int kRowWarps = 8 / XRT_COLS_PER_CTA;  // warps per column (32 rows each)
-constexpr int kWarps = kColsPerCta * kRowWarps;  // 8 warps = 256 threads
+constexpr int kColsPerCta = XRT_COLS_PER_CTA;               // detector columns per CTA
+constexpr int kRowWarps = XRT_CTA_WARPS / XRT_COLS_PER_CTA;  // warps per column (32 rows each)
+constexpr int kWarps = kColsPerCta * kRowWarps;
 constexpr int kSlices = 64;                      // major slices per chunk (2 x 32 lanes)
-constexpr int kSegCap = 2 * kSlices;             // segments per chunk
 
 struct __align__(16) Seg {
     unsigned long long ptr;  // address of (cell, padded k = 0) in the z-fastest volume
@@ -387,10 +389,19 @@ __global__ void __launch_bounds__(kWarps * 32, XRT_MIN_BLOCKS) k_column(const Vi
                                                          float* __restrict__ sino_out, int view0,
                                                          const ColDesc* __restrict__ desc,
                                                          ColumnLaunch L) {
-    __shared__ Seg s_seg[kWarps][kSegCap];
-    __shared__ float s_first[kWarps];
+    // CTA = kColsPerCta detector columns x kRowWarps warps of 32 rows.  The in-plane path of each
+    // column is generated cooperatively by its kRowWarps warps (one slice per thread, block-level
+    // scan) and shared through shared memory by all of them.
+    constexpr int kChunk = kRowWarps * 32;   // slices per chunk and column
+    constexpr int kCap = 2 * kChunk;         // segments per chunk and column
+    __shared__ Seg s_seg[kColsPerCta][kCap];
+    __shared__ int s_wtot[kWarps];
+    __shared__ int s_nch[kColsPerCta];
+    __shared__ float s_first[kColsPerCta];
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
+    const int col = warp / kRowWarps;        // column of this warp inside the CTA
+    const int sub = warp % kRowWarps;        // row group of this warp inside the column
     const unsigned bid = blockIdx.x;
     const int band = (int)(bid % (unsigned)L.n_bands);
     const unsigned it = bid / (unsigned)L.n_bands;
@@ -407,24 +418,25 @@ __global__ void __launch_bounds__(kWarps * 32, XRT_MIN_BLOCKS) k_column(const Vi
         vv = (int)(it / (unsigned)L.n_cgroups);
     }
     const bool tiled = L.items != nullptr;
-    const int c = cg * kColsPerCta + (warp % kColsPerCta);
-    const int r = (band * kRowWarps + warp / kColsPerCta) * 32 + lane;
+    const int c = cg * kColsPerCta + col;
+    const int r = (band * kRowWarps + sub) * 32 + lane;
     const int v = view0 + vv;
-    if (c >= dc.cols) return;  // warp-uniform
+    const bool col_ok = c < dc.cols;
     const ViewRec V = views[v];
     ColumnPath P;
-    double ca;
-    float pux, puy, pwx, pwy;
-    load_path(desc + ((int64_t)v * dc.cols + c), g.n[0], P, ca, pux, puy, pwx, pwy);
+    double ca = 1.0;
+    float pux = 0.f, puy = 0.f, pwx = 0.f, pwy = 0.f;
+    if (col_ok) load_path(desc + ((int64_t)v * dc.cols + c), g.n[0], P, ca, pux, puy, pwx, pwy);
+    else { P.hit = false; P.n_slices = 0; }
     RayZ Z;
     ray_z(V, dc, g, P, ca, r, L.pad, Z);
     const int64_t m = ((int64_t)v * dc.rows + r) * dc.cols + c;
     float y = 0.f;
     if (kAdjoint && Z.active) y = sino_in[m] * Z.scale;
     const bool live = kAdjoint ? (Z.active && y != 0.f) : Z.active;
-    // slice range of the tile: clip the in-plane line to the tile box (fp64), then widen by one
-    // slice each way (segments outside the tile are filtered exactly)
-    int na = 0, nb = P.n_slices;
+    // slice range of the tile: clip the in-plane line to the tile box, then widen (segments
+    // outside the tile are filtered exactly by slice_segments)
+    int na = 0, nb = P.hit ? P.n_slices : 0;
     if (tiled && P.hit) {
         float lo = -INFINITY, hi = INFINITY;
         if (pwx != 0.f) {
@@ -437,98 +449,105 @@ __global__ void __launch_bounds__(kWarps * 32, XRT_MIN_BLOCKS) k_column(const Vi
         } else if (!(puy >= tj0 - 1e-3f && puy <= tj1 + 1e-3f)) { hi = -INFINITY; }
         if (!(hi >= lo)) { na = nb = 0; }
         else {
-            // conservative slice range (segments outside the tile are filtered exactly)
             const float ida = 1.f / P.dta;
             na = max(0, __float2int_rd((lo - P.t0a) * ida) - 1);
             nb = min(P.n_slices, __float2int_rd((hi - P.t0a) * ida) + 3);
         }
     }
+    // CTA-uniform chunk count (the loop contains __syncthreads)
+    if (sub == 0 && lane == 0) s_nch[col] = nb > na ? (nb - na + kChunk - 1) / kChunk : 0;
+    __syncthreads();
+    int nch = 0;
+#pragma unroll
+    for (int q = 0; q < kColsPerCta; ++q) nch = max(nch, s_nch[q]);
     float acc_s = 0.f, acc_e = 0.f;
-    Seg* seg = s_seg[warp];
+    Seg* seg = s_seg[col];
     const unsigned long long base = (unsigned long long)(kAdjoint ? (const float*)volw : vol);
     const unsigned long long cstride = 4ull * (unsigned long long)L.nzp;
     unsigned kp = (unsigned)Z.kp;
     float tz = Z.t0z, mz = 0.f;
     bool zinit = !tiled;  // untiled: the z state at sigma = 0 is the initial one
-    if (__any_sync(0xffffffffu, live) && nb > na) {
-        for (int n0 = na; n0 < nb; n0 += kSlices) {
-            // ---- warp-cooperative: slices n0 .. n0+63 -> in-tile segments in path order
-            int total = 0;
+    for (int ich = 0; ich < nch; ++ich) {
+        // ---- block-cooperative: slice n = na + ich*kChunk + sub*32 + lane -> in-tile segments
+        const int n = na + ich * kChunk + sub * 32 + lane;
+        float a0s = 0.f, a0e = 0.f, a1s = 0.f, a1e = 0.f;
+        int c0 = 0, c1 = 0, cnt = 0;
+        if (n < nb) cnt = slice_segments(P, n, ti0, ti1, tj0, tj1, a0s, a0e, c0, a1s, a1e, c1);
+        int incl = cnt;
 #pragma unroll
-            for (int half = 0; half < 2; ++half) {
-                const int n = n0 + half * 32 + lane;
-                float a0s = 0.f, a0e = 0.f, a1s = 0.f, a1e = 0.f;
-                int c0 = 0, c1 = 0, cnt = 0;
-                if (n < nb) cnt = slice_segments(P, n, ti0, ti1, tj0, tj1, a0s, a0e, c0, a1s, a1e, c1);
-                int incl = cnt;
+        for (int o = 1; o < 32; o <<= 1) {
+            const int t = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += t;
+        }
+        if (lane == 31) s_wtot[warp] = incl;
+        __syncthreads();
+        int before = 0, total = 0;
 #pragma unroll
-                for (int o = 1; o < 32; o <<= 1) {
-                    const int t = __shfl_up_sync(0xffffffffu, incl, o);
-                    if (lane >= o) incl += t;
-                }
-                const int b = total + incl - cnt;
-                if (cnt > 0) {
-                    Seg q; q.ptr = base + cstride * (unsigned)c0; q.se = a0e; q.ds = a0e - a0s;
-                    seg[b] = q;
-                    if (b == 0) s_first[warp] = a0s;
-                }
-                if (cnt > 1) {
-                    Seg q; q.ptr = base + cstride * (unsigned)c1; q.se = a1e; q.ds = a1e - a1s;
-                    seg[b + 1] = q;
-                }
-                total += __shfl_sync(0xffffffffu, incl, 31);
+        for (int q = 0; q < kRowWarps; ++q) {
+            const int wt = s_wtot[col * kRowWarps + q];
+            before += q < sub ? wt : 0;
+            total += wt;
+        }
+        const int b = before + incl - cnt;
+        if (cnt > 0) {
+            Seg q; q.ptr = base + cstride * (unsigned)c0; q.se = a0e; q.ds = a0e - a0s;
+            seg[b] = q;
+            if (b == 0) s_first[col] = a0s;
+        }
+        if (cnt > 1) {
+            Seg q; q.ptr = base + cstride * (unsigned)c1; q.se = a1e; q.ds = a1e - a1s;
+            seg[b + 1] = q;
+        }
+        __syncthreads();
+        if (!zinit && total > 0) {
+            // z state at the first in-tile segment: crossings tau_m < sigma_first already taken
+            zinit = true;
+            if (Z.dk != 0) {
+                const float sf = s_first[col];
+                int m0 = (int)ceilf((sf - Z.t0z) / Z.dtz);
+                m0 = m0 < 0 ? 0 : m0;
+                if (fmaf((float)m0, Z.dtz, Z.t0z) < sf) ++m0;
+                if (m0 > 0 && !(fmaf((float)(m0 - 1), Z.dtz, Z.t0z) < sf)) --m0;
+                kp = (unsigned)(Z.kp + Z.dk * m0);
+                mz = (float)m0;
+                tz = fmaf(mz, Z.dtz, Z.t0z);
             }
-            __syncwarp();
-            if (!zinit && total > 0) {
-                // z state at the first in-tile segment: crossings tau_m < sigma_first already taken
-                zinit = true;
-                if (Z.dk != 0) {
-                    const float sf = s_first[warp];
-                    int m0 = (int)ceilf((sf - Z.t0z) / Z.dtz);
-                    m0 = m0 < 0 ? 0 : m0;
-                    if (fmaf((float)m0, Z.dtz, Z.t0z) < sf) ++m0;
-                    if (m0 > 0 && !(fmaf((float)(m0 - 1), Z.dtz, Z.t0z) < sf)) --m0;
-                    kp = (unsigned)(Z.kp + Z.dk * m0);
-                    mz = (float)m0;
-                    tz = fmaf(mz, Z.dtz, Z.t0z);
-                }
-            }
-            if (live) {
-                // ---- units of each segment: cell k_s, and k_s + dk after the z crossing tz
+        }
+        if (live) {
+            // ---- units of each segment: cell k_s, and k_s + dk after the z crossing tz
 #pragma unroll 4
-                for (int s = 0; s < total; ++s) {
-                    const uint4 raw = *reinterpret_cast<const uint4*>(&seg[s]);
-                    const unsigned long long qptr = ((unsigned long long)raw.y << 32) | raw.x;
-                    const float qse = __uint_as_float(raw.z);
-                    const float qds = __uint_as_float(raw.w);
-                    const bool cross = tz < qse;
-                    if (kAdjoint) {
-                        const float l_e = fmaxf(qse - tz, 0.f);     // C_up - C_low, cell k_e
-                        atomicAdd((float*)(qptr + 4ull * kp), y * (qds - l_e));
-                        if (cross) {
-                            kp += Z.dk;
-                            atomicAdd((float*)(qptr + 4ull * kp), y * l_e);
-                            mz += 1.f;
-                            tz = fmaf(mz, Z.dtz, Z.t0z);
-                        }
-                    } else {
-                        // f_s * d_sigma for the whole segment, then move (sigma_e - tau) to k_e
-                        const float fs = __ldg((const float*)(qptr + 4ull * kp));
-                        acc_s = fmaf(fs, qds, acc_s);
-                        if (cross) {
-                            kp += Z.dk;
-                            const float fe = __ldg((const float*)(qptr + 4ull * kp));
-                            acc_e = fmaf(fe - fs, qse - tz, acc_e);
-                            mz += 1.f;
-                            tz = fmaf(mz, Z.dtz, Z.t0z);
-                        }
+            for (int s = 0; s < total; ++s) {
+                const uint4 raw = *reinterpret_cast<const uint4*>(&seg[s]);
+                const unsigned long long qptr = ((unsigned long long)raw.y << 32) | raw.x;
+                const float qse = __uint_as_float(raw.z);
+                const float qds = __uint_as_float(raw.w);
+                const bool cross = tz < qse;
+                if (kAdjoint) {
+                    const float l_e = fmaxf(qse - tz, 0.f);     // C_up - C_low, cell k_e
+                    atomicAdd((float*)(qptr + 4ull * kp), y * (qds - l_e));
+                    if (cross) {
+                        kp += Z.dk;
+                        atomicAdd((float*)(qptr + 4ull * kp), y * l_e);
+                        mz += 1.f;
+                        tz = fmaf(mz, Z.dtz, Z.t0z);
+                    }
+                } else {
+                    // f_s * d_sigma for the whole segment, then move (sigma_e - tau) to k_e
+                    const float fs = __ldg((const float*)(qptr + 4ull * kp));
+                    acc_s = fmaf(fs, qds, acc_s);
+                    if (cross) {
+                        kp += Z.dk;
+                        const float fe = __ldg((const float*)(qptr + 4ull * kp));
+                        acc_e = fmaf(fe - fs, qse - tz, acc_e);
+                        mz += 1.f;
+                        tz = fmaf(mz, Z.dtz, Z.t0z);
                     }
                 }
             }
-            __syncwarp();
         }
+        __syncthreads();  // the next chunk overwrites the segments
     }
-    if (!kAdjoint && r < dc.rows) {
+    if (!kAdjoint && col_ok && r < dc.rows) {
         const float out = (acc_s + acc_e) * Z.scale;
         if (tiled) { if (out != 0.f) atomicAdd(sino_out + m, out); }
         else sino_out[m] = out;
