@@ -326,6 +326,7 @@ xrt_status xrt_plan_create(const xrt_geometry* g, int cuda_device, xrt_plan* out
                    column_single_crossing(g, G);
     if (p->column_ok) {
         p->zpad = column_zpad(g, G);
+        p->col_cta = xrt::choose_col_cta(D.rows);
         p->nzp = G.n[2] + 2 * p->zpad;
         const size_t bytes = sizeof(float) * (size_t)(G.nxy * p->nzp);
         e = cudaMalloc(&p->d_work_fwd, bytes);

@@ -44,18 +44,10 @@ namespace xrt {
 
 namespace {
 
-#ifndef XRT_COLS_PER_CTA
-#define XRT_COLS_PER_CTA 1
-#endif
-#ifndef XRT_CTA_WARPS
-#define XRT_CTA_WARPS 8
-#endif
 #ifndef XRT_MIN_BLOCKS
 #define XRT_MIN_BLOCKS 4
 #endif
-constexpr int kColsPerCta = XRT_COLS_PER_CTA;               // detector columns per CTA
-constexpr int kRowWarps = XRT_CTA_WARPS / XRT_COLS_PER_CTA;  // warps per column (32 rows each)
-constexpr int kWarps = kColsPerCta * kRowWarps;
+constexpr int kWarps = 8;  // warps per CTA = (detector columns per CTA) x (32-row groups per column)
 constexpr int kSlices = 64;                      // major slices per chunk (2 x 32 lanes)
 
 struct __align__(16) Seg {
@@ -381,7 +373,7 @@ struct ColumnLaunch {
     int nzp, pad;
 };
 
-template <bool kAdjoint>
+template <bool kAdjoint, int kColsPerCta>
 __global__ void __launch_bounds__(kWarps * 32, XRT_MIN_BLOCKS) k_column(const ViewRec* __restrict__ views, DetC dc,
                                                          GridC g, const float* __restrict__ vol,
                                                          float* __restrict__ volw,
@@ -392,6 +384,7 @@ __global__ void __launch_bounds__(kWarps * 32, XRT_MIN_BLOCKS) k_column(const Vi
     // CTA = kColsPerCta detector columns x kRowWarps warps of 32 rows.  The in-plane path of each
     // column is generated cooperatively by its kRowWarps warps (one slice per thread, block-level
     // scan) and shared through shared memory by all of them.
+    constexpr int kRowWarps = kWarps / kColsPerCta;
     constexpr int kChunk = kRowWarps * 32;   // slices per chunk and column
     constexpr int kCap = 2 * kChunk;         // segments per chunk and column
     __shared__ Seg s_seg[kColsPerCta][kCap];
@@ -597,29 +590,37 @@ cudaError_t launch_from_zfast(const xrt_plan_s* p, const float* work, float* img
 
 ColumnLaunch make_launch(const xrt_plan_s* p, int64_t v0, int64_t v1, int& nblk) {
     ColumnLaunch L;
-    const int rows_per_cta = kRowWarps * 32;
+    const int C = p->col_cta;
+    const int rows_per_cta = (kWarps / C) * 32;
     L.n_views = (int)(v1 - v0);
-    L.n_cgroups = (p->det.cols + kColsPerCta - 1) / kColsPerCta;
+    L.n_cgroups = (p->det.cols + C - 1) / C;
     L.n_bands = (p->det.rows + rows_per_cta - 1) / rows_per_cta;
     L.nzp = (int)p->nzp;
     L.pad = (int)p->zpad;
     L.tile = p->tile;
     L.n_tx = p->n_tx;
-    if (p->d_items && v0 == 0 && v1 == p->n_views) {
+    if (p->d_items) {
         L.items = (const uint2*)p->d_items;
         L.n_items = (int)p->n_items;
-        nblk = L.n_items * L.n_bands;
-    } else if (p->d_items) {
-        // view sub-range of a tiled plan (host pipeline chunks): the items of those views
-        L.items = (const uint2*)p->d_items;
-        L.n_items = (int)p->n_items;
-        nblk = L.n_items * L.n_bands;
     } else {
         L.items = nullptr;
         L.n_items = L.n_views * L.n_cgroups;
-        nblk = L.n_items * L.n_bands;
     }
+    nblk = L.n_items * L.n_bands;
     return L;
+}
+
+template <bool kAdj>
+cudaError_t launch_column(const xrt_plan_s* p, const float* vol, float* volw, const float* sino_in,
+                          float* sino_out, int64_t v0, const ColumnLaunch& L, int nblk, cudaStream_t s) {
+    const ColDesc* d = (const ColDesc*)p->d_coldesc;
+    switch (p->col_cta) {
+        case 1: k_column<kAdj, 1><<<nblk, kWarps * 32, 0, s>>>(p->d_views, p->det, p->grid, vol, volw, sino_in, sino_out, (int)v0, d, L); break;
+        case 2: k_column<kAdj, 2><<<nblk, kWarps * 32, 0, s>>>(p->d_views, p->det, p->grid, vol, volw, sino_in, sino_out, (int)v0, d, L); break;
+        case 4: k_column<kAdj, 4><<<nblk, kWarps * 32, 0, s>>>(p->d_views, p->det, p->grid, vol, volw, sino_in, sino_out, (int)v0, d, L); break;
+        default: k_column<kAdj, 8><<<nblk, kWarps * 32, 0, s>>>(p->d_views, p->det, p->grid, vol, volw, sino_in, sino_out, (int)v0, d, L); break;
+    }
+    return cudaGetLastError();
 }
 
 cudaError_t launch_forward_column(const xrt_plan_s* p, const float* vol_zfast, float* sino,
@@ -632,9 +633,7 @@ cudaError_t launch_forward_column(const xrt_plan_s* p, const float* vol_zfast, f
         cudaError_t e = cudaMemsetAsync(sino, 0, sizeof(float) * (size_t)p->n_rays, s);
         if (e != cudaSuccess) return e;
     }
-    k_column<false><<<nblk, kWarps * 32, 0, s>>>(p->d_views, p->det, p->grid, vol_zfast, nullptr,
-                                                nullptr, sino, (int)v0, (const ColDesc*)p->d_coldesc, L);
-    return cudaGetLastError();
+    return launch_column<false>(p, vol_zfast, nullptr, nullptr, sino, v0, L, nblk, s);
 }
 
 cudaError_t launch_adjoint_column(const xrt_plan_s* p, const float* sino, float* vol_zfast,
@@ -643,9 +642,19 @@ cudaError_t launch_adjoint_column(const xrt_plan_s* p, const float* sino, float*
     int nblk = 0;
     ColumnLaunch L = make_launch(p, v0, v1, nblk);
     if (L.items && !(v0 == 0 && v1 == p->n_views)) return cudaErrorInvalidValue;
-    k_column<true><<<nblk, kWarps * 32, 0, s>>>(p->d_views, p->det, p->grid, nullptr, vol_zfast,
-                                               sino, nullptr, (int)v0, (const ColDesc*)p->d_coldesc, L);
-    return cudaGetLastError();
+    return launch_column<true>(p, nullptr, vol_zfast, sino, nullptr, v0, L, nblk, s);
+}
+
+// CTA shape: 32-row groups per column R in {1, 2, 4, 8} with the least idle rows (ties: larger R,
+// i.e. more rays sharing one in-plane path); columns per CTA = 8 / R.
+int choose_col_cta(int rows) {
+    int best_r = 1, best_waste = 1 << 30;
+    for (int R = 1; R <= kWarps; R *= 2) {
+        const int per = 32 * R;
+        const int waste = (rows + per - 1) / per * per - rows;
+        if (waste <= best_waste) { best_waste = waste; best_r = R; }
+    }
+    return kWarps / best_r;
 }
 
 size_t column_desc_bytes() { return sizeof(ColDesc); }
@@ -663,13 +672,14 @@ int build_column_items(const xrt_plan_s* p, const ViewRec* views_host, std::vect
     const GridC& g = p->grid;
     const DetC& dc = p->det;
     const int ts = p->tile, ntx = p->n_tx, nty = p->n_ty;
-    const int ncg = (dc.cols + kColsPerCta - 1) / kColsPerCta;
+    const int C = p->col_cta;
+    const int ncg = (dc.cols + C - 1) / C;
     std::vector<std::vector<uint2>> per_tile((size_t)ntx * nty);
     std::vector<int> mark((size_t)ntx * nty, -1);
     for (int64_t v = 0; v < p->n_views; ++v) {
         for (int cgi = 0; cgi < ncg; ++cgi) {
             const int stamp = (int)(v * ncg + cgi);
-            for (int c = cgi * kColsPerCta; c < std::min(dc.cols, (cgi + 1) * kColsPerCta); ++c) {
+            for (int c = cgi * C; c < std::min(dc.cols, (cgi + 1) * C); ++c) {
                 double qx, qy, ex, ey, ca;
                 column_line(views_host[v], dc, c, qx, qy, ex, ey, ca);
                 const double ux = (qx - g.x_lo) / g.d[0], uy = (g.y_hi - qy) / g.d[1];
