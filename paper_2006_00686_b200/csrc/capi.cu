@@ -143,6 +143,48 @@ int64_t column_zpad(const xrt_geometry* g, const xrt::GridC& G) {
     return pad + 4;
 }
 
+// Largest number of z cells that the rays of one band of `band_rows` detector rows can reach inside
+// the image (over all views).  z of a ray at in-plane distance rho from the source (divergent) or at
+// in-plane arc sigma (parallel) is affine in the row coordinate v, so the extreme rows and extreme
+// rho bound it.  Used only to size the xy tiles (performance), never for correctness.
+double column_band_slab(const xrt_geometry* g, const xrt::GridC& G, int band_rows) {
+    const double hx = G.n[0] * G.d[0] / 2 + std::fabs(g->center[0]);
+    const double hy = G.n[1] * G.d[1] / 2 + std::fabs(g->center[1]);
+    const double R = std::sqrt(hx * hx + hy * hy);
+    double worst = 0.0;
+    for (int64_t r0 = 0; r0 < g->det_rows; r0 += band_rows) {
+        const int64_t r1 = std::min<int64_t>(g->det_rows, r0 + band_rows) - 1;
+        const double v0 = (r0 - (g->det_rows - 1) / 2.0) * g->det_spacing[1] + g->det_offset[1];
+        const double v1 = (r1 - (g->det_rows - 1) / 2.0) * g->det_spacing[1] + g->det_offset[1];
+        double zlo, zhi;
+        if (g->beam == XRT_PAR3D) {
+            const double c2 = std::cos(g->tilt), t2 = std::fabs(std::tan(g->tilt));
+            zlo = std::min(v0, v1) / c2 - R * t2;
+            zhi = std::max(v0, v1) / c2 + R * t2;
+        } else {
+            const double rmin = std::max(0.0, g->sod - R), rmax = g->sod + R;
+            double a[4] = {v0 * rmin / g->sdd, v0 * rmax / g->sdd, v1 * rmin / g->sdd, v1 * rmax / g->sdd};
+            zlo = std::min(std::min(a[0], a[1]), std::min(a[2], a[3]));
+            zhi = std::max(std::max(a[0], a[1]), std::max(a[2], a[3]));
+            if (g->beam == XRT_HELICAL) {
+                double hmin = INFINITY, hmax = -INFINITY;
+                for (int64_t v = 0; v < g->n_views; ++v) {
+                    const double H = g->z0 + g->pitch * g->angles[v] / (2.0 * M_PI);
+                    hmin = std::min(hmin, H);
+                    hmax = std::max(hmax, H);
+                }
+                zlo += hmin;
+                zhi += hmax;
+            }
+        }
+        const double c = g->center[2], half = G.n[2] * G.d[2] / 2;
+        zlo = std::max(zlo, c - half);
+        zhi = std::min(zhi, c + half);
+        worst = std::max(worst, (zhi - zlo) / G.d[2] + 1.0);
+    }
+    return worst;
+}
+
 // The column kernels split an in-plane segment at no more than one z plane: need
 // max segment length (the in-plane unit diagonal) * max |d u_z / d sigma| < 1.
 bool column_single_crossing(const xrt_geometry* g, const xrt::GridC& G) {
@@ -326,7 +368,7 @@ xrt_status xrt_plan_create(const xrt_geometry* g, int cuda_device, xrt_plan* out
                    column_single_crossing(g, G);
     if (p->column_ok) {
         p->zpad = column_zpad(g, G);
-        p->col_cta = xrt::choose_col_cta(D.rows);
+        p->col_np = xrt::choose_col_np(D.rows);
         p->nzp = G.n[2] + 2 * p->zpad;
         const size_t bytes = sizeof(float) * (size_t)(G.nxy * p->nzp);
         e = cudaMalloc(&p->d_work_fwd, bytes);
@@ -336,10 +378,12 @@ xrt_status xrt_plan_create(const xrt_geometry* g, int cuda_device, xrt_plan* out
             e = cudaMalloc(&p->d_coldesc, xrt::column_desc_bytes() * (size_t)(p->n_views * D.cols));
         if (e == cudaSuccess) e = xrt::launch_col_desc(p, (cudaStream_t)0);
         if (e == cudaSuccess) e = cudaDeviceSynchronize();
-        // xy tiling: largest power-of-two tile whose z-fastest columns fit the L2 budget
+        // xy tiling: largest power-of-two tile whose z-fastest columns, restricted to the z slab one
+        // band of detector rows can reach (the kernels run band-major), fit the L2 budget
         const double budget = 64.0 * 1024 * 1024;
+        const double slab = std::min((double)p->nzp, column_band_slab(g, G, 64 * p->col_np) + 2.0);
         int ts = 32;
-        while ((double)(2 * ts) * (2 * ts) * (double)p->nzp * 4.0 <= budget) ts *= 2;
+        while ((double)(2 * ts) * (2 * ts) * slab * 4.0 <= budget) ts *= 2;
         if (const char* f = std::getenv("XRT_COLUMN_TILE")) ts = std::max(4, std::atoi(f));  // testing
         if (ts >= std::max(G.n[0], G.n[1])) {
             p->tile = std::max(G.n[0], G.n[1]);

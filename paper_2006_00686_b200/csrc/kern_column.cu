@@ -44,11 +44,8 @@ namespace xrt {
 
 namespace {
 
-#ifndef XRT_MIN_BLOCKS
-#define XRT_MIN_BLOCKS 4
-#endif
-constexpr int kWarps = 8;  // warps per CTA = (detector columns per CTA) x (32-row groups per column)
-constexpr int kSlices = 64;                      // major slices per chunk (2 x 32 lanes)
+constexpr int kWarps = 8;  // warps per CTA = adjacent detector columns per CTA (one per warp)
+constexpr int kPasses = 4; // 32-slice path-generation passes per chunk (chunk = 128 major slices)
 
 struct __align__(16) Seg {
     unsigned long long ptr;  // address of (cell, padded k = 0) in the z-fastest volume
@@ -297,22 +294,14 @@ __device__ __forceinline__ void load_path(const ColDesc* __restrict__ dsc, int n
     ca = q4.y;
 }
 
-// Per-ray z description along the shared path (sigma from the square entry).  The z cell at sigma is
-// kp(sigma) = kp0 + dk * c(sigma), c = number of z-plane crossings tau_m = t0z + m dtz <= sigma, and is
-// evaluated statelessly: x = fmaf(sigma, A, B) = dk * ((sigma - t0z + dtz) / dtz) - dk / 2 has
-// rint(x) = dk * c, read from the mantissa of x + 1.5 * 2^23 (one FADD); x is small (|x| <= L/dtz
-// + 1), so the decision is made in sigma to within rounding of sigma (well conditioned also for
-// rays almost parallel to the z planes).
-constexpr float kMagic = 12582912.0f;          // 1.5 * 2^23: bits(x + kMagic) = 0x4B400000 + rint(x)
-constexpr unsigned kMagicBits = 0x4B400000u;
-
+// Per-ray z description along the shared path (sigma from the square entry): the z cell at the
+// square entry and the z-plane crossings tau_m = t0z + m dtz, evaluated in sigma (well conditioned
+// also for rays almost parallel to the z planes).
 struct RayZ {
     bool active;      // ray exists (row in range) and the column hits the square
     int kp;           // padded z index (k + pad) of the cell at sigma = 0
     int dk;           // +1 / -1 per z-plane crossing, 0 when z is fixed
     float t0z, dtz;   // z-plane crossings tau_m = t0z + m dtz (INF when fixed)
-    float A, B;       // x(sigma) = fmaf(sigma, A, B), rint(x) = dk * c(sigma)
-    unsigned off;     // kp(sigma) = bits(x + kMagic) + off  (off = kp0 - kMagicBits, mod 2^32)
     float scale;      // 1 / cos(beta): physical length per unit sigma
 };
 
@@ -320,7 +309,6 @@ __device__ __forceinline__ void ray_z(const ViewRec& V, const DetC& dc, const Gr
                                       const ColumnPath& P, double ca, int r, int pad, RayZ& Z) {
     Z.active = false;
     Z.kp = pad; Z.dk = 0; Z.t0z = INFINITY; Z.dtz = 0.f; Z.scale = 1.f;
-    Z.A = 0.f; Z.B = 0.f; Z.off = (unsigned)pad - kMagicBits;
     if (r >= dc.rows || !P.hit) return;
     const double v = ((double)r - dc.cv) * dc.dv + dc.off_v;
     double tb, z0;  // tan(beta), z at absolute sigma 0
@@ -342,7 +330,6 @@ __device__ __forceinline__ void ray_z(const ViewRec& V, const DetC& dc, const Gr
         double kk = floor((g.z_hi - z0) / g.d[2]);
         kk = fmin(fmax(kk, (double)(-pad)), (double)(g.n[2] + pad - 1));
         Z.kp = (int)kk + pad;
-        Z.off = (unsigned)Z.kp - kMagicBits;
     } else {
         const double uz0 = (g.z_hi - (z0 + P.sig_in * tb)) * g.inv_dz;   // u_z at sigma = 0
         const double iw = -g.d[2] * __drcp_rn(tb);                          // 1 / (d u_z / d sigma)
@@ -354,11 +341,6 @@ __device__ __forceinline__ void ray_z(const ViewRec& V, const DetC& dc, const Gr
         Z.t0z = (float)t0;
         Z.dtz = (float)dt;
         Z.dk = iw > 0.0 ? 1 : -1;
-        // c(sigma) = floor((sigma - (t0 - dt)) / dt): x = dk * (sigma - t0 + dt) / dt - dk / 2
-        const double idt = 1.0 / dt;
-        Z.A = (float)(Z.dk * idt);
-        Z.B = (float)(Z.dk * ((dt - t0) * idt - 0.5));
-        Z.off = (unsigned)Z.kp - kMagicBits;
     }
     Z.active = true;
 }
@@ -373,31 +355,196 @@ struct ColumnLaunch {
     int nzp, pad;
 };
 
-template <bool kAdjoint, int kColsPerCta>
-__global__ void __launch_bounds__(kWarps * 32, XRT_MIN_BLOCKS) k_column(const ViewRec* __restrict__ views, DetC dc,
-                                                         GridC g, const float* __restrict__ vol,
-                                                         float* __restrict__ volw,
-                                                         const float* __restrict__ sino_in,
-                                                         float* __restrict__ sino_out, int view0,
-                                                         const ColDesc* __restrict__ desc,
-                                                         ColumnLaunch L) {
-    // CTA = kColsPerCta detector columns x kRowWarps warps of 32 rows.  The in-plane path of each
-    // column is generated cooperatively by its kRowWarps warps (one slice per thread, block-level
-    // scan) and shared through shared memory by all of them.
-    constexpr int kRowWarps = kWarps / kColsPerCta;
-    constexpr int kChunk = kRowWarps * 32;   // slices per chunk and column
-    constexpr int kCap = 2 * kChunk;         // segments per chunk and column
-    __shared__ Seg s_seg[kColsPerCta][kCap];
-    __shared__ int s_wtot[kWarps];
-    __shared__ int s_nch[kColsPerCta];
-    __shared__ float s_first[kColsPerCta];
+// z state of two rays of one lane (rows lane + 32 q), packed so the per-segment arithmetic of the
+// pair issues as f32x2 instructions (FADD2 / FFMA2 / FMUL2).  The padded z cell is carried as the
+// float kp + 1.5 * 2^23, whose bit pattern is 0x4B400000 + kp: a crossing adds +-1.0 (exact), and
+// the segment pointers are stored pre-offset by -4 * 0x4B400000 bytes, so the address of the cell is
+// ptr + 4 * bits(kpf) with no float -> int conversion.
+constexpr float kMagic = 12582912.0f;          // 1.5 * 2^23
+constexpr unsigned kMagicBits = 0x4B400000u;   // bits(kMagic)
+constexpr float kNoCross = -1.0e30f;           // -(next crossing) of a ray with fixed z (finite: x * 0 = 0)
+
+struct RayPair {
+    float2 ntz;        // -(next z-plane crossing) = -(t0z + mz dtz)
+    float2 mz;         // z-plane crossings taken so far
+    float2 ndtz, nt0z; // -dtz, -t0z   (0, kNoCross when z is fixed)
+    float2 kpf;        // padded z cell of the current segment, + kMagic
+    float2 dkf;        // +-1 per crossing (0 when fixed), as float
+    float2 acc0, acc1; // forward: sum f_s d_sigma, sum (f_e - f_s)(sigma_e - tau)
+    float2 w;          // forward: 1 / cos(beta); adjoint: y / cos(beta)
+    int dk0, dk1;      // +-1 / 0 as int (neighbour offset in the mixed-direction loop)
+    bool live0, live1; // ray exists and (adjoint) carries a non-zero value
+};
+
+__device__ __forceinline__ void pair_init(RayPair& P, const RayZ& Za, const RayZ& Zb, float ya, float yb,
+                                          bool kAdj) {
+    P.kpf = make_float2((float)Za.kp + kMagic, (float)Zb.kp + kMagic);
+    P.dk0 = Za.dk; P.dk1 = Zb.dk;
+    P.dkf = make_float2((float)Za.dk, (float)Zb.dk);
+    P.mz = make_float2(0.f, 0.f);
+    P.ndtz = make_float2(Za.dk ? -Za.dtz : 0.f, Zb.dk ? -Zb.dtz : 0.f);
+    P.nt0z = make_float2(Za.dk ? -Za.t0z : kNoCross, Zb.dk ? -Zb.t0z : kNoCross);
+    P.ntz = P.nt0z;
+    P.acc0 = make_float2(0.f, 0.f);
+    P.acc1 = make_float2(0.f, 0.f);
+    P.w = kAdj ? make_float2(ya * Za.scale, yb * Zb.scale) : make_float2(Za.scale, Zb.scale);
+    P.live0 = Za.active && (!kAdj || ya != 0.f);
+    P.live1 = Zb.active && (!kAdj || yb != 0.f);
+}
+
+// z state at sigma_first (the first in-tile segment start): crossings tau_m < sigma_first taken.
+__device__ __forceinline__ void z_skip(float& kpf, int dk, float& mzv, float& ntzv, float ndtz, float nt0z,
+                                       float sf) {
+    if (dk == 0) return;
+    const float t0z = -nt0z, dtz = -ndtz;
+    int m0 = (int)ceilf((sf - t0z) / dtz);
+    m0 = m0 < 0 ? 0 : m0;
+    if (fmaf((float)m0, dtz, t0z) < sf) ++m0;
+    if (m0 > 0 && !(fmaf((float)(m0 - 1), dtz, t0z) < sf)) --m0;
+    kpf += (float)(dk * m0);
+    mzv = (float)m0;
+    ntzv = -fmaf(mzv, dtz, t0z);
+}
+
+// 1.0f if x > 0 else 0.0f (one FSET)
+__device__ __forceinline__ float gt0(float x) {
+    float r;
+    asm("set.gt.f32.f32 %0, %1, 0f00000000;" : "=f"(r) : "f"(x));
+    return r;
+}
+
+// Units of the chunk's segments for the lane's 2*NP rays.  Per segment (cell, sigma_e, d_sigma)
+// and ray: the cell k_s at the segment start and, if the ray's next z crossing tau < sigma_e, the
+// cell k_s + dk; l_e = max(sigma_e - tau, 0) and l_s = d_sigma - l_e are C_up - C_low of the two
+// units (eq:range_length_3D).  DK = +1 / -1: every ray of the warp steps that way (or is
+// fixed), so the neighbour cell is an immediate offset; DK = 0: per-ray offsets.
+__device__ __forceinline__ uint4 lds128(const Seg* p) {
+    uint4 raw;   // one 128-bit shared load per segment (broadcast to the warp)
+    asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(raw.x), "=r"(raw.y), "=r"(raw.z), "=r"(raw.w)
+                 : "r"((unsigned)__cvta_generic_to_shared(p)));
+    return raw;
+}
+
+__device__ __forceinline__ unsigned long long seg_ptr(const uint4& raw) {
+    return ((unsigned long long)raw.y << 32) | raw.x;
+}
+
+// z crossing inside the segment: cr = 1 if tau < sigma_e, lm = l_e = max(sigma_e - tau, 0); then
+// the ray's z state advances to the next segment.
+template <int DK>
+__device__ __forceinline__ void z_step(RayPair& P, const float2 se2, float2& cr, float2& lm) {
+    const float2 m1 = make_float2(-1.f, -1.f);
+    const float2 le = __fadd2_rn(se2, P.ntz);               // sigma_e - tau
+    cr = make_float2(gt0(le.x), gt0(le.y));
+    lm = __fmul2_rn(le, cr);
+    if (DK > 0) P.kpf = __fadd2_rn(P.kpf, cr);
+    else if (DK < 0) P.kpf = __ffma2_rn(cr, m1, P.kpf);
+    else P.kpf = __ffma2_rn(cr, P.dkf, P.kpf);
+    P.mz = __fadd2_rn(P.mz, cr);
+    P.ntz = __ffma2_rn(P.mz, P.ndtz, P.nt0z);                 // -(t0z + mz dtz)
+}
+
+// Forward units of the chunk's segments for the lane's 2*NP rays.  Per segment (cell, sigma_e,
+// d_sigma) and ray: the cell k_s at the segment start and, if the ray's next z crossing
+// tau < sigma_e, the cell k_s + dk; l_e = max(sigma_e - tau, 0) and l_s = d_sigma - l_e are
+// C_up - C_low of the two units (eq:range_length_3D):
+//     acc += f_s d_sigma + (f_e - f_s) l_e.
+// DK = +1 / -1: every ray of the warp steps that way (or is fixed), so the neighbour cell is an
+// immediate offset; DK = 0: per-ray offsets.  Software-pipelined one segment deep: the z state
+// decides the next segment's cells before this segment's arithmetic, so the next loads are in
+// flight while this segment's values are consumed.
+template <int NP, int DK>
+__device__ __forceinline__ void column_segments_fwd(const Seg* __restrict__ seg, int total, RayPair (&P)[NP]) {
+    const float2 m1 = make_float2(-1.f, -1.f);
+    uint4 raw = lds128(&seg[0]);
+    float2 f0[NP], f1[NP];
+#pragma unroll
+    for (int p = 0; p < NP; ++p) {
+        const float* a0 = (const float*)(seg_ptr(raw) + 4ull * __float_as_uint(P[p].kpf.x));
+        const float* a1 = (const float*)(seg_ptr(raw) + 4ull * __float_as_uint(P[p].kpf.y));
+        const int o0 = DK != 0 ? DK : P[p].dk0, o1 = DK != 0 ? DK : P[p].dk1;
+        f0[p] = make_float2(__ldg(a0), __ldg(a1));
+        f1[p] = make_float2(__ldg(a0 + o0), __ldg(a1 + o1));
+    }
+#pragma unroll 2
+    for (int s = 0; s < total; ++s) {
+        const float qse = __uint_as_float(raw.z), qds = __uint_as_float(raw.w);
+        const float2 se2 = make_float2(qse, qse), ds2 = make_float2(qds, qds);
+        const uint4 nraw = lds128(&seg[min(s + 1, total - 1)]);   // last trip: harmless reload
+#pragma unroll
+        for (int p = 0; p < NP; ++p) {
+            float2 cr, lm;
+            z_step<DK>(P[p], se2, cr, lm);
+            // next segment's loads (cells from the advanced z state)
+            const float* a0 = (const float*)(seg_ptr(nraw) + 4ull * __float_as_uint(P[p].kpf.x));
+            const float* a1 = (const float*)(seg_ptr(nraw) + 4ull * __float_as_uint(P[p].kpf.y));
+            const int o0 = DK != 0 ? DK : P[p].dk0, o1 = DK != 0 ? DK : P[p].dk1;
+            const float2 g0 = make_float2(__ldg(a0), __ldg(a1));
+            const float2 g1 = make_float2(__ldg(a0 + o0), __ldg(a1 + o1));
+            // this segment's arithmetic
+            P[p].acc0 = __ffma2_rn(f0[p], ds2, P[p].acc0);        // f_s * d_sigma
+            const float2 d = __ffma2_rn(f0[p], m1, f1[p]);        // f_e - f_s
+            P[p].acc1 = __ffma2_rn(d, lm, P[p].acc1);             // (f_e - f_s) * l_e
+            f0[p] = g0;
+            f1[p] = g1;
+        }
+        raw = nraw;
+    }
+}
+
+// Adjoint: the same units, y l scattered with red.global.add (the second unit only when the z
+// crossing lies inside the segment).
+template <int NP, int DK>
+__device__ __forceinline__ void column_segments_adj(const Seg* __restrict__ seg, int total, RayPair (&P)[NP]) {
+    const float2 m1 = make_float2(-1.f, -1.f);
+#pragma unroll 2
+    for (int s = 0; s < total; ++s) {
+        const uint4 raw = lds128(&seg[s]);
+        const float qse = __uint_as_float(raw.z), qds = __uint_as_float(raw.w);
+        const float2 se2 = make_float2(qse, qse), ds2 = make_float2(qds, qds);
+#pragma unroll
+        for (int p = 0; p < NP; ++p) {
+            float* a0 = (float*)(seg_ptr(raw) + 4ull * __float_as_uint(P[p].kpf.x));
+            float* a1 = (float*)(seg_ptr(raw) + 4ull * __float_as_uint(P[p].kpf.y));
+            const int o0 = DK != 0 ? DK : P[p].dk0, o1 = DK != 0 ? DK : P[p].dk1;
+            float2 cr, lm;
+            z_step<DK>(P[p], se2, cr, lm);
+            const float2 ls = __ffma2_rn(lm, m1, ds2);               // l_s = d_sigma - l_e
+            const float2 ws = __fmul2_rn(P[p].w, ls), we = __fmul2_rn(P[p].w, lm);
+            if (P[p].live0) atomicAdd(a0, ws.x);
+            if (P[p].live1) atomicAdd(a1, ws.y);
+            if (P[p].live0 && cr.x != 0.f) atomicAdd(a0 + o0, we.x);
+            if (P[p].live1 && cr.y != 0.f) atomicAdd(a1 + o1, we.y);
+        }
+    }
+}
+
+// CTA = kWarps adjacent detector columns of one view, one band of 64 NP rows, one xy tile.  Each
+// warp owns one column: it generates the column's in-plane path chunk by chunk (lane = one major
+// slice, warp scan, segments in its own shared-memory buffer; no CTA barrier) and walks it for its
+// 2 NP rays per lane (rows band*64NP + 32q + lane: adjacent rows in adjacent lanes, so the lanes'
+// loads of one segment fall on consecutive addresses of the z-fastest volume).
+#ifndef XRT_COL_MINB
+#define XRT_COL_MINB 2
+#endif
+
+template <bool kAdjoint, int NP>
+__global__ void __launch_bounds__(kWarps * 32, XRT_COL_MINB) k_column(const ViewRec* __restrict__ views, DetC dc, GridC g,
+                                                       const float* __restrict__ vol, float* __restrict__ volw,
+                                                       const float* __restrict__ sino_in,
+                                                       float* __restrict__ sino_out, int view0,
+                                                       const ColDesc* __restrict__ desc, ColumnLaunch L) {
+    constexpr int R = 2 * NP;
+    __shared__ Seg s_seg[kWarps][2 * 32 * kPasses];
+    __shared__ float s_first[kWarps];
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
-    const int col = warp / kRowWarps;        // column of this warp inside the CTA
-    const int sub = warp % kRowWarps;        // row group of this warp inside the column
     const unsigned bid = blockIdx.x;
-    const int band = (int)(bid % (unsigned)L.n_bands);
-    const unsigned it = bid / (unsigned)L.n_bands;
+    // band-major order: every view / column / tile of one band of detector rows (one z slab of
+    // the volume) runs before the next band, so the volume working set is that slab
+    const int band = (int)(bid / (unsigned)L.n_items);
+    const unsigned it = bid % (unsigned)L.n_items;
     int vv, cg, ti0 = 0, ti1 = g.n[0], tj0 = 0, tj1 = g.n[1];
     if (L.items) {
         const uint2 w = L.items[it];
@@ -411,26 +558,19 @@ __global__ void __launch_bounds__(kWarps * 32, XRT_MIN_BLOCKS) k_column(const Vi
         vv = (int)(it / (unsigned)L.n_cgroups);
     }
     const bool tiled = L.items != nullptr;
-    const int c = cg * kColsPerCta + col;
-    const int r = (band * kRowWarps + sub) * 32 + lane;
+    const int c = cg * kWarps + warp;
+    if (c >= dc.cols) return;                      // warp-uniform; no CTA barrier below
     const int v = view0 + vv;
-    const bool col_ok = c < dc.cols;
     const ViewRec V = views[v];
-    ColumnPath P;
+    ColumnPath Pth;
     double ca = 1.0;
     float pux = 0.f, puy = 0.f, pwx = 0.f, pwy = 0.f;
-    if (col_ok) load_path(desc + ((int64_t)v * dc.cols + c), g.n[0], P, ca, pux, puy, pwx, pwy);
-    else { P.hit = false; P.n_slices = 0; }
-    RayZ Z;
-    ray_z(V, dc, g, P, ca, r, L.pad, Z);
-    const int64_t m = ((int64_t)v * dc.rows + r) * dc.cols + c;
-    float y = 0.f;
-    if (kAdjoint && Z.active) y = sino_in[m] * Z.scale;
-    const bool live = kAdjoint ? (Z.active && y != 0.f) : Z.active;
+    load_path(desc + ((int64_t)v * dc.cols + c), g.n[0], Pth, ca, pux, puy, pwx, pwy);
+    if (!Pth.hit) return;
     // slice range of the tile: clip the in-plane line to the tile box, then widen (segments
     // outside the tile are filtered exactly by slice_segments)
-    int na = 0, nb = P.hit ? P.n_slices : 0;
-    if (tiled && P.hit) {
+    int na = 0, nb = Pth.n_slices;
+    if (tiled) {
         float lo = -INFINITY, hi = INFINITY;
         if (pwx != 0.f) {
             const float a0 = (ti0 - pux) / pwx, a1 = (ti1 - pux) / pwx;
@@ -440,110 +580,99 @@ __global__ void __launch_bounds__(kWarps * 32, XRT_MIN_BLOCKS) k_column(const Vi
             const float a0 = (tj0 - puy) / pwy, a1 = (tj1 - puy) / pwy;
             lo = fmaxf(lo, fminf(a0, a1)); hi = fminf(hi, fmaxf(a0, a1));
         } else if (!(puy >= tj0 - 1e-3f && puy <= tj1 + 1e-3f)) { hi = -INFINITY; }
-        if (!(hi >= lo)) { na = nb = 0; }
-        else {
-            const float ida = 1.f / P.dta;
-            na = max(0, __float2int_rd((lo - P.t0a) * ida) - 1);
-            nb = min(P.n_slices, __float2int_rd((hi - P.t0a) * ida) + 3);
-        }
+        if (!(hi >= lo)) return;
+        const float ida = 1.f / Pth.dta;
+        na = max(0, __float2int_rd((lo - Pth.t0a) * ida) - 1);
+        nb = min(Pth.n_slices, __float2int_rd((hi - Pth.t0a) * ida) + 3);
     }
-    // CTA-uniform chunk count (the loop contains __syncthreads)
-    if (sub == 0 && lane == 0) s_nch[col] = nb > na ? (nb - na + kChunk - 1) / kChunk : 0;
-    __syncthreads();
-    int nch = 0;
+    // the lane's rays: rows (band * R + q) * 32 + lane
+    RayPair P[NP];
+    bool any_live = false, pos = true, neg = true;
 #pragma unroll
-    for (int q = 0; q < kColsPerCta; ++q) nch = max(nch, s_nch[q]);
-    float acc_s = 0.f, acc_e = 0.f;
-    Seg* seg = s_seg[col];
-    const unsigned long long base = (unsigned long long)(kAdjoint ? (const float*)volw : vol);
+    for (int p = 0; p < NP; ++p) {
+        RayZ Za, Zb;
+        const int ra = (band * R + 2 * p) * 32 + lane, rb = ra + 32;
+        ray_z(V, dc, g, Pth, ca, ra, L.pad, Za);
+        ray_z(V, dc, g, Pth, ca, rb, L.pad, Zb);
+        const float ya = (kAdjoint && Za.active) ? sino_in[((int64_t)v * dc.rows + ra) * dc.cols + c] : 0.f;
+        const float yb = (kAdjoint && Zb.active) ? sino_in[((int64_t)v * dc.rows + rb) * dc.cols + c] : 0.f;
+        pair_init(P[p], Za, Zb, ya, yb, kAdjoint);
+        any_live |= P[p].live0 | P[p].live1;
+        pos &= Za.dk >= 0 && Zb.dk >= 0;
+        neg &= Za.dk <= 0 && Zb.dk <= 0;
+    }
+    if (!__any_sync(0xffffffffu, any_live)) return;
+    // warp-uniform z stepping direction
+    const int mode = __all_sync(0xffffffffu, pos) ? 1 : (__all_sync(0xffffffffu, neg) ? -1 : 0);
+    Seg* seg = s_seg[warp];
+    // segment pointers pre-offset by -4 kMagicBits bytes (see RayPair)
+    const unsigned long long base = (unsigned long long)(kAdjoint ? (const float*)volw : vol) -
+                                    4ull * kMagicBits;
     const unsigned long long cstride = 4ull * (unsigned long long)L.nzp;
-    unsigned kp = (unsigned)Z.kp;
-    float tz = Z.t0z, mz = 0.f;
     bool zinit = !tiled;  // untiled: the z state at sigma = 0 is the initial one
-    for (int ich = 0; ich < nch; ++ich) {
-        // ---- block-cooperative: slice n = na + ich*kChunk + sub*32 + lane -> in-tile segments
-        const int n = na + ich * kChunk + sub * 32 + lane;
-        float a0s = 0.f, a0e = 0.f, a1s = 0.f, a1e = 0.f;
-        int c0 = 0, c1 = 0, cnt = 0;
-        if (n < nb) cnt = slice_segments(P, n, ti0, ti1, tj0, tj1, a0s, a0e, c0, a1s, a1e, c1);
-        int incl = cnt;
+    for (int n0 = na; n0 < nb; n0 += 32 * kPasses) {
+        // ---- warp-cooperative: kPasses passes of 32 slices (slice n = n0 + 32 pass + lane) ->
+        //      in-tile segments, in path order
+        int total = 0;
 #pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const int t = __shfl_up_sync(0xffffffffu, incl, o);
-            if (lane >= o) incl += t;
-        }
-        if (lane == 31) s_wtot[warp] = incl;
-        __syncthreads();
-        int before = 0, total = 0;
+        for (int pass = 0; pass < kPasses; ++pass) {
+            const int n = n0 + 32 * pass + lane;
+            if (n0 + 32 * pass >= nb) break;   // warp-uniform
+            float a0s = 0.f, a0e = 0.f, a1s = 0.f, a1e = 0.f;
+            int c0 = 0, c1 = 0, cnt = 0;
+            if (n < nb) cnt = slice_segments(Pth, n, ti0, ti1, tj0, tj1, a0s, a0e, c0, a1s, a1e, c1);
+            int incl = cnt;
 #pragma unroll
-        for (int q = 0; q < kRowWarps; ++q) {
-            const int wt = s_wtot[col * kRowWarps + q];
-            before += q < sub ? wt : 0;
-            total += wt;
-        }
-        const int b = before + incl - cnt;
-        if (cnt > 0) {
-            Seg q; q.ptr = base + cstride * (unsigned)c0; q.se = a0e; q.ds = a0e - a0s;
-            seg[b] = q;
-            if (b == 0) s_first[col] = a0s;
-        }
-        if (cnt > 1) {
-            Seg q; q.ptr = base + cstride * (unsigned)c1; q.se = a1e; q.ds = a1e - a1s;
-            seg[b + 1] = q;
-        }
-        __syncthreads();
-        if (!zinit && total > 0) {
-            // z state at the first in-tile segment: crossings tau_m < sigma_first already taken
-            zinit = true;
-            if (Z.dk != 0) {
-                const float sf = s_first[col];
-                int m0 = (int)ceilf((sf - Z.t0z) / Z.dtz);
-                m0 = m0 < 0 ? 0 : m0;
-                if (fmaf((float)m0, Z.dtz, Z.t0z) < sf) ++m0;
-                if (m0 > 0 && !(fmaf((float)(m0 - 1), Z.dtz, Z.t0z) < sf)) --m0;
-                kp = (unsigned)(Z.kp + Z.dk * m0);
-                mz = (float)m0;
-                tz = fmaf(mz, Z.dtz, Z.t0z);
+            for (int o = 1; o < 32; o <<= 1) {
+                const int t = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += t;
             }
+            const int b = total + incl - cnt;
+            if (cnt > 0) {
+                Seg q; q.ptr = base + cstride * (unsigned)c0; q.se = a0e; q.ds = a0e - a0s;
+                seg[b] = q;
+                if (b == 0) s_first[warp] = a0s;
+            }
+            if (cnt > 1) {
+                Seg q; q.ptr = base + cstride * (unsigned)c1; q.se = a1e; q.ds = a1e - a1s;
+                seg[b + 1] = q;
+            }
+            total += __shfl_sync(0xffffffffu, incl, 31);
         }
-        if (live) {
-            // ---- units of each segment: cell k_s, and k_s + dk after the z crossing tz
-#pragma unroll 4
-            for (int s = 0; s < total; ++s) {
-                const uint4 raw = *reinterpret_cast<const uint4*>(&seg[s]);
-                const unsigned long long qptr = ((unsigned long long)raw.y << 32) | raw.x;
-                const float qse = __uint_as_float(raw.z);
-                const float qds = __uint_as_float(raw.w);
-                const bool cross = tz < qse;
-                if (kAdjoint) {
-                    const float l_e = fmaxf(qse - tz, 0.f);     // C_up - C_low, cell k_e
-                    atomicAdd((float*)(qptr + 4ull * kp), y * (qds - l_e));
-                    if (cross) {
-                        kp += Z.dk;
-                        atomicAdd((float*)(qptr + 4ull * kp), y * l_e);
-                        mz += 1.f;
-                        tz = fmaf(mz, Z.dtz, Z.t0z);
-                    }
-                } else {
-                    // f_s * d_sigma for the whole segment, then move (sigma_e - tau) to k_e
-                    const float fs = __ldg((const float*)(qptr + 4ull * kp));
-                    acc_s = fmaf(fs, qds, acc_s);
-                    if (cross) {
-                        kp += Z.dk;
-                        const float fe = __ldg((const float*)(qptr + 4ull * kp));
-                        acc_e = fmaf(fe - fs, qse - tz, acc_e);
-                        mz += 1.f;
-                        tz = fmaf(mz, Z.dtz, Z.t0z);
-                    }
+        __syncwarp();
+        if (total > 0) {
+            if (!zinit) {
+                zinit = true;
+                const float sf = s_first[warp];
+#pragma unroll
+                for (int p = 0; p < NP; ++p) {
+                    z_skip(P[p].kpf.x, P[p].dk0, P[p].mz.x, P[p].ntz.x, P[p].ndtz.x, P[p].nt0z.x, sf);
+                    z_skip(P[p].kpf.y, P[p].dk1, P[p].mz.y, P[p].ntz.y, P[p].ndtz.y, P[p].nt0z.y, sf);
                 }
             }
+            if (kAdjoint) {
+                if (mode > 0) column_segments_adj<NP, 1>(seg, total, P);
+                else if (mode < 0) column_segments_adj<NP, -1>(seg, total, P);
+                else column_segments_adj<NP, 0>(seg, total, P);
+            } else {
+                if (mode > 0) column_segments_fwd<NP, 1>(seg, total, P);
+                else if (mode < 0) column_segments_fwd<NP, -1>(seg, total, P);
+                else column_segments_fwd<NP, 0>(seg, total, P);
+            }
         }
-        __syncthreads();  // the next chunk overwrites the segments
+        __syncwarp();  // the next chunk overwrites the segments
     }
-    if (!kAdjoint && col_ok && r < dc.rows) {
-        const float out = (acc_s + acc_e) * Z.scale;
-        if (tiled) { if (out != 0.f) atomicAdd(sino_out + m, out); }
-        else sino_out[m] = out;
+    if (!kAdjoint) {
+#pragma unroll
+        for (int q = 0; q < R; ++q) {
+            const RayPair& Q = P[q >> 1];
+            if (!((q & 1) ? Q.live1 : Q.live0)) continue;
+            const float a = (q & 1) ? Q.acc0.y + Q.acc1.y : Q.acc0.x + Q.acc1.x;
+            const float out = a * ((q & 1) ? Q.w.y : Q.w.x);
+            const int64_t m = ((int64_t)v * dc.rows + (band * R + q) * 32 + lane) * dc.cols + c;
+            if (tiled) { if (out != 0.f) atomicAdd(sino_out + m, out); }
+            else sino_out[m] = out;
+        }
     }
 }
 
@@ -590,11 +719,10 @@ cudaError_t launch_from_zfast(const xrt_plan_s* p, const float* work, float* img
 
 ColumnLaunch make_launch(const xrt_plan_s* p, int64_t v0, int64_t v1, int& nblk) {
     ColumnLaunch L;
-    const int C = p->col_cta;
-    const int rows_per_cta = (kWarps / C) * 32;
+    const int rows_per_band = 64 * p->col_np;
     L.n_views = (int)(v1 - v0);
-    L.n_cgroups = (p->det.cols + C - 1) / C;
-    L.n_bands = (p->det.rows + rows_per_cta - 1) / rows_per_cta;
+    L.n_cgroups = (p->det.cols + kWarps - 1) / kWarps;
+    L.n_bands = (p->det.rows + rows_per_band - 1) / rows_per_band;
     L.nzp = (int)p->nzp;
     L.pad = (int)p->zpad;
     L.tile = p->tile;
@@ -614,12 +742,11 @@ template <bool kAdj>
 cudaError_t launch_column(const xrt_plan_s* p, const float* vol, float* volw, const float* sino_in,
                           float* sino_out, int64_t v0, const ColumnLaunch& L, int nblk, cudaStream_t s) {
     const ColDesc* d = (const ColDesc*)p->d_coldesc;
-    switch (p->col_cta) {
-        case 1: k_column<kAdj, 1><<<nblk, kWarps * 32, 0, s>>>(p->d_views, p->det, p->grid, vol, volw, sino_in, sino_out, (int)v0, d, L); break;
-        case 2: k_column<kAdj, 2><<<nblk, kWarps * 32, 0, s>>>(p->d_views, p->det, p->grid, vol, volw, sino_in, sino_out, (int)v0, d, L); break;
-        case 4: k_column<kAdj, 4><<<nblk, kWarps * 32, 0, s>>>(p->d_views, p->det, p->grid, vol, volw, sino_in, sino_out, (int)v0, d, L); break;
-        default: k_column<kAdj, 8><<<nblk, kWarps * 32, 0, s>>>(p->d_views, p->det, p->grid, vol, volw, sino_in, sino_out, (int)v0, d, L); break;
-    }
+    if (nblk <= 0) return cudaSuccess;
+    if (p->col_np == 1)
+        k_column<kAdj, 1><<<nblk, kWarps * 32, 0, s>>>(p->d_views, p->det, p->grid, vol, volw, sino_in, sino_out, (int)v0, d, L);
+    else
+        k_column<kAdj, 2><<<nblk, kWarps * 32, 0, s>>>(p->d_views, p->det, p->grid, vol, volw, sino_in, sino_out, (int)v0, d, L);
     return cudaGetLastError();
 }
 
@@ -629,10 +756,9 @@ cudaError_t launch_forward_column(const xrt_plan_s* p, const float* vol_zfast, f
     int nblk = 0;
     ColumnLaunch L = make_launch(p, v0, v1, nblk);
     if (L.items && !(v0 == 0 && v1 == p->n_views)) return cudaErrorInvalidValue;
-    if (L.items) {
-        cudaError_t e = cudaMemsetAsync(sino, 0, sizeof(float) * (size_t)p->n_rays, s);
-        if (e != cudaSuccess) return e;
-    }
+    // rays whose column misses the image (or, tiled, every ray: partial sums) need zeros
+    cudaError_t e = cudaMemsetAsync(sino + v0 * p->det.per_view, 0, sizeof(float) * (size_t)((v1 - v0) * p->det.per_view), s);
+    if (e != cudaSuccess) return e;
     return launch_column<false>(p, vol_zfast, nullptr, nullptr, sino, v0, L, nblk, s);
 }
 
@@ -645,17 +771,19 @@ cudaError_t launch_adjoint_column(const xrt_plan_s* p, const float* sino, float*
     return launch_column<true>(p, nullptr, vol_zfast, sino, nullptr, v0, L, nblk, s);
 }
 
-// CTA shape: 32-row groups per column R in {1, 2, 4, 8} with the least idle rows (ties: larger R,
-// i.e. more rays sharing one in-plane path); columns per CTA = 8 / R.
-int choose_col_cta(int rows) {
-    int best_r = 1, best_waste = 1 << 30;
-    for (int R = 1; R <= kWarps; R *= 2) {
-        const int per = 32 * R;
+// Rays per lane 2 NP, NP in {1, 2}: the fewest idle rows in the last band of 64 NP rows (ties:
+// more rays per lane, i.e. each segment descriptor shared by more rays).
+int choose_col_np(int rows) {
+    int best = 1, best_waste = 1 << 30;
+    for (int np = 1; np <= 2; ++np) {
+        const int per = 64 * np;
         const int waste = (rows + per - 1) / per * per - rows;
-        if (waste <= best_waste) { best_waste = waste; best_r = R; }
+        if (waste <= best_waste) { best_waste = waste; best = np; }
     }
-    return kWarps / best_r;
+    return best;
 }
+
+int column_cta_columns() { return kWarps; }
 
 size_t column_desc_bytes() { return sizeof(ColDesc); }
 
@@ -672,7 +800,7 @@ int build_column_items(const xrt_plan_s* p, const ViewRec* views_host, std::vect
     const GridC& g = p->grid;
     const DetC& dc = p->det;
     const int ts = p->tile, ntx = p->n_tx, nty = p->n_ty;
-    const int C = p->col_cta;
+    const int C = kWarps;
     const int ncg = (dc.cols + C - 1) / C;
     std::vector<std::vector<uint2>> per_tile((size_t)ntx * nty);
     std::vector<int> mark((size_t)ntx * nty, -1);

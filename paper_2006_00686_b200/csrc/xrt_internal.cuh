@@ -189,7 +189,7 @@ struct xrt_plan_s {
     float* d_work_adj = nullptr;       // z-fastest, z-padded adjoint accumulator (COLUMN)
     int64_t zpad = 0, nzp = 0;         // z padding per side and padded column length
     int tile = 0, n_tx = 1, n_ty = 1;  // xy tiling of the column kernels (L2 residency)
-    int col_cta = 1;                   // detector columns per CTA of the column kernels
+    int col_np = 2;                    // ray pairs per lane of the column kernels (rows per band = 64 col_np)
     void* d_items = nullptr;           // device uint2 work list (tiled) or nullptr
     void* d_coldesc = nullptr;         // per-(view, column) path descriptors (COLUMN)
     int64_t n_items = 0;
@@ -225,6 +225,7 @@ cudaError_t launch_adjoint_column(const xrt_plan_s* p, const float* sino, float*
 namespace xrt {
 int build_column_items(const xrt_plan_s* p, const ViewRec* views_host, std::vector<uint2>& items);
 size_t column_desc_bytes();
-int choose_col_cta(int rows);
+int choose_col_np(int rows);
+int column_cta_columns();
 cudaError_t launch_col_desc(const xrt_plan_s* p, cudaStream_t s);
 }  // namespace xrt
