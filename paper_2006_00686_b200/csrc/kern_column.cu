@@ -406,6 +406,12 @@ __device__ __forceinline__ void z_skip(float& kpf, int dk, float& mzv, float& nt
     ntzv = -fmaf(mzv, dtz, t0z);
 }
 
+// red.global.add.f32 on an address built by integer arithmetic (a plain atomicAdd on such a generic
+// pointer compiles to a generic ATOM with a shared-window check and CAS fallback)
+__device__ __forceinline__ void red_add(float* a, float v) {
+    asm volatile("red.global.add.f32 [%0], %1;" :: "l"(a), "f"(v) : "memory");
+}
+
 // 1.0f if x > 0 else 0.0f (one FSET)
 __device__ __forceinline__ float gt0(float x) {
     float r;
@@ -512,10 +518,10 @@ __device__ __forceinline__ void column_segments_adj(const Seg* __restrict__ seg,
             z_step<DK>(P[p], se2, cr, lm);
             const float2 ls = __ffma2_rn(lm, m1, ds2);               // l_s = d_sigma - l_e
             const float2 ws = __fmul2_rn(P[p].w, ls), we = __fmul2_rn(P[p].w, lm);
-            if (P[p].live0) atomicAdd(a0, ws.x);
-            if (P[p].live1) atomicAdd(a1, ws.y);
-            if (P[p].live0 && cr.x != 0.f) atomicAdd(a0 + o0, we.x);
-            if (P[p].live1 && cr.y != 0.f) atomicAdd(a1 + o1, we.y);
+            if (P[p].live0) red_add(a0, ws.x);
+            if (P[p].live1) red_add(a1, ws.y);
+            if (P[p].live0 && cr.x != 0.f) red_add(a0 + o0, we.x);
+            if (P[p].live1 && cr.y != 0.f) red_add(a1 + o1, we.y);
         }
     }
 }
@@ -526,7 +532,7 @@ __device__ __forceinline__ void column_segments_adj(const Seg* __restrict__ seg,
 // 2 NP rays per lane (rows band*64NP + 32q + lane: adjacent rows in adjacent lanes, so the lanes'
 // loads of one segment fall on consecutive addresses of the z-fastest volume).
 #ifndef XRT_COL_MINB
-#define XRT_COL_MINB 2
+#define XRT_COL_MINB 3
 #endif
 
 template <bool kAdjoint, int NP>
