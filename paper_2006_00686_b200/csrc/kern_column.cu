@@ -408,8 +408,34 @@ __device__ __forceinline__ void z_skip(float& kpf, int dk, float& mzv, float& nt
 
 // red.global.add.f32 on an address built by integer arithmetic (a plain atomicAdd on such a generic
 // pointer compiles to a generic ATOM with a shared-window check and CAS fallback)
-__device__ __forceinline__ void red_add(float* a, float v) {
-    asm volatile("red.global.add.f32 [%0], %1;" :: "l"(a), "f"(v) : "memory");
+__device__ __forceinline__ void red_add(float* a, float v, unsigned long long pol) {
+    asm volatile("red.global.add.L2::cache_hint.f32 [%0], %1, %2;" :: "l"(a), "f"(v), "l"(pol) : "memory");
+}
+
+// L2 policies: the volume / accumulator tile is re-used by every view of a band -> evict_last;
+// sinogram elements are touched once or twice -> evict_first (do not displace the tile).
+__device__ __forceinline__ unsigned long long l2_evict_last() {
+    unsigned long long pol;
+    asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+__device__ __forceinline__ unsigned long long l2_evict_first() {
+    unsigned long long pol;
+    asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+__device__ __forceinline__ float ldg_hint(const float* a, unsigned long long pol) {
+    float v;
+    asm("ld.global.nc.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(v) : "l"(a), "l"(pol));
+    return v;
+}
+__device__ __forceinline__ float ld_stream(const float* a, unsigned long long pol) {
+    float v;
+    asm("ld.global.nc.L1::no_allocate.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(v) : "l"(a), "l"(pol));
+    return v;
+}
+__device__ __forceinline__ void red_sino(float* a, float v, unsigned long long pol) {
+    asm volatile("red.global.add.L2::cache_hint.f32 [%0], %1, %2;" :: "l"(a), "f"(v), "l"(pol) : "memory");
 }
 
 // 1.0f if x > 0 else 0.0f (one FSET)
@@ -424,11 +450,10 @@ __device__ __forceinline__ float gt0(float x) {
 // cell k_s + dk; l_e = max(sigma_e - tau, 0) and l_s = d_sigma - l_e are C_up - C_low of the two
 // units (eq:range_length_3D).  DK = +1 / -1: every ray of the warp steps that way (or is
 // fixed), so the neighbour cell is an immediate offset; DK = 0: per-ray offsets.
-__device__ __forceinline__ uint4 lds128(const Seg* p) {
+__device__ __forceinline__ uint4 lds128(unsigned saddr) {
     uint4 raw;   // one 128-bit shared load per segment (broadcast to the warp)
     asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
-                 : "=r"(raw.x), "=r"(raw.y), "=r"(raw.z), "=r"(raw.w)
-                 : "r"((unsigned)__cvta_generic_to_shared(p)));
+                 : "=r"(raw.x), "=r"(raw.y), "=r"(raw.z), "=r"(raw.w) : "r"(saddr));
     return raw;
 }
 
@@ -461,23 +486,24 @@ __device__ __forceinline__ void z_step(RayPair& P, const float2 se2, float2& cr,
 // decides the next segment's cells before this segment's arithmetic, so the next loads are in
 // flight while this segment's values are consumed.
 template <int NP, int DK>
-__device__ __forceinline__ void column_segments_fwd(const Seg* __restrict__ seg, int total, RayPair (&P)[NP]) {
+__device__ __forceinline__ void column_segments_fwd(unsigned seg, int total, RayPair (&P)[NP]) {
     const float2 m1 = make_float2(-1.f, -1.f);
-    uint4 raw = lds128(&seg[0]);
+    const unsigned long long pol = l2_evict_last();
+    uint4 raw = lds128(seg);
     float2 f0[NP], f1[NP];
 #pragma unroll
     for (int p = 0; p < NP; ++p) {
         const float* a0 = (const float*)(seg_ptr(raw) + 4ull * __float_as_uint(P[p].kpf.x));
         const float* a1 = (const float*)(seg_ptr(raw) + 4ull * __float_as_uint(P[p].kpf.y));
         const int o0 = DK != 0 ? DK : P[p].dk0, o1 = DK != 0 ? DK : P[p].dk1;
-        f0[p] = make_float2(__ldg(a0), __ldg(a1));
-        f1[p] = make_float2(__ldg(a0 + o0), __ldg(a1 + o1));
+        f0[p] = make_float2(ldg_hint(a0, pol), ldg_hint(a1, pol));
+        f1[p] = make_float2(ldg_hint(a0 + o0, pol), ldg_hint(a1 + o1, pol));
     }
 #pragma unroll 2
     for (int s = 0; s < total; ++s) {
         const float qse = __uint_as_float(raw.z), qds = __uint_as_float(raw.w);
         const float2 se2 = make_float2(qse, qse), ds2 = make_float2(qds, qds);
-        const uint4 nraw = lds128(&seg[min(s + 1, total - 1)]);   // last trip: harmless reload
+        const uint4 nraw = lds128(seg + 16u * (unsigned)min(s + 1, total - 1));   // last trip: reload
 #pragma unroll
         for (int p = 0; p < NP; ++p) {
             float2 cr, lm;
@@ -486,8 +512,8 @@ __device__ __forceinline__ void column_segments_fwd(const Seg* __restrict__ seg,
             const float* a0 = (const float*)(seg_ptr(nraw) + 4ull * __float_as_uint(P[p].kpf.x));
             const float* a1 = (const float*)(seg_ptr(nraw) + 4ull * __float_as_uint(P[p].kpf.y));
             const int o0 = DK != 0 ? DK : P[p].dk0, o1 = DK != 0 ? DK : P[p].dk1;
-            const float2 g0 = make_float2(__ldg(a0), __ldg(a1));
-            const float2 g1 = make_float2(__ldg(a0 + o0), __ldg(a1 + o1));
+            const float2 g0 = make_float2(ldg_hint(a0, pol), ldg_hint(a1, pol));
+            const float2 g1 = make_float2(ldg_hint(a0 + o0, pol), ldg_hint(a1 + o1, pol));
             // this segment's arithmetic
             P[p].acc0 = __ffma2_rn(f0[p], ds2, P[p].acc0);        // f_s * d_sigma
             const float2 d = __ffma2_rn(f0[p], m1, f1[p]);        // f_e - f_s
@@ -502,11 +528,12 @@ __device__ __forceinline__ void column_segments_fwd(const Seg* __restrict__ seg,
 // Adjoint: the same units, y l scattered with red.global.add (the second unit only when the z
 // crossing lies inside the segment).
 template <int NP, int DK>
-__device__ __forceinline__ void column_segments_adj(const Seg* __restrict__ seg, int total, RayPair (&P)[NP]) {
+__device__ __forceinline__ void column_segments_adj(unsigned seg, int total, RayPair (&P)[NP]) {
     const float2 m1 = make_float2(-1.f, -1.f);
+    const unsigned long long pol = l2_evict_last();
 #pragma unroll 2
     for (int s = 0; s < total; ++s) {
-        const uint4 raw = lds128(&seg[s]);
+        const uint4 raw = lds128(seg + 16u * (unsigned)s);
         const float qse = __uint_as_float(raw.z), qds = __uint_as_float(raw.w);
         const float2 se2 = make_float2(qse, qse), ds2 = make_float2(qds, qds);
 #pragma unroll
@@ -518,10 +545,10 @@ __device__ __forceinline__ void column_segments_adj(const Seg* __restrict__ seg,
             z_step<DK>(P[p], se2, cr, lm);
             const float2 ls = __ffma2_rn(lm, m1, ds2);               // l_s = d_sigma - l_e
             const float2 ws = __fmul2_rn(P[p].w, ls), we = __fmul2_rn(P[p].w, lm);
-            if (P[p].live0) red_add(a0, ws.x);
-            if (P[p].live1) red_add(a1, ws.y);
-            if (P[p].live0 && cr.x != 0.f) red_add(a0 + o0, we.x);
-            if (P[p].live1 && cr.y != 0.f) red_add(a1 + o1, we.y);
+            if (P[p].live0) red_add(a0, ws.x, pol);
+            if (P[p].live1) red_add(a1, ws.y, pol);
+            if (P[p].live0 && cr.x != 0.f) red_add(a0 + o0, we.x, pol);
+            if (P[p].live1 && cr.y != 0.f) red_add(a1 + o1, we.y, pol);
         }
     }
 }
@@ -600,8 +627,8 @@ __global__ void __launch_bounds__(kWarps * 32, XRT_COL_MINB) k_column(const View
         const int ra = (band * R + 2 * p) * 32 + lane, rb = ra + 32;
         ray_z(V, dc, g, Pth, ca, ra, L.pad, Za);
         ray_z(V, dc, g, Pth, ca, rb, L.pad, Zb);
-        const float ya = (kAdjoint && Za.active) ? sino_in[((int64_t)v * dc.rows + ra) * dc.cols + c] : 0.f;
-        const float yb = (kAdjoint && Zb.active) ? sino_in[((int64_t)v * dc.rows + rb) * dc.cols + c] : 0.f;
+        const float ya = (kAdjoint && Za.active) ? ld_stream(sino_in + ((int64_t)v * dc.rows + ra) * dc.cols + c, l2_evict_first()) : 0.f;
+        const float yb = (kAdjoint && Zb.active) ? ld_stream(sino_in + ((int64_t)v * dc.rows + rb) * dc.cols + c, l2_evict_first()) : 0.f;
         pair_init(P[p], Za, Zb, ya, yb, kAdjoint);
         any_live |= P[p].live0 | P[p].live1;
         pos &= Za.dk >= 0 && Zb.dk >= 0;
@@ -611,6 +638,7 @@ __global__ void __launch_bounds__(kWarps * 32, XRT_COL_MINB) k_column(const View
     // warp-uniform z stepping direction
     const int mode = __all_sync(0xffffffffu, pos) ? 1 : (__all_sync(0xffffffffu, neg) ? -1 : 0);
     Seg* seg = s_seg[warp];
+    const unsigned seg_s = (unsigned)__cvta_generic_to_shared(seg);
     // segment pointers pre-offset by -4 kMagicBits bytes (see RayPair)
     const unsigned long long base = (unsigned long long)(kAdjoint ? (const float*)volw : vol) -
                                     4ull * kMagicBits;
@@ -657,13 +685,13 @@ __global__ void __launch_bounds__(kWarps * 32, XRT_COL_MINB) k_column(const View
                 }
             }
             if (kAdjoint) {
-                if (mode > 0) column_segments_adj<NP, 1>(seg, total, P);
-                else if (mode < 0) column_segments_adj<NP, -1>(seg, total, P);
-                else column_segments_adj<NP, 0>(seg, total, P);
+                if (mode > 0) column_segments_adj<NP, 1>(seg_s, total, P);
+                else if (mode < 0) column_segments_adj<NP, -1>(seg_s, total, P);
+                else column_segments_adj<NP, 0>(seg_s, total, P);
             } else {
-                if (mode > 0) column_segments_fwd<NP, 1>(seg, total, P);
-                else if (mode < 0) column_segments_fwd<NP, -1>(seg, total, P);
-                else column_segments_fwd<NP, 0>(seg, total, P);
+                if (mode > 0) column_segments_fwd<NP, 1>(seg_s, total, P);
+                else if (mode < 0) column_segments_fwd<NP, -1>(seg_s, total, P);
+                else column_segments_fwd<NP, 0>(seg_s, total, P);
             }
         }
         __syncwarp();  // the next chunk overwrites the segments
@@ -676,8 +704,8 @@ __global__ void __launch_bounds__(kWarps * 32, XRT_COL_MINB) k_column(const View
             const float a = (q & 1) ? Q.acc0.y + Q.acc1.y : Q.acc0.x + Q.acc1.x;
             const float out = a * ((q & 1) ? Q.w.y : Q.w.x);
             const int64_t m = ((int64_t)v * dc.rows + (band * R + q) * 32 + lane) * dc.cols + c;
-            if (tiled) { if (out != 0.f) atomicAdd(sino_out + m, out); }
-            else sino_out[m] = out;
+            if (tiled) { if (out != 0.f) red_sino(sino_out + m, out, l2_evict_first()); }
+            else __stcs(sino_out + m, out);
         }
     }
 }

@@ -2,8 +2,8 @@
 # time cfg4 forward/adjoint for tile-size overrides and lib variants
 set -u
 out=gpurun_out; mkdir -p $out
-for lib in paper_2006_00686_b200/libxrt.so paper_2006_00686_b200/libxrt_minb3.so; do
-  for tile in default 256 4096; do
+for lib in ${LIBS:-paper_2006_00686_b200/libxrt.so}; do
+  for tile in ${TILES:-default 256 4096}; do
     if [ $tile = default ]; then unset XRT_COLUMN_TILE; else export XRT_COLUMN_TILE=$tile; fi
     f=$out/tiles_$(basename $lib .so)_$tile.json
     XRT_LIB=$lib timeout 600 python bench.py --config 4 --steps 2 --warmup 3 --no-e2e --no-cpu > $f 2>&1
