@@ -106,6 +106,17 @@ class ClockSampler:
 
 
 
+def measured_traffic(workload: str, kernel: str):
+    """DRAM bytes (read + write) per launch of `kernel` from the committed ncu --set full capture
+    (profiles/traffic.json, written by tools/ncu_summary.py traffic); None if not captured."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            t = json.load(f)
+        return t[workload][kernel]["dram_bytes"]
+    except Exception:
+        return None
+
+
 def cpu_baseline(c: dict, budget_s: float = 12.0):
     """The oracle, as it stands, on a bounded sample of the workload's rays (forward)."""
     import oracle
@@ -293,7 +304,10 @@ def main():
     k_adj = {"ms": adj_avg, "tflops": c_ops * nnz_local / (adj_avg / 1e3) / 1e12}
     dom_name, dom = ("adjoint", k_adj) if adj_avg >= fwd_avg else ("forward", k_fwd)
     roof = {"bound": "alu", "kernel": dom_name, "achieved": dom["tflops"], "peak": pk["fp32_tops"],
-            "unit": "TFLOP/s", "frac": dom["tflops"] / pk["fp32_tops"], "traffic": None,
+            "unit": "TFLOP/s", "frac": dom["tflops"] / pk["fp32_tops"],
+            "traffic": measured_traffic(c["name"], dom_name) if world == 1 else None,
+            "traffic_unit": "bytes per launch (dram__bytes_read.sum + dram__bytes_write.sum, ncu --set full)",
+            "algorithmic_bytes": int(4 * (x.numel() + sino.numel())),
             "peak_source": f"FP32 issue 148 SM x 128 lanes x {pk['sm_mhz']:.0f} MHz ({pk['src']} sm_max_mhz)",
             "ops_per_intersection": c_ops}
     line = {

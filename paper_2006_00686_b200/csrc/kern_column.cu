@@ -412,8 +412,9 @@ __device__ __forceinline__ void red_add(float* a, float v, unsigned long long po
     asm volatile("red.global.add.L2::cache_hint.f32 [%0], %1, %2;" :: "l"(a), "f"(v), "l"(pol) : "memory");
 }
 
-// L2 policies: the volume / accumulator tile is re-used by every view of a band -> evict_last;
-// sinogram elements are touched once or twice -> evict_first (do not displace the tile).
+// L2 policies: the adjoint's accumulator tile is re-used by every view of a band -> evict_last;
+// sinogram elements are touched once or twice -> evict_first (do not displace the tile).  (The
+// forward's plain __ldg measured faster than ld.global.nc.L2::cache_hint.)
 __device__ __forceinline__ unsigned long long l2_evict_last() {
     unsigned long long pol;
     asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
@@ -423,11 +424,6 @@ __device__ __forceinline__ unsigned long long l2_evict_first() {
     unsigned long long pol;
     asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
     return pol;
-}
-__device__ __forceinline__ float ldg_hint(const float* a, unsigned long long pol) {
-    float v;
-    asm("ld.global.nc.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(v) : "l"(a), "l"(pol));
-    return v;
 }
 __device__ __forceinline__ float ld_stream(const float* a, unsigned long long pol) {
     float v;
@@ -488,7 +484,6 @@ __device__ __forceinline__ void z_step(RayPair& P, const float2 se2, float2& cr,
 template <int NP, int DK>
 __device__ __forceinline__ void column_segments_fwd(unsigned seg, int total, RayPair (&P)[NP]) {
     const float2 m1 = make_float2(-1.f, -1.f);
-    const unsigned long long pol = l2_evict_last();
     uint4 raw = lds128(seg);
     float2 f0[NP], f1[NP];
 #pragma unroll
@@ -496,8 +491,8 @@ __device__ __forceinline__ void column_segments_fwd(unsigned seg, int total, Ray
         const float* a0 = (const float*)(seg_ptr(raw) + 4ull * __float_as_uint(P[p].kpf.x));
         const float* a1 = (const float*)(seg_ptr(raw) + 4ull * __float_as_uint(P[p].kpf.y));
         const int o0 = DK != 0 ? DK : P[p].dk0, o1 = DK != 0 ? DK : P[p].dk1;
-        f0[p] = make_float2(ldg_hint(a0, pol), ldg_hint(a1, pol));
-        f1[p] = make_float2(ldg_hint(a0 + o0, pol), ldg_hint(a1 + o1, pol));
+        f0[p] = make_float2(__ldg(a0), __ldg(a1));
+        f1[p] = make_float2(__ldg(a0 + o0), __ldg(a1 + o1));
     }
 #pragma unroll 2
     for (int s = 0; s < total; ++s) {
@@ -512,8 +507,8 @@ __device__ __forceinline__ void column_segments_fwd(unsigned seg, int total, Ray
             const float* a0 = (const float*)(seg_ptr(nraw) + 4ull * __float_as_uint(P[p].kpf.x));
             const float* a1 = (const float*)(seg_ptr(nraw) + 4ull * __float_as_uint(P[p].kpf.y));
             const int o0 = DK != 0 ? DK : P[p].dk0, o1 = DK != 0 ? DK : P[p].dk1;
-            const float2 g0 = make_float2(ldg_hint(a0, pol), ldg_hint(a1, pol));
-            const float2 g1 = make_float2(ldg_hint(a0 + o0, pol), ldg_hint(a1 + o1, pol));
+            const float2 g0 = make_float2(__ldg(a0), __ldg(a1));
+            const float2 g1 = make_float2(__ldg(a0 + o0), __ldg(a1 + o1));
             // this segment's arithmetic
             P[p].acc0 = __ffma2_rn(f0[p], ds2, P[p].acc0);        // f_s * d_sigma
             const float2 d = __ffma2_rn(f0[p], m1, f1[p]);        // f_e - f_s

@@ -89,5 +89,33 @@ def full(path: str) -> None:
         print()
 
 
+def traffic(path: str, workload: str, kernel: str, out: str = "profiles/traffic.json") -> None:
+    """Record dram__bytes_read.sum + dram__bytes_write.sum of the (single) kernel in `path` as the
+    per-launch traffic of `kernel` ("forward" / "adjoint") on `workload` (read by bench.py)."""
+    import json
+    import os
+    raw = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    rows = list(csv.reader(io.StringIO(raw)))
+    hdr, units, data = rows[0], rows[1], rows[2:]
+    col = {h: i for i, h in enumerate(hdr)}
+    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
+    d = data[0]
+    tot = 0.0
+    for m in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+        tot += float(d[col[m]].replace(",", "")) * scale[units[col[m]]]
+    t = {}
+    if os.path.exists(out):
+        with open(out) as f:
+            t = json.load(f)
+    t.setdefault(workload, {})[kernel] = {
+        "dram_bytes": int(tot), "kernel": d[col["Kernel Name"]][:120],
+        "duration_ms": float(d[col["gpu__time_duration.sum"]].replace(",", "")) *
+        {"nsecond": 1e-6, "ns": 1e-6, "usecond": 1e-3, "us": 1e-3, "msecond": 1.0, "ms": 1.0, "second": 1e3, "s": 1e3}[units[col["gpu__time_duration.sum"]]],
+        "source": os.path.basename(path)}
+    with open(out, "w") as f:
+        json.dump(t, f, indent=1)
+    print(workload, kernel, t[workload][kernel])
+
+
 if __name__ == "__main__":
-    {"launches": launches, "full": full}[sys.argv[1]](sys.argv[2])
+    {"launches": launches, "full": full, "traffic": traffic}[sys.argv[1]](*sys.argv[2:])
