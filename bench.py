@@ -182,6 +182,8 @@ def main():
     ap.add_argument("--config", type=int, default=4)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--algo", default="auto", choices=["auto", "ray", "column"])
+    ap.add_argument("--adj-algo", default=None, choices=["auto", "ray", "column", "gather"],
+                    help="adjoint kernel family (default: --algo)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--ref-rays", type=int, default=256)
@@ -207,6 +209,8 @@ def main():
     if args.algo != "auto":
         plan.set_algorithm("forward", args.algo)
         plan.set_algorithm("adjoint", args.algo)
+    if args.adj_algo is not None:
+        plan.set_algorithm("adjoint", args.adj_algo)
     x = workloads.make_image(c, device=dev)
     sino = torch.empty(plan.sino_shape, dtype=torch.float32, device=dev)
     xo = torch.empty_like(x)
@@ -330,7 +334,7 @@ def main():
         "roofline": roof,
         "gpu_launches": launches,
         "clocks": clk.summary(),
-        "algo": args.algo,
+        "algo": args.algo, "adj_algo": args.adj_algo or args.algo,
     }
     if e2e is not None:
         line["e2e"] = e2e

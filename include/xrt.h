@@ -103,8 +103,10 @@ typedef enum { XRT_OP_FORWARD = 0, XRT_OP_ADJOINT = 1 } xrt_op;
 typedef enum {
     XRT_ALGO_AUTO = 0,
     XRT_ALGO_RAY = 1,    /* one thread per ray, per-ray unit enumeration (any geometry)          */
-    XRT_ALGO_COLUMN = 2  /* one warp per detector column: shared in-plane unit band, per-lane
+    XRT_ALGO_COLUMN = 2, /* one warp per detector column: shared in-plane unit band, per-lane
                             z band (3D beams whose rays have a common xy line per column)        */
+    XRT_ALGO_GATHER = 3  /* adjoint only: voxel-driven gather (a warp per cell column, no atomics);
+                            same geometries as XRT_ALGO_COLUMN                                   */
 } xrt_algo;
 
 /* Validate `g`, build the per-view geometry tables on `cuda_device` and allocate workspace.

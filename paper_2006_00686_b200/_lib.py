@@ -18,8 +18,8 @@ STATUS_NAMES = {0: "XRT_OK", 1: "XRT_ERR_INVALID_ARG", 2: "XRT_ERR_UNSUPPORTED",
                 4: "XRT_ERR_OOM", 5: "XRT_ERR_CAPACITY"}
 BEAMS = {"par2d": 0, "fan2d": 1, "par3d": 2, "cone": 3, "helical": 4}
 OP_FORWARD, OP_ADJOINT = 0, 1
-ALGO_AUTO, ALGO_RAY, ALGO_COLUMN = 0, 1, 2
-ALGOS = {"auto": 0, "ray": 1, "column": 2}
+ALGO_AUTO, ALGO_RAY, ALGO_COLUMN, ALGO_GATHER = 0, 1, 2, 3
+ALGOS = {"auto": 0, "ray": 1, "column": 2, "gather": 3}
 
 # every symbol include/xrt.h declares (checked by tests/test_abi.py)
 EXPORTS = ("xrt_plan_create", "xrt_plan_destroy", "xrt_plan_query", "xrt_plan_set_algorithm",

@@ -242,7 +242,9 @@ xrt_status forward_range(xrt_plan p, const float* img, float* sino, int64_t v0, 
 // Adjoint: adj_begin() clears the accumulator, adjoint_range() adds views [v0, v1),
 // adj_finish() writes the caller's image (COLUMN: work_adj -> img transpose).
 xrt_status adj_begin(xrt_plan p, float* img, cudaStream_t s) {
-    const bool col = resolve(p->algo_adj, p->column_ok) == XRT_ALGO_COLUMN;
+    const int algo = resolve(p->algo_adj, p->column_ok);
+    if (algo == XRT_ALGO_GATHER) return XRT_OK;   // the gather writes every interior voxel
+    const bool col = algo == XRT_ALGO_COLUMN;
     if (col) XRT_CUDA(cudaMemsetAsync(p->d_work_adj, 0, sizeof(float) * (size_t)(p->grid.nxy * p->nzp), s));
     else XRT_CUDA(cudaMemsetAsync(img, 0, sizeof(float) * (size_t)p->grid.nxyz, s));
     return XRT_OK;
@@ -257,6 +259,10 @@ xrt_status adjoint_range(xrt_plan p, const float* sino, float* img, int64_t v0, 
         e = xrt::launch_adjoint_ray(p, sino, img, v0 * pv, v1 * pv, s);
     } else if (algo == XRT_ALGO_COLUMN) {
         e = xrt::launch_adjoint_column(p, sino, p->d_work_adj, v0, v1, s);
+    } else if (algo == XRT_ALGO_GATHER) {
+        if (!(v0 == 0 && v1 == p->n_views)) return fail(XRT_ERR_UNSUPPORTED, "gather adjoint runs all views at once");
+        e = xrt::launch_adjoint_gather(p, sino, p->d_work_adj, s);
+        p->launches += xrt::gather_launches(p) - 1;
     } else {
         return fail(XRT_ERR_UNSUPPORTED, "adjoint algorithm %d not built", algo);
     }
@@ -266,7 +272,8 @@ xrt_status adjoint_range(xrt_plan p, const float* sino, float* img, int64_t v0, 
 }
 
 xrt_status adj_finish(xrt_plan p, float* img, cudaStream_t s) {
-    if (resolve(p->algo_adj, p->column_ok) != XRT_ALGO_COLUMN) return XRT_OK;
+    const int algo = resolve(p->algo_adj, p->column_ok);
+    if (algo != XRT_ALGO_COLUMN && algo != XRT_ALGO_GATHER) return XRT_OK;
     cudaError_t e = xrt::launch_from_zfast(p, p->d_work_adj, img, s);
     p->launches += 1;
     if (e != cudaSuccess) return cuda_fail(e, "transpose launch");
@@ -377,6 +384,11 @@ xrt_status xrt_plan_create(const xrt_geometry* g, int cuda_device, xrt_plan* out
         if (e == cudaSuccess)
             e = cudaMalloc(&p->d_coldesc, xrt::column_desc_bytes() * (size_t)(p->n_views * D.cols));
         if (e == cudaSuccess) e = xrt::launch_col_desc(p, (cudaStream_t)0);
+        // gather workspace: one block of views of the rescaled, transposed sinogram (~40 MB, so the
+        // block stays L2-resident while every voxel reads it)
+        p->gather_views = std::max<int64_t>(1, std::min<int64_t>(g->n_views, (40ll << 20) / (4 * D.per_view)));
+        if (e == cudaSuccess)
+            e = cudaMalloc(&p->d_gather_y, sizeof(float) * (size_t)(p->gather_views * D.per_view));
         if (e == cudaSuccess) e = cudaDeviceSynchronize();
         // xy tiling: largest power-of-two tile whose z-fastest columns, restricted to the z slab one
         // band of detector rows can reach (the kernels run band-major), fit the L2 budget
@@ -416,6 +428,7 @@ xrt_status xrt_plan_destroy(xrt_plan p) {
     cudaFree(p->d_work_adj);
     cudaFree(p->d_items);
     cudaFree(p->d_coldesc);
+    cudaFree(p->d_gather_y);
     cudaFree(p->d_stage_img);
     cudaFree(p->d_stage_sino);
     if (p->aux_stream) cudaStreamDestroy((cudaStream_t)p->aux_stream);
@@ -440,7 +453,11 @@ xrt_status xrt_plan_query(xrt_plan p, int64_t* n_rays, int64_t* n_units) {
 xrt_status xrt_plan_set_algorithm(xrt_plan p, int32_t op, int32_t algo) {
     if (!p) return fail(XRT_ERR_INVALID_ARG, "plan is NULL");
     if (op != XRT_OP_FORWARD && op != XRT_OP_ADJOINT) return fail(XRT_ERR_INVALID_ARG, "bad op %d", op);
-    if (algo < XRT_ALGO_AUTO || algo > XRT_ALGO_COLUMN) return fail(XRT_ERR_INVALID_ARG, "bad algo %d", algo);
+    if (algo < XRT_ALGO_AUTO || algo > XRT_ALGO_GATHER) return fail(XRT_ERR_INVALID_ARG, "bad algo %d", algo);
+    if (algo == XRT_ALGO_GATHER && op != XRT_OP_ADJOINT)
+        return fail(XRT_ERR_UNSUPPORTED, "the gather algorithm is an adjoint");
+    if (algo == XRT_ALGO_GATHER && (!p->column_ok || p->det.rows > 12288))
+        return fail(XRT_ERR_UNSUPPORTED, "gather algorithm does not serve this geometry");
     if (algo == XRT_ALGO_COLUMN && !p->column_ok)
         return fail(XRT_ERR_UNSUPPORTED, "column algorithm does not serve this geometry");
     if (op == XRT_OP_FORWARD) p->algo_fwd = algo; else p->algo_adj = algo;
@@ -515,7 +532,8 @@ xrt_status xrt_adjoint_host(xrt_plan p, const float* sino_host, float* img_host,
     cudaStream_t s = (cudaStream_t)cuda_stream, a = (cudaStream_t)p->aux_stream;
     st = adj_begin(p, p->d_stage_img, s);
     if (st != XRT_OK) return st;
-    const bool whole = p->d_items && resolve(p->algo_adj, p->column_ok) == XRT_ALGO_COLUMN;
+    const bool whole = (p->d_items && resolve(p->algo_adj, p->column_ok) == XRT_ALGO_COLUMN) ||
+                       resolve(p->algo_adj, p->column_ok) == XRT_ALGO_GATHER;
     const int64_t nchunk = whole ? 1 : std::min<int64_t>(8, p->n_views);
     const int64_t pv = p->det.per_view;
     std::vector<cudaEvent_t> ev((size_t)nchunk);

@@ -35,6 +35,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <climits>
 #include <cstdlib>
 #include <vector>
 
@@ -733,6 +734,248 @@ inline cudaError_t transpose(const float* in, float* out, int64_t rows, int64_t 
     k_transpose<<<grid, dim3(32, 8), 0, s>>>(in, out, rows, cols, in_ld, in_off, out_ld, out_off);
     return cudaGetLastError();
 }
+
+// ============================================================================ voxel-driven gather
+// The adjoint as a GATHER (north_star: "a voxel-driven gather that reuses the same
+// per-ray unit condition"): every voxel sums y_m l_I(ray m) over the rays that cross it, with no
+// atomics.  A warp owns one in-plane cell (i, j) and 32 Q consecutive voxels k of its z column
+// (lane = k0 + lane + 32 q).  For each view, the detector columns whose in-plane lines can cross the
+// cell come from the cell's four corners projected on the detector (+-1 column margin; a candidate
+// that misses contributes exactly 0).  For each candidate column the in-plane part of the unit
+// condition is the slab clip of the column's line (the same per-(view, column) descriptor the
+// column kernels walk) with the cell: sigma in [C_low, C_up] of the in-plane unit
+// (eq:conditions_3D_1 P:460-468 restricted to x, y; half-open for a fixed axis).  For
+// each voxel, the candidate detector rows are those whose z line reaches z cell k inside that sigma
+// range (z is affine in the row coordinate at fixed sigma); per row the z slab [k, k+1) gives the
+// third pair of bounds and l = C_up - C_low of the 3D unit (eq:range_length_3D P:503-506) in
+// physical units (the 1 / cos(beta) factor is folded into y by k_gather_prep).
+
+// y'[v][c][r] = y[v][r][c] / cos(beta(r, c)), per-view 32x32 smem transposes (rows fastest, so the
+// gather's lanes -- consecutive voxels k, consecutive rows r -- read consecutive addresses).
+__global__ void k_gather_prep(const ViewRec* __restrict__ views, DetC dc, const ColDesc* __restrict__ desc,
+                              const float* __restrict__ sino, float* __restrict__ yp, int v0) {
+    __shared__ float tile[32][33];
+    const int v = v0 + blockIdx.z;
+    const int c0 = blockIdx.x * 32, r0 = blockIdx.y * 32;
+    const ViewRec V = views[v];
+    (void)V;
+    for (int jj = threadIdx.y; jj < 32; jj += 8) {
+        const int r = r0 + jj, c = c0 + threadIdx.x;
+        float val = 0.f;
+        if (r < dc.rows && c < dc.cols) {
+            double tb;
+            if (dc.beam == XRT_PAR3D) {
+                tb = fabs(V.s2) <= kSnap ? 0.0 : V.pad[0];
+            } else {
+                const double vr = ((double)r - dc.cv) * dc.dv + dc.off_v;
+                const double h = vr * dc.D / dc.sdd;
+                const double ca = __ldg(reinterpret_cast<const double2*>(desc + ((int64_t)v * dc.cols + c)) + 4).y;
+                tb = h * ca * dc.inv_D;
+                if (fabs(tb) <= kSnap) tb = 0.0;
+            }
+            const float scale = sqrtf(1.f + (float)(tb * tb));   // as ray_z
+            val = sino[((int64_t)v * dc.rows + r) * dc.cols + c] * scale;
+        }
+        tile[jj][threadIdx.x] = val;
+    }
+    __syncthreads();
+    for (int jj = threadIdx.y; jj < 32; jj += 8) {
+        const int c = c0 + jj, r = r0 + threadIdx.x;
+        if (r < dc.rows && c < dc.cols) yp[((int64_t)(v - v0) * dc.cols + c) * dc.rows + r] = tile[threadIdx.x][jj];
+    }
+}
+
+template <int Q>
+__global__ void __launch_bounds__(256) k_gather(const ViewRec* __restrict__ views, DetC dc, GridC g,
+                                                const ColDesc* __restrict__ desc, const float* __restrict__ yp,
+                                                float* __restrict__ work, int64_t nzp, int pad, int v0, int v1,
+                                                int first) {
+    extern __shared__ int s_kfix[];   // par3d without tilt: fixed z cell of every detector row
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int i = blockIdx.x * 8 + warp, j = blockIdx.y;
+    const int kb = blockIdx.z * 32 * Q;
+    const bool par = dc.beam == XRT_PAR3D;
+    const ViewRec V0 = views[v0];
+    const bool par_flat = par && fabs(V0.s2) <= kSnap;
+    if (par_flat) {
+        // the half-open cell floor((z_hi - z) / d_z) of each (horizontal) row, in fp64 exactly as
+        // ray_z / the oracle decide it (rows often lie exactly on z planes)
+        for (int r = threadIdx.x; r < dc.rows; r += blockDim.x) {
+            const double vr = ((double)r - dc.cv) * dc.dv + dc.off_v;
+            s_kfix[r] = (int)floor((g.z_hi - vr * V0.c2) / g.d[2]);
+        }
+        __syncthreads();
+    }
+    if (i >= g.n[0]) return;
+    const float x0 = (float)(g.x_lo + i * g.d[0]), x1 = (float)(g.x_lo + (i + 1) * g.d[0]);
+    const float y1 = (float)(g.y_hi - j * g.d[1]), y0 = (float)(g.y_hi - (j + 1) * g.d[1]);
+    const float inv_du = (float)(1.0 / dc.du), Df = (float)dc.D, sddf = (float)dc.sdd;
+    float acc[Q];
+#pragma unroll
+    for (int q = 0; q < Q; ++q) acc[q] = 0.f;
+    // row coordinate <-> z-line parameter h: cone h = v D / sdd (P:636 with t, h scaled to the iso
+    // plane, reading 8); par3d h = v.
+    const float hscale = par ? 1.f : (float)(dc.D / dc.sdd);
+    const float row_of_h = (float)(1.0 / (hscale * dc.dv));
+    const float row_off = (float)(dc.cv - dc.off_v / dc.dv);
+    const float h_of_row = (float)(hscale * dc.dv);
+    const float h_off = (float)(hscale * (dc.off_v - dc.cv * dc.dv));
+    const double h_of_row_d = (par ? 1.0 : dc.D / dc.sdd) * dc.dv;
+    const double h_off_d = (par ? 1.0 : dc.D / dc.sdd) * (dc.off_v - dc.cv * dc.dv);
+    // the (at most one) row with h == 0 exactly: a horizontal cone ray (fixed z cell per view)
+    const double r0d = dc.cv - dc.off_v / dc.dv;
+    const int r_flat = (!par && r0d == floor(r0d) && r0d >= 0 && r0d < dc.rows) ? (int)r0d : -1;
+    const float kb_lo = (float)kb, kb_hi = (float)(kb + 32 * Q);
+    for (int v = v0; v < v1; ++v) {
+        const ViewRec V = views[v];
+        const float c1 = (float)V.c1, s1 = (float)V.s1;
+        // detector u of the four corners -> candidate columns (+-1 margin)
+        float umin = INFINITY, umax = -INFINITY;
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+            const float px = (t & 1) ? x1 : x0, py = (t & 2) ? y1 : y0;
+            float u;
+            if (par) {
+                u = -px * s1 + py * c1;
+            } else {
+                const float ddx = px + Df * c1, ddy = py + Df * s1;   // P - S
+                u = sddf * __fdividef(-ddx * s1 + ddy * c1, ddx * c1 + ddy * s1);
+            }
+            umin = fminf(umin, u);
+            umax = fmaxf(umax, u);
+        }
+        const int c_lo = max(0, (int)floorf((umin - (float)dc.off_u) * inv_du + (float)dc.cu) - 1);
+        const int c_hi = min(dc.cols - 1, (int)ceilf((umax - (float)dc.off_u) * inv_du + (float)dc.cu) + 1);
+        for (int c = c_lo; c <= c_hi; ++c) {
+            const ColDesc* dsc = desc + ((int64_t)v * dc.cols + c);
+            const float4 q3 = __ldg(reinterpret_cast<const float4*>(dsc) + 3);   // ux0 uy0 wx wy
+            const int flags = __ldg(reinterpret_cast<const int*>(dsc) + 7);
+            if (!(flags & 1)) continue;
+            // in-plane clip of the column's line with cell (i, j): [C_low, C_up] in sigma.  A fixed
+            // (minor) axis keeps the descriptor's fp64 half-open cell.
+            const int cell_b = __ldg(reinterpret_cast<const int*>(dsc) + 9);
+            float lo = -INFINITY, hi = INFINITY;
+            if (q3.z != 0.f) {
+                const float iw = 1.f / q3.z;
+                const float a = ((float)i - q3.x) * iw, b = ((float)(i + 1) - q3.x) * iw;
+                lo = fmaxf(lo, fminf(a, b)); hi = fminf(hi, fmaxf(a, b));
+            } else if (i != cell_b) continue;
+            if (q3.w != 0.f) {
+                const float iw = 1.f / q3.w;
+                const float a = ((float)j - q3.y) * iw, b = ((float)(j + 1) - q3.y) * iw;
+                lo = fmaxf(lo, fminf(a, b)); hi = fminf(hi, fmaxf(a, b));
+            } else if (j != cell_b) continue;
+            if (!(hi > lo)) continue;
+            // z line of row h along the column: u_z(sigma) = A - T sigma - h (G0 + G1 sigma)
+            // (cone / helical, from ray_z: tan(beta) = h ca / D, z(0) = h ca^2 + H; par3d: rows
+            // parallel in the (sigma, z) plane, u_z = A - T sigma - h G0)
+            const double2 q4 = __ldg(reinterpret_cast<const double2*>(dsc) + 4);   // sig_in, ca
+            double Ad, G0d, G1d, Td;
+            if (par) {
+                const double tb = par_flat ? 0.0 : V.pad[0], zv = par_flat ? V.c2 : V.pad[1];
+                Ad = (g.z_hi - q4.x * tb) * g.inv_dz;
+                G0d = zv * g.inv_dz;
+                G1d = 0.0;
+                Td = tb * g.inv_dz;
+            } else {
+                Ad = (g.z_hi - V.H) * g.inv_dz;
+                G0d = (q4.y * q4.y + q4.x * q4.y * dc.inv_D) * g.inv_dz;
+                G1d = q4.y * dc.inv_D * g.inv_dz;
+                Td = 0.0;
+            }
+            const float A = (float)Ad, G0 = (float)G0d, G1 = (float)G1d, T = (float)Td;
+            const float Gs = fmaf(lo, G1, G0), Ge = fmaf(hi, G1, G0);   // > 0
+            // z range of all rows of this column inside the cell; skip if it misses the warp's k block
+            {
+                const float hA = fmaf(0.f, h_of_row, h_off), hB = fmaf((float)(dc.rows - 1), h_of_row, h_off);
+                const float za = A - T * lo, zb = A - T * hi;
+                const float u1 = za - hA * Gs, u2 = za - hB * Gs, u3 = zb - hA * Ge, u4 = zb - hB * Ge;
+                const float umn = fminf(fminf(u1, u2), fminf(u3, u4)), umx = fmaxf(fmaxf(u1, u2), fmaxf(u3, u4));
+                if (umx < kb_lo - 1.f || umn > kb_hi + 1.f) continue;
+            }
+            const float iGs = 1.f / Gs, iGe = 1.f / Ge;
+            int kflat = INT_MIN;   // cone: the h == 0 row's fixed cell (fp64, as ray_z)
+            if (r_flat >= 0) kflat = (int)floor((g.z_hi - V.H) / g.d[2]);
+            const float* yc = yp + ((int64_t)(v - v0) * dc.cols + c) * dc.rows;
+#pragma unroll
+            for (int q = 0; q < Q; ++q) {
+                const int k = kb + lane + 32 * q;
+                if (k >= g.n[2]) continue;
+                // rows whose z line reaches [k, k+1) for some sigma in [lo, hi]:
+                // A - T s - h G(s) in [k, k+1)  <=>  h in ((A - T s - k - 1) / G, (A - T s - k) / G]
+                const float as = A - T * lo - (float)k, ae = A - T * hi - (float)k;
+                const float h1 = fminf((as - 1.f) * iGs, (ae - 1.f) * iGe);
+                const float h2 = fmaxf(as * iGs, ae * iGe);
+                const float ra = fmaf(h1, row_of_h, row_off), rb = fmaf(h2, row_of_h, row_off);
+                const int r_lo = max(0, (int)ceilf(fminf(ra, rb) - 0.01f));
+                const int r_hi = min(dc.rows - 1, (int)floorf(fmaxf(ra, rb) + 0.01f));
+                float sum = 0.f;
+                for (int r = r_lo; r <= r_hi; ++r) {
+                    float l;
+                    if (par_flat) {
+                        l = s_kfix[r] == k ? hi - lo : 0.f;
+                    } else if (r == r_flat) {
+                        l = kflat == k ? hi - lo : 0.f;
+                    } else {
+                        // u_z(sigma) in [k, k+1)  <=>  sigma in (base - 1, base] / slope (sorted).
+                        // base = u_z(0) - k in fp64: u_z(0) is a difference of O(N) terms and a
+                        // u error becomes a sigma error / slope (shallow rays), as in ray_z
+                        const double hd = fma((double)r, h_of_row_d, h_off_d);
+                        const double base = fma(-hd, G0d, Ad) - (double)k;
+                        const double is = 1.0 / fma(hd, G1d, Td);
+                        const float t0 = (float)((base - 1.0) * is), t1 = (float)(base * is);
+                        l = fminf(hi, fmaxf(t0, t1)) - fmaxf(lo, fminf(t0, t1));
+                    }
+                    if (l > 0.f) sum = fmaf(__ldg(yc + r), l, sum);
+                }
+                acc[q] += sum;
+            }
+        }
+    }
+    float* col = work + ((int64_t)j * g.n[0] + i) * nzp + pad;
+#pragma unroll
+    for (int q = 0; q < Q; ++q) {
+        const int k = kb + lane + 32 * q;
+        if (k < g.n[2]) col[k] = first ? acc[q] : col[k] + acc[q];
+    }
+}
+
+}  // namespace
+
+// Adjoint by the voxel-driven gather: sino -> z-fastest accumulator (interior rows fully written).
+// Views are processed in blocks whose rescaled, transposed sinogram (workspace) stays L2-resident.
+cudaError_t launch_adjoint_gather(const xrt_plan_s* p, const float* sino, float* vol_zfast, cudaStream_t s) {
+    const ColDesc* d = (const ColDesc*)p->d_coldesc;
+    const int64_t vb = p->gather_views;
+    const int Q = p->grid.n[2] > 64 ? 4 : (p->grid.n[2] > 32 ? 2 : 1);
+    for (int64_t v0 = 0; v0 < p->n_views; v0 += vb) {
+        const int64_t v1 = std::min(p->n_views, v0 + vb);
+        dim3 gp((unsigned)((p->det.cols + 31) / 32), (unsigned)((p->det.rows + 31) / 32), (unsigned)(v1 - v0));
+        k_gather_prep<<<gp, dim3(32, 8), 0, s>>>(p->d_views, p->det, d, sino, p->d_gather_y, (int)v0);
+        dim3 gg((unsigned)((p->grid.n[0] + 7) / 8), (unsigned)p->grid.n[1],
+                (unsigned)((p->grid.n[2] + 32 * Q - 1) / (32 * Q)));
+        const int first = v0 == 0;
+        const size_t smem = sizeof(int) * (size_t)p->det.rows;   // par3d fixed-cell table
+        if (Q == 4)
+            k_gather<4><<<gg, 256, smem, s>>>(p->d_views, p->det, p->grid, d, p->d_gather_y, vol_zfast, p->nzp,
+                                           (int)p->zpad, (int)v0, (int)v1, first);
+        else if (Q == 2)
+            k_gather<2><<<gg, 256, smem, s>>>(p->d_views, p->det, p->grid, d, p->d_gather_y, vol_zfast, p->nzp,
+                                           (int)p->zpad, (int)v0, (int)v1, first);
+        else
+            k_gather<1><<<gg, 256, smem, s>>>(p->d_views, p->det, p->grid, d, p->d_gather_y, vol_zfast, p->nzp,
+                                           (int)p->zpad, (int)v0, (int)v1, first);
+        cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) return e;
+    }
+    return cudaSuccess;
+}
+
+int64_t gather_launches(const xrt_plan_s* p) {
+    return 2 * ((p->n_views + p->gather_views - 1) / p->gather_views);
+}
+
+namespace {
 
 }  // namespace
 

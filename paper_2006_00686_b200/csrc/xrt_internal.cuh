@@ -191,7 +191,9 @@ struct xrt_plan_s {
     int tile = 0, n_tx = 1, n_ty = 1;  // xy tiling of the column kernels (L2 residency)
     int col_np = 2;                    // ray pairs per lane of the column kernels (rows per band = 64 col_np)
     void* d_items = nullptr;           // device uint2 work list (tiled) or nullptr
-    void* d_coldesc = nullptr;         // per-(view, column) path descriptors (COLUMN)
+    void* d_coldesc = nullptr;         // per-(view, column) path descriptors (COLUMN, GATHER)
+    float* d_gather_y = nullptr;       // GATHER workspace: rescaled, transposed sinogram of one view block
+    int64_t gather_views = 0;          // views per GATHER launch
     int64_t n_items = 0;
     // host-pipeline staging (allocated on first *_host call)
     float* d_stage_img = nullptr;
@@ -228,4 +230,6 @@ size_t column_desc_bytes();
 int choose_col_np(int rows);
 int column_cta_columns();
 cudaError_t launch_col_desc(const xrt_plan_s* p, cudaStream_t s);
+cudaError_t launch_adjoint_gather(const xrt_plan_s* p, const float* sino, float* vol_zfast, cudaStream_t s);
+int64_t gather_launches(const xrt_plan_s* p);
 }  // namespace xrt

@@ -17,13 +17,15 @@ import helpers as H
 pytestmark = pytest.mark.gpu
 
 ALGOS = ["ray", "column"]
+ADJ_ALGOS = ["ray", "column", "gather"]   # gather: voxel-driven adjoint (forward stays AUTO)
 
 
 def _plan(c, algo=None):
     p = Plan(c, device=0)
     if algo is not None:
         try:
-            p.set_algorithm("forward", algo)
+            if algo != "gather":
+                p.set_algorithm("forward", algo)
             p.set_algorithm("adjoint", algo)
         except XrtError as e:
             if e.status == _lib.XRT_ERR_UNSUPPORTED:
@@ -170,7 +172,7 @@ def test_forward_deterministic_and_linear(cuda_ok, algo):
 
 
 # ------------------------------------------------------------------- adjoint
-@pytest.mark.parametrize("algo", ALGOS)
+@pytest.mark.parametrize("algo", ADJ_ALGOS)
 @pytest.mark.parametrize("idx", [1, 2, 3, 4, 5])
 def test_adjoint_small_sparse_parity(cuda_ok, idx, algo):
     c = H.small_config(idx)
@@ -187,7 +189,7 @@ def test_adjoint_small_sparse_parity(cuda_ok, idx, algo):
     assert err <= H.ADJ_TOL, err
 
 
-@pytest.mark.parametrize("algo", ALGOS)
+@pytest.mark.parametrize("algo", ADJ_ALGOS)
 @pytest.mark.parametrize("idx", [2, 4, 5])
 def test_adjoint_full_size_sparse_parity(cuda_ok, idx, algo):
     c = workloads.config(idx)
@@ -203,7 +205,7 @@ def test_adjoint_full_size_sparse_parity(cuda_ok, idx, algo):
     assert err <= H.ADJ_TOL, err
 
 
-@pytest.mark.parametrize("algo", ALGOS)
+@pytest.mark.parametrize("algo", ADJ_ALGOS)
 @pytest.mark.parametrize("idx", [1, 2, 3, 4, 5])
 def test_dot_product(cuda_ok, idx, algo):
     c = H.small_config(idx) if idx in (3, 4, 5) else workloads.config(idx)
@@ -230,6 +232,25 @@ def test_host_path_matches_device(cuda_ok):
     a_dev = p.adjoint(y.cuda())
     a_host = p.adjoint_host(y.contiguous())
     assert H.rel_l2(a_host.numpy(), a_dev.cpu().numpy()) < 1e-6
+
+
+def test_adjoint_algorithms_agree(cuda_ok):
+    """Scatter (COLUMN) and gather compute the same A^T y up to fp32 reassociation."""
+    for idx in (3, 4, 5):
+        c = H.small_config(idx)
+        p = _plan(c)
+        y = workloads.make_sino_input(c, device="cuda")
+        p.set_algorithm("adjoint", "column")
+        a = p.adjoint(y).clone()
+        p.set_algorithm("adjoint", "gather")
+        b = p.adjoint(y)
+        assert H.rel_l2(b.cpu().numpy(), a.cpu().numpy()) < 1e-5, idx
+
+
+def test_gather_rejected_for_forward(cuda_ok):
+    p = _plan(H.small_config(4))
+    with pytest.raises(XrtError):
+        p.set_algorithm("forward", "gather")
 
 
 def test_algorithms_agree(cuda_ok):
