@@ -826,11 +826,14 @@ __global__ void __launch_bounds__(256) k_gather(const ViewRec* __restrict__ view
     const double r0d = dc.cv - dc.off_v / dc.dv;
     const int r_flat = (!par && r0d == floor(r0d) && r0d >= 0 && r0d < dc.rows) ? (int)r0d : -1;
     const float kb_lo = (float)kb, kb_hi = (float)(kb + 32 * Q);
+    const float vmin = (float)((0 - dc.cv) * dc.dv + dc.off_v), vmax = (float)((dc.rows - 1 - dc.cv) * dc.dv + dc.off_v);
+    const float inv_sdd = (float)(1.0 / dc.sdd), inv_dzf = (float)g.inv_dz;
     for (int v = v0; v < v1; ++v) {
         const ViewRec V = views[v];
         const float c1 = (float)V.c1, s1 = (float)V.s1;
-        // detector u of the four corners -> candidate columns (+-1 margin)
-        float umin = INFINITY, umax = -INFINITY;
+        // detector u of the four corners -> candidate columns; rho = distance from the source along
+        // the central ray (cone: a ray through detector row v is at z = H + v rho / sdd there)
+        float umin = INFINITY, umax = -INFINITY, rmin = INFINITY, rmax = -INFINITY;
 #pragma unroll
         for (int t = 0; t < 4; ++t) {
             const float px = (t & 1) ? x1 : x0, py = (t & 2) ? y1 : y0;
@@ -839,13 +842,26 @@ __global__ void __launch_bounds__(256) k_gather(const ViewRec* __restrict__ view
                 u = -px * s1 + py * c1;
             } else {
                 const float ddx = px + Df * c1, ddy = py + Df * s1;   // P - S
-                u = sddf * __fdividef(-ddx * s1 + ddy * c1, ddx * c1 + ddy * s1);
+                const float rho = ddx * c1 + ddy * s1;
+                u = sddf * __fdividef(-ddx * s1 + ddy * c1, rho);
+                rmin = fminf(rmin, rho);
+                rmax = fmaxf(rmax, rho);
             }
             umin = fminf(umin, u);
             umax = fmaxf(umax, u);
         }
-        const int c_lo = max(0, (int)floorf((umin - (float)dc.off_u) * inv_du + (float)dc.cu) - 1);
-        const int c_hi = min(dc.cols - 1, (int)ceilf((umax - (float)dc.off_u) * inv_du + (float)dc.cu) + 1);
+        if (!par) {
+            // z cells any ray of this view can reach in the cell column; skip the view if that
+            // misses the warp's k block (helical: most views)
+            const float za = fminf(vmin * rmin, vmin * rmax) * inv_sdd, zb = fmaxf(vmax * rmin, vmax * rmax) * inv_sdd;
+            const float Hf = (float)V.H;
+            const float ua = ((float)g.z_hi - (Hf + zb)) * inv_dzf, ub = ((float)g.z_hi - (Hf + za)) * inv_dzf;
+            if (ub < kb_lo - 2.f || ua > kb_hi + 2.f) continue;
+        }
+        // a column line crosses the cell iff its u lies inside the corners' u range (the fan is
+        // monotone in u); 0.01-column margin for rounding (a spurious candidate adds exactly 0)
+        const int c_lo = max(0, (int)ceilf((umin - (float)dc.off_u) * inv_du + (float)dc.cu - 0.01f));
+        const int c_hi = min(dc.cols - 1, (int)floorf((umax - (float)dc.off_u) * inv_du + (float)dc.cu + 0.01f));
         for (int c = c_lo; c <= c_hi; ++c) {
             const ColDesc* dsc = desc + ((int64_t)v * dc.cols + c);
             const float4 q3 = __ldg(reinterpret_cast<const float4*>(dsc) + 3);   // ux0 uy0 wx wy
