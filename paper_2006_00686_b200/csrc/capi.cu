@@ -497,7 +497,35 @@ xrt_status xrt_forward_host(xrt_plan p, const float* img_host, float* sino_host,
                              cudaMemcpyHostToDevice, s));
     st = fwd_prepare(p, p->d_stage_img, s);
     if (st != XRT_OK) return st;
-    const bool whole = p->d_items && resolve(p->algo_fwd, p->column_ok) == XRT_ALGO_COLUMN;
+    if (resolve(p->algo_fwd, p->column_ok) == XRT_ALGO_COLUMN) {
+        // COLUMN: one launch per band of detector rows; the band's sinogram rows (every view) go
+        // back on the aux stream while the next band computes
+        const int nb = xrt::column_bands(p), rb = xrt::column_band_rows(p);
+        const size_t pitch = sizeof(float) * (size_t)p->det.per_view;
+        std::vector<cudaEvent_t> ev((size_t)nb);
+        for (auto& x : ev) XRT_CUDA(cudaEventCreateWithFlags(&x, cudaEventDisableTiming));
+        for (int b = 0; b < nb && st == XRT_OK; ++b) {
+            const int r0 = b * rb, r1 = std::min(p->det.rows, r0 + rb);
+            cudaError_t e = xrt::launch_forward_column_bands(p, p->d_work_fwd, p->d_stage_sino, b, b + 1, s);
+            p->launches += 1;
+            if (e == cudaSuccess) e = cudaEventRecord(ev[b], s);
+            if (e == cudaSuccess) e = cudaStreamWaitEvent(a, ev[b], 0);
+            if (e == cudaSuccess)
+                e = cudaMemcpy2DAsync(sino_host + (int64_t)r0 * p->det.cols, pitch,
+                                      p->d_stage_sino + (int64_t)r0 * p->det.cols, pitch,
+                                      sizeof(float) * (size_t)(r1 - r0) * p->det.cols, (size_t)p->n_views,
+                                      cudaMemcpyDeviceToHost, a);
+            if (e != cudaSuccess) st = cuda_fail(e, "forward_host band pipeline");
+        }
+        cudaError_t e1 = cudaStreamSynchronize(a);
+        cudaError_t e2 = cudaStreamSynchronize(s);
+        for (auto& x : ev) cudaEventDestroy(x);
+        if (st != XRT_OK) return st;
+        if (e1 != cudaSuccess) return cuda_fail(e1, "forward_host sync");
+        if (e2 != cudaSuccess) return cuda_fail(e2, "forward_host sync");
+        return XRT_OK;
+    }
+    const bool whole = false;
     const int64_t nchunk = whole ? 1 : std::min<int64_t>(8, p->n_views);
     const int64_t pv = p->det.per_view;
     std::vector<cudaEvent_t> ev((size_t)nchunk);
@@ -532,8 +560,40 @@ xrt_status xrt_adjoint_host(xrt_plan p, const float* sino_host, float* img_host,
     cudaStream_t s = (cudaStream_t)cuda_stream, a = (cudaStream_t)p->aux_stream;
     st = adj_begin(p, p->d_stage_img, s);
     if (st != XRT_OK) return st;
-    const bool whole = (p->d_items && resolve(p->algo_adj, p->column_ok) == XRT_ALGO_COLUMN) ||
-                       resolve(p->algo_adj, p->column_ok) == XRT_ALGO_GATHER;
+    if (resolve(p->algo_adj, p->column_ok) == XRT_ALGO_COLUMN) {
+        // COLUMN: the sinogram rows of band b (every view) are uploaded on the aux stream while
+        // band b - 1 computes; one launch per band
+        const int nb = xrt::column_bands(p), rb = xrt::column_band_rows(p);
+        const size_t pitch = sizeof(float) * (size_t)p->det.per_view;
+        std::vector<cudaEvent_t> ev((size_t)nb);
+        for (auto& x : ev) XRT_CUDA(cudaEventCreateWithFlags(&x, cudaEventDisableTiming));
+        for (int b = 0; b < nb && st == XRT_OK; ++b) {
+            const int r0 = b * rb, r1 = std::min(p->det.rows, r0 + rb);
+            cudaError_t e = cudaMemcpy2DAsync(p->d_stage_sino + (int64_t)r0 * p->det.cols, pitch,
+                                              sino_host + (int64_t)r0 * p->det.cols, pitch,
+                                              sizeof(float) * (size_t)(r1 - r0) * p->det.cols,
+                                              (size_t)p->n_views, cudaMemcpyHostToDevice, a);
+            if (e == cudaSuccess) e = cudaEventRecord(ev[b], a);
+            if (e == cudaSuccess) e = cudaStreamWaitEvent(s, ev[b], 0);
+            if (e == cudaSuccess) e = xrt::launch_adjoint_column_bands(p, p->d_stage_sino, p->d_work_adj, b, b + 1, s);
+            p->launches += 1;
+            if (e != cudaSuccess) st = cuda_fail(e, "adjoint_host band pipeline");
+        }
+        if (st == XRT_OK) st = adj_finish(p, p->d_stage_img, s);
+        if (st == XRT_OK) {
+            cudaError_t e = cudaMemcpyAsync(img_host, p->d_stage_img, sizeof(float) * (size_t)p->grid.nxyz,
+                                            cudaMemcpyDeviceToHost, s);
+            if (e != cudaSuccess) st = cuda_fail(e, "adjoint_host D2H");
+        }
+        cudaError_t e1 = cudaStreamSynchronize(s);
+        cudaError_t e2 = cudaStreamSynchronize(a);
+        for (auto& x : ev) cudaEventDestroy(x);
+        if (st != XRT_OK) return st;
+        if (e1 != cudaSuccess) return cuda_fail(e1, "adjoint_host sync");
+        if (e2 != cudaSuccess) return cuda_fail(e2, "adjoint_host sync");
+        return XRT_OK;
+    }
+    const bool whole = resolve(p->algo_adj, p->column_ok) == XRT_ALGO_GATHER;
     const int64_t nchunk = whole ? 1 : std::min<int64_t>(8, p->n_views);
     const int64_t pv = p->det.per_view;
     std::vector<cudaEvent_t> ev((size_t)nchunk);

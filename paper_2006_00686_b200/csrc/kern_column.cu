@@ -352,6 +352,7 @@ struct ColumnLaunch {
     const uint2* items;   // nullptr: untiled, (view, cgroup) from the block id
     int n_items;
     int n_views, n_cgroups, n_bands;
+    int band0;            // first band of this launch (bands band0 .. band0 + grid / n_items - 1)
     int tile, n_tx;       // tile side in cells, tiles along x
     int nzp, pad;
 };
@@ -572,7 +573,7 @@ __global__ void __launch_bounds__(kWarps * 32, XRT_COL_MINB) k_column(const View
     const unsigned bid = blockIdx.x;
     // band-major order: every view / column / tile of one band of detector rows (one z slab of
     // the volume) runs before the next band, so the volume working set is that slab
-    const int band = (int)(bid / (unsigned)L.n_items);
+    const int band = L.band0 + (int)(bid / (unsigned)L.n_items);
     const unsigned it = bid % (unsigned)L.n_items;
     int vv, cg, ti0 = 0, ti1 = g.n[0], tj0 = 0, tj1 = g.n[1];
     if (L.items) {
@@ -1022,6 +1023,7 @@ ColumnLaunch make_launch(const xrt_plan_s* p, int64_t v0, int64_t v1, int& nblk)
         L.items = nullptr;
         L.n_items = L.n_views * L.n_cgroups;
     }
+    L.band0 = 0;
     nblk = L.n_items * L.n_bands;
     return L;
 }
@@ -1048,6 +1050,34 @@ cudaError_t launch_forward_column(const xrt_plan_s* p, const float* vol_zfast, f
     cudaError_t e = cudaMemsetAsync(sino + v0 * p->det.per_view, 0, sizeof(float) * (size_t)((v1 - v0) * p->det.per_view), s);
     if (e != cudaSuccess) return e;
     return launch_column<false>(p, vol_zfast, nullptr, nullptr, sino, v0, L, nblk, s);
+}
+
+// All views, detector-row bands [b0, b1) only (host pipelines: the sinogram rows of one band are
+// transferred while the next band computes).  Rows of band b: [b * rows_per_band, ...).
+int column_band_rows(const xrt_plan_s* p) { return 64 * p->col_np; }
+int column_bands(const xrt_plan_s* p) { return (p->det.rows + 64 * p->col_np - 1) / (64 * p->col_np); }
+
+cudaError_t launch_forward_column_bands(const xrt_plan_s* p, const float* vol_zfast, float* sino, int b0,
+                                        int b1, cudaStream_t s) {
+    int nblk = 0;
+    ColumnLaunch L = make_launch(p, 0, p->n_views, nblk);
+    const int rb = column_band_rows(p);
+    const int r0 = b0 * rb, r1 = std::min(p->det.rows, b1 * rb);
+    if (r1 <= r0) return cudaSuccess;
+    const size_t pitch = sizeof(float) * (size_t)p->det.per_view;
+    cudaError_t e = cudaMemset2DAsync(sino + (int64_t)r0 * p->det.cols, pitch, 0,
+                                      sizeof(float) * (size_t)(r1 - r0) * p->det.cols, (size_t)p->n_views, s);
+    if (e != cudaSuccess) return e;
+    L.band0 = b0;
+    return launch_column<false>(p, vol_zfast, nullptr, nullptr, sino, 0, L, L.n_items * (b1 - b0), s);
+}
+
+cudaError_t launch_adjoint_column_bands(const xrt_plan_s* p, const float* sino, float* vol_zfast, int b0,
+                                        int b1, cudaStream_t s) {
+    int nblk = 0;
+    ColumnLaunch L = make_launch(p, 0, p->n_views, nblk);
+    L.band0 = b0;
+    return launch_column<true>(p, nullptr, vol_zfast, sino, nullptr, 0, L, L.n_items * (b1 - b0), s);
 }
 
 cudaError_t launch_adjoint_column(const xrt_plan_s* p, const float* sino, float* vol_zfast,

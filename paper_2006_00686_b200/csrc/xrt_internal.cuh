@@ -232,4 +232,10 @@ int column_cta_columns();
 cudaError_t launch_col_desc(const xrt_plan_s* p, cudaStream_t s);
 cudaError_t launch_adjoint_gather(const xrt_plan_s* p, const float* sino, float* vol_zfast, cudaStream_t s);
 int64_t gather_launches(const xrt_plan_s* p);
+int column_band_rows(const xrt_plan_s* p);
+int column_bands(const xrt_plan_s* p);
+cudaError_t launch_forward_column_bands(const xrt_plan_s* p, const float* vol_zfast, float* sino, int b0,
+                                        int b1, cudaStream_t s);
+cudaError_t launch_adjoint_column_bands(const xrt_plan_s* p, const float* sino, float* vol_zfast, int b0,
+                                        int b1, cudaStream_t s);
 }  // namespace xrt
