@@ -135,6 +135,14 @@ xrt_status xrt_forward(xrt_plan p, const float* img, float* sino, void* cuda_str
  * overwritten with A^T sino. */
 xrt_status xrt_adjoint(xrt_plan p, const float* sino, float* img, void* cuda_stream);
 
+/* fp64 variants (the paper's "switching float ... into double"): the same
+ * operator with the fp64 unit enumeration of xrt_ray_units (units with l <= tau dropped) and fp64
+ * sums.  img: device fp64 [N_z][N_y][N_x]; sino: device fp64 [n_views][det_rows][det_cols]; the
+ * output is fully overwritten.  One thread per ray (RAY family), every geometry.  The adjoint
+ * accumulates with fp64 atomics, so its last bits depend on the order of execution. */
+xrt_status xrt_forward_f64(xrt_plan p, const double* img, double* sino, void* cuda_stream);
+xrt_status xrt_adjoint_f64(xrt_plan p, const double* sino, double* img, void* cuda_stream);
+
 /* As xrt_forward / xrt_adjoint but with HOST buffers (pageable or pinned): the host->device copy
  * of the input, the kernels and the device->host copy of the output all run inside the call,
  * pipelined over view chunks; returns after the output is in host memory. */

@@ -485,6 +485,26 @@ xrt_status xrt_adjoint(xrt_plan p, const float* sino, float* img, void* cuda_str
     return st;
 }
 
+xrt_status xrt_forward_f64(xrt_plan p, const double* img, double* sino, void* cuda_stream) {
+    if (!p || !img || !sino) return fail(XRT_ERR_INVALID_ARG, "NULL argument");
+    DevGuard guard(p->device);
+    cudaError_t e = xrt::launch_forward64(p, img, sino, 0, p->n_rays, (cudaStream_t)cuda_stream);
+    p->launches += 1;
+    if (e != cudaSuccess) return cuda_fail(e, "forward_f64 launch");
+    return XRT_OK;
+}
+
+xrt_status xrt_adjoint_f64(xrt_plan p, const double* sino, double* img, void* cuda_stream) {
+    if (!p || !img || !sino) return fail(XRT_ERR_INVALID_ARG, "NULL argument");
+    DevGuard guard(p->device);
+    cudaStream_t s = (cudaStream_t)cuda_stream;
+    XRT_CUDA(cudaMemsetAsync(img, 0, sizeof(double) * (size_t)p->grid.nxyz, s));
+    cudaError_t e = xrt::launch_adjoint64(p, sino, img, 0, p->n_rays, s);
+    p->launches += 1;
+    if (e != cudaSuccess) return cuda_fail(e, "adjoint_f64 launch");
+    return XRT_OK;
+}
+
 // Host-buffer forward: H2D(image) -> per view chunk: kernel, then D2H of that chunk on the aux
 // stream, so the sinogram download overlaps the next chunk's kernel.
 xrt_status xrt_forward_host(xrt_plan p, const float* img_host, float* sino_host, void* cuda_stream) {

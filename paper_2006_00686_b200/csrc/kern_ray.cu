@@ -207,6 +207,82 @@ __global__ void __launch_bounds__(128) k_units_fill(const ViewRec* __restrict__ 
     }
 }
 
+// fp64 forward / adjoint (the paper's own precision option: "switching float ...
+// into double"): the same fp64 enumeration as the CSR dump (units64), lengths and sums in
+// double.  One thread per ray.
+__global__ void __launch_bounds__(128) k_forward64(const ViewRec* __restrict__ views, DetC dc, GridC g,
+                                                    const double* __restrict__ img, double* __restrict__ sino,
+                                                    int64_t ray0, int64_t ray1) {
+    const int64_t m = ray0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (m >= ray1) return;
+    int v, r, c;
+    ray_of(m, dc, v, r, c);
+    Ray64 R;
+    double acc = 0.0;
+    if (setup_ray(views[v], dc, g, r, c, R)) {
+        int cell[3] = {R.cell[0], R.cell[1], R.cell[2]};
+        double T[3];
+        int bnd[3], sgn[3];
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            if (!R.moving[a]) { T[a] = INFINITY; bnd[a] = 0; sgn[a] = 0; continue; }
+            sgn[a] = R.w[a] > 0.0 ? 1 : -1;
+            bnd[a] = sgn[a] > 0 ? cell[a] + 1 : cell[a];
+            T[a] = ((double)bnd[a] - R.u0[a]) * R.inv_w[a];
+        }
+        double t = R.t_in;
+        const int budget = 2 + g.n[0] + g.n[1] + g.n[2];
+        for (int it = 0; it < budget; ++it) {
+            const double tn = fmin(fmin(T[0], T[1]), fmin(T[2], R.t_out));
+            const double l = tn - t;   // C_up - C_low (eq:range_length_3D)
+            if (l > g.tau) acc = fma(img[((int64_t)cell[2] * g.n[1] + cell[1]) * g.n[0] + cell[0]], l, acc);
+            if (tn >= R.t_out) break;
+            const int a = (tn == T[0]) ? 0 : ((tn == T[1]) ? 1 : 2);
+            cell[a] += sgn[a];
+            bnd[a] += sgn[a];
+            T[a] = ((double)bnd[a] - R.u0[a]) * R.inv_w[a];
+            t = tn;
+        }
+    }
+    sino[m] = acc;
+}
+
+__global__ void __launch_bounds__(128) k_adjoint64(const ViewRec* __restrict__ views, DetC dc, GridC g,
+                                                    const double* __restrict__ sino, double* __restrict__ img,
+                                                    int64_t ray0, int64_t ray1) {
+    const int64_t m = ray0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (m >= ray1) return;
+    const double y = sino[m];
+    if (y == 0.0) return;
+    int v, r, c;
+    ray_of(m, dc, v, r, c);
+    Ray64 R;
+    if (!setup_ray(views[v], dc, g, r, c, R)) return;
+    int cell[3] = {R.cell[0], R.cell[1], R.cell[2]};
+    double T[3];
+    int bnd[3], sgn[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        if (!R.moving[a]) { T[a] = INFINITY; bnd[a] = 0; sgn[a] = 0; continue; }
+        sgn[a] = R.w[a] > 0.0 ? 1 : -1;
+        bnd[a] = sgn[a] > 0 ? cell[a] + 1 : cell[a];
+        T[a] = ((double)bnd[a] - R.u0[a]) * R.inv_w[a];
+    }
+    double t = R.t_in;
+    const int budget = 2 + g.n[0] + g.n[1] + g.n[2];
+    for (int it = 0; it < budget; ++it) {
+        const double tn = fmin(fmin(T[0], T[1]), fmin(T[2], R.t_out));
+        const double l = tn - t;
+        if (l > g.tau) atomicAdd(img + ((int64_t)cell[2] * g.n[1] + cell[1]) * g.n[0] + cell[0], y * l);
+        if (tn >= R.t_out) break;
+        const int a = (tn == T[0]) ? 0 : ((tn == T[1]) ? 1 : 2);
+        cell[a] += sgn[a];
+        bnd[a] += sgn[a];
+        T[a] = ((double)bnd[a] - R.u0[a]) * R.inv_w[a];
+        t = tn;
+    }
+}
+
 inline unsigned blocks_for(int64_t n, int bs) { return (unsigned)((n + bs - 1) / bs); }
 
 }  // namespace
@@ -224,6 +300,20 @@ cudaError_t launch_adjoint_ray(const xrt_plan_s* p, const float* sino, float* im
     if (ray1 <= ray0) return cudaSuccess;
     k_adjoint_ray<<<blocks_for(ray1 - ray0, 256), 256, 0, s>>>(p->d_views, p->det, p->grid, sino,
                                                                img, ray0, ray1);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_forward64(const xrt_plan_s* p, const double* img, double* sino, int64_t ray0,
+                             int64_t ray1, cudaStream_t s) {
+    if (ray1 <= ray0) return cudaSuccess;
+    k_forward64<<<blocks_for(ray1 - ray0, 128), 128, 0, s>>>(p->d_views, p->det, p->grid, img, sino, ray0, ray1);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_adjoint64(const xrt_plan_s* p, const double* sino, double* img, int64_t ray0,
+                             int64_t ray1, cudaStream_t s) {
+    if (ray1 <= ray0) return cudaSuccess;
+    k_adjoint64<<<blocks_for(ray1 - ray0, 128), 128, 0, s>>>(p->d_views, p->det, p->grid, sino, img, ray0, ray1);
     return cudaGetLastError();
 }
 

@@ -97,9 +97,9 @@ class Plan:
         check(self._lib.xrt_plan_set_algorithm(self._h, o, _lib.ALGOS[algo]))
 
     # -------------------------------------------------------------- operators
-    def _check_dev(self, t: torch.Tensor, shape, name):
-        if not (t.is_cuda and t.dtype == torch.float32 and t.is_contiguous()):
-            raise ValueError(f"{name} must be a contiguous float32 CUDA tensor")
+    def _check_dev(self, t: torch.Tensor, shape, name, dtype=torch.float32):
+        if not (t.is_cuda and t.dtype == dtype and t.is_contiguous()):
+            raise ValueError(f"{name} must be a contiguous {dtype} CUDA tensor")
         if t.device.index != self.device:
             raise ValueError(f"{name} is on cuda:{t.device.index}, plan on cuda:{self.device}")
         if t.numel() != int(np.prod(shape)):
@@ -121,6 +121,24 @@ class Plan:
             out = torch.empty(self.image_shape, dtype=torch.float32, device=sino.device)
         self._check_dev(out, self.image_shape, "img")
         check(self._lib.xrt_adjoint(self._h, sino.data_ptr(), out.data_ptr(), _stream_handle(stream)))
+        return out
+
+    def forward64(self, img: torch.Tensor, out: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+        """xrt_forward_f64: the same operator in fp64 (P:725's double option)."""
+        self._check_dev(img, self.image_shape, "img", torch.float64)
+        if out is None:
+            out = torch.empty(self.sino_shape, dtype=torch.float64, device=img.device)
+        self._check_dev(out, self.sino_shape, "sino", torch.float64)
+        check(self._lib.xrt_forward_f64(self._h, img.data_ptr(), out.data_ptr(), _stream_handle(stream)))
+        return out
+
+    def adjoint64(self, sino: torch.Tensor, out: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+        """xrt_adjoint_f64."""
+        self._check_dev(sino, self.sino_shape, "sino", torch.float64)
+        if out is None:
+            out = torch.empty(self.image_shape, dtype=torch.float64, device=sino.device)
+        self._check_dev(out, self.image_shape, "img", torch.float64)
+        check(self._lib.xrt_adjoint_f64(self._h, sino.data_ptr(), out.data_ptr(), _stream_handle(stream)))
         return out
 
     def forward_host(self, img: torch.Tensor, out: torch.Tensor | None = None, stream=None) -> torch.Tensor:

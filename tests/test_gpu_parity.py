@@ -328,3 +328,39 @@ def test_host_band_pipeline_tiled(cuda_ok, idx, monkeypatch):
     a_dev = p.adjoint(y.cuda())
     a_host = p.adjoint_host(y.contiguous())
     assert H.rel_l2(a_host.numpy(), a_dev.cpu().numpy()) < 1e-6
+
+
+# ------------------------------------------------------------------- fp64 variant
+F64_TOL = 1e-11   # fp64 lengths and sums vs the fp64 brute-force oracle: rounding order only
+
+
+@pytest.mark.parametrize("idx", [1, 2, 3, 4, 5])
+def test_forward64_small_every_ray(cuda_ok, idx):
+    c = H.small_config(idx)
+    p = _plan(c)
+    img = _image(c)
+    sino = p.forward64(img.double())
+    ref = H.oracle_forward(c, img.cpu(), H.ray_ids_all(c))
+    assert H.fwd_err(sino.cpu().numpy().ravel(), ref) <= F64_TOL
+
+
+@pytest.mark.parametrize("idx", [1, 3, 4, 5])
+def test_adjoint64_small_sparse_parity(cuda_ok, idx):
+    c = H.small_config(idx)
+    p = _plan(c)
+    ids = workloads.sample_rays(c, min(p.n_rays, 2000), seed=900 + idx)
+    y = np.zeros(p.n_rays)
+    y[ids] = np.random.Generator(np.random.PCG64(910 + idx)).uniform(-1, 1, size=ids.size)
+    back = p.adjoint64(torch.from_numpy(y).reshape(p.sino_shape).cuda())
+    ref = H.oracle_adjoint(c, y[ids], ids)
+    assert H.rel_l2(back.cpu().numpy().ravel(), ref) <= F64_TOL
+
+
+def test_forward64_agrees_with_fp32(cuda_ok):
+    """fp32 (production) and fp64 forwards differ only by fp32 rounding (<= the 1e-5 bar)."""
+    c = H.small_config(4)
+    p = _plan(c)
+    img = _image(c)
+    a = p.forward(img).double()
+    b = p.forward64(img.double())
+    assert H.fwd_err(a.cpu().numpy().ravel(), b.cpu().numpy().ravel()) <= H.FWD_TOL
