@@ -32,6 +32,10 @@
  *                 +u = (-sin p, cos p, 0), +v = +z.
  *     XRT_HELICAL as XRT_CONE with source height H(p) = z0 + pitch*p/(2 pi) (detector moves
  *                 with the source; angles are unwrapped and may exceed 2 pi).
+ *   detector  flat by default (equispaced columns, P:268-272 / P:627-642).  flags & XRT_DET_CURVED
+ *             (fan / cone / helical only): a cylinder of radius sdd about the source, columns
+ *             equiangular with fan angle alpha_c = u_c / sdd, rows flat with tan(beta) = v_r / sdd;
+ *             rays by the paper's equiangular transforms.
  *
  * Ownership: every image / sinogram / CSR buffer is caller-allocated device memory (e.g. a torch
  * tensor's data_ptr()) unless the function name ends in _host.  The plan owns only its geometry
@@ -68,6 +72,8 @@ typedef enum {
     XRT_ERR_CAPACITY = 5     /* xrt_ray_units: caller capacity < nnz (nnz_out still set)     */
 } xrt_status;
 
+#define XRT_DET_CURVED 1 /* xrt_geometry.flags: cylindrical (equiangular-column) detector */
+
 typedef enum {
     XRT_PAR2D = 0,
     XRT_FAN2D = 1,
@@ -79,7 +85,7 @@ typedef enum {
 /* Acquisition geometry.  All lengths in the same physical unit (e.g. mm), angles in radians. */
 typedef struct {
     int32_t beam;            /* xrt_beam                                                         */
-    int32_t reserved0;       /* must be 0                                                        */
+    int32_t flags;           /* XRT_DET_CURVED or 0; other bits must be 0                        */
     int64_t n[3];            /* N_x, N_y, N_z >= 1 (N_z = 1 for 2D beams)                         */
     double spacing[3];       /* d_x, d_y, d_z > 0 (anisotropic allowed; d_z ignored for 2D)       */
     double center[3];        /* physical centre of the image box (z ignored for 2D)              */
@@ -112,7 +118,8 @@ typedef enum {
 /* Validate `g`, build the per-view geometry tables on `cuda_device` and allocate workspace.
  * Errors: XRT_ERR_INVALID_ARG (non-finite values, n <= 0, spacing <= 0, n_views <= 0,
  * angles == NULL, det_rows != 1 for 2D, sod <= 0 or sdd <= sod for divergent beams,
- * |tilt| >= pi/2, reserved0 != 0); XRT_ERR_OOM; XRT_ERR_CUDA. */
+ * |tilt| >= pi/2, unknown flags, XRT_DET_CURVED with a parallel beam or a fan half-angle
+ * >= pi/2); XRT_ERR_OOM; XRT_ERR_CUDA. */
 xrt_status xrt_plan_create(const xrt_geometry* g, int cuda_device, xrt_plan* out);
 xrt_status xrt_plan_destroy(xrt_plan p);
 

@@ -155,6 +155,9 @@ def rays(c: dict, ids) -> tuple[np.ndarray, np.ndarray]:
     if beam in ("par2d", "fan2d"):
         if beam == "par2d":
             s, phi = u, ang                                   # ray (s, phi)
+        elif c.get("det_curved", False):
+            # cylindrical detector of radius sdd: equiangular fan angle gamma = u / sdd
+            s, phi = fan_equiangular_to_parallel(c["sod"], ang, u / c["sdd"])
         else:
             D = c["sod"]
             t = u * c["sod"] / c["sdd"]                       # flat detector scaled to the iso plane (reading 8)
@@ -165,6 +168,15 @@ def rays(c: dict, ids) -> tuple[np.ndarray, np.ndarray]:
     else:
         if beam == "par3d":
             s1, s2, phi1, phi2 = u, v, ang, np.full(n, c.get("tilt", 0.0))
+        elif beam in ("cone", "helical") and c.get("det_curved", False):
+            # cylindrical detector: alpha = u / sdd (equiangular columns), tan(beta) = v / sdd (flat
+            # rows); the equiangular transforms P:619-624 / P:652-654
+            alpha, beta = u / c["sdd"], np.arctan(v / c["sdd"])
+            if beam == "cone":
+                s1, s2, phi1, phi2 = cone_equiangular_to_parallel(c["sod"], ang, alpha, beta)
+            else:
+                H = c["z0"] + c["pitch"] * ang / (2 * math.pi)
+                s1, s2, phi1, phi2 = helical_equiangular_to_parallel(c["sod"], ang, alpha, beta, H)
         elif beam == "cone":
             t = u * c["sod"] / c["sdd"]
             h = v * c["sod"] / c["sdd"]

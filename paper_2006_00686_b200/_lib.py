@@ -18,6 +18,7 @@ STATUS_NAMES = {0: "XRT_OK", 1: "XRT_ERR_INVALID_ARG", 2: "XRT_ERR_UNSUPPORTED",
                 4: "XRT_ERR_OOM", 5: "XRT_ERR_CAPACITY"}
 BEAMS = {"par2d": 0, "fan2d": 1, "par3d": 2, "cone": 3, "helical": 4}
 OP_FORWARD, OP_ADJOINT = 0, 1
+DET_CURVED = 1
 ALGO_AUTO, ALGO_RAY, ALGO_COLUMN, ALGO_GATHER = 0, 1, 2, 3
 ALGOS = {"auto": 0, "ray": 1, "column": 2, "gather": 3}
 
@@ -29,7 +30,7 @@ EXPORTS = ("xrt_plan_create", "xrt_plan_destroy", "xrt_plan_query", "xrt_plan_se
 
 class XrtGeometry(ctypes.Structure):
     _fields_ = [
-        ("beam", ctypes.c_int32), ("reserved0", ctypes.c_int32),
+        ("beam", ctypes.c_int32), ("flags", ctypes.c_int32),
         ("n", ctypes.c_int64 * 3), ("spacing", ctypes.c_double * 3), ("center", ctypes.c_double * 3),
         ("n_views", ctypes.c_int64), ("angles", ctypes.POINTER(ctypes.c_double)),
         ("det_cols", ctypes.c_int64), ("det_rows", ctypes.c_int64),

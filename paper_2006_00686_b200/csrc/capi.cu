@@ -58,7 +58,7 @@ struct DevGuard {
 
 xrt_status validate(const xrt_geometry* g) {
     if (!g) return fail(XRT_ERR_INVALID_ARG, "geometry is NULL");
-    if (g->reserved0 != 0) return fail(XRT_ERR_INVALID_ARG, "reserved0 must be 0");
+    if (g->flags & ~XRT_DET_CURVED) return fail(XRT_ERR_INVALID_ARG, "unknown flags 0x%x", (unsigned)g->flags);
     if (g->beam < XRT_PAR2D || g->beam > XRT_HELICAL) return fail(XRT_ERR_INVALID_ARG, "unknown beam %d", g->beam);
     const bool is2d = g->beam == XRT_PAR2D || g->beam == XRT_FAN2D;
     const bool divergent = g->beam == XRT_FAN2D || g->beam == XRT_CONE || g->beam == XRT_HELICAL;
@@ -88,6 +88,12 @@ xrt_status validate(const xrt_geometry* g) {
     if (divergent) {
         if (!(std::isfinite(g->sod) && g->sod > 0)) return fail(XRT_ERR_INVALID_ARG, "sod must be > 0");
         if (!(std::isfinite(g->sdd) && g->sdd > g->sod)) return fail(XRT_ERR_INVALID_ARG, "sdd must be > sod");
+    }
+    if ((g->flags & XRT_DET_CURVED) && !divergent)
+        return fail(XRT_ERR_INVALID_ARG, "XRT_DET_CURVED needs a fan / cone / helical beam");
+    if (g->flags & XRT_DET_CURVED) {
+        const double half = ((g->det_cols - 1) / 2.0) * g->det_spacing[0] + std::fabs(g->det_offset[0]);
+        if (!(half / g->sdd < M_PI / 2)) return fail(XRT_ERR_INVALID_ARG, "curved detector fan half-angle >= pi/2");
     }
     if (g->beam == XRT_HELICAL && !(std::isfinite(g->pitch) && std::isfinite(g->z0)))
         return fail(XRT_ERR_INVALID_ARG, "pitch / z0 not finite");
@@ -348,6 +354,7 @@ xrt_status xrt_plan_create(const xrt_geometry* g, int cuda_device, xrt_plan* out
     G.nxyz = G.nxy * G.n[2];
     xrt::DetC& D = p->det;
     D.beam = g->beam;
+    D.curved = (g->flags & XRT_DET_CURVED) ? 1 : 0;
     D.D = g->sod;
     D.sdd = g->sdd;
     D.inv_D = g->sod > 0 ? 1.0 / g->sod : 0.0;

@@ -82,9 +82,14 @@ __host__ __device__ __forceinline__ void column_line(const ViewRec& V, const Det
         ca_out = 1.0;
     } else {
         const double D = dc.D;
-        const double t = u * D / dc.sdd;
-        const double sq = sqrt(D * D + t * t);
-        const double ca = D / sq, sa = t / sq;           // alpha = arctan(t / D)
+        double ca, sa;
+        if (dc.curved) {                                 // equiangular column: alpha = u / sdd
+            ca = cos(u / dc.sdd); sa = sin(u / dc.sdd);
+        } else {
+            const double t = u * D / dc.sdd;
+            const double sq = sqrt(D * D + t * t);
+            ca = D / sq; sa = t / sq;                    // alpha = arctan(t / D)
+        }
         const double s1 = D * sa;
         const double c1 = V.c1 * ca - V.s1 * sa;         // phi1 = phi1' + alpha
         const double n1 = V.s1 * ca + V.c1 * sa;
@@ -318,11 +323,18 @@ __device__ __forceinline__ void ray_z(const ViewRec& V, const DetC& dc, const Gr
         if (fabs(V.s2) <= kSnap) { tb = 0.0; z0 = v * V.c2; }
         else { tb = V.pad[0]; z0 = v * V.pad[1]; }      // tan(phi2), 1 / cos(phi2) (plan)
     } else {
-        // tan(beta) = h / sqrt(D^2 + t^2) = h cos(alpha) / D, z(sigma=0) = s2 / cos(beta) = h cos^2
-        // (alpha) + H  (P:636, P:660 divided by cos(beta))
-        const double h = v * dc.D / dc.sdd;
-        tb = h * ca * dc.inv_D;
-        z0 = h * (ca * ca) + V.H;
+        if (dc.curved) {
+            // cylindrical detector: tan(beta) = v / sdd, z(sigma=0) = s2 / cos(beta) = D cos(alpha)
+            // tan(beta) + H  (P:622, P:654 divided by cos(beta))
+            tb = v / dc.sdd;
+            z0 = dc.D * ca * tb + V.H;
+        } else {
+            // tan(beta) = h / sqrt(D^2 + t^2) = h cos(alpha) / D, z(sigma=0) = s2 / cos(beta) = h cos^2
+            // (alpha) + H  (P:636, P:660 divided by cos(beta))
+            const double h = v * dc.D / dc.sdd;
+            tb = h * ca * dc.inv_D;
+            z0 = h * (ca * ca) + V.H;
+        }
         if (fabs(tb) <= kSnap) tb = 0.0;
     }
     Z.scale = sqrtf(1.f + (float)(tb * tb));           // 1 / cos(beta)
@@ -771,7 +783,7 @@ __global__ void k_gather_prep(const ViewRec* __restrict__ views, DetC dc, const 
                 const double vr = ((double)r - dc.cv) * dc.dv + dc.off_v;
                 const double h = vr * dc.D / dc.sdd;
                 const double ca = __ldg(reinterpret_cast<const double2*>(desc + ((int64_t)v * dc.cols + c)) + 4).y;
-                tb = h * ca * dc.inv_D;
+                tb = dc.curved ? vr / dc.sdd : h * ca * dc.inv_D;
                 if (fabs(tb) <= kSnap) tb = 0.0;
             }
             const float scale = sqrtf(1.f + (float)(tb * tb));   // as ray_z
@@ -844,9 +856,13 @@ __global__ void __launch_bounds__(256) k_gather(const ViewRec* __restrict__ view
             } else {
                 const float ddx = px + Df * c1, ddy = py + Df * s1;   // P - S
                 const float rho = ddx * c1 + ddy * s1;
-                u = sddf * __fdividef(-ddx * s1 + ddy * c1, rho);
-                rmin = fminf(rmin, rho);
-                rmax = fmaxf(rmax, rho);
+                u = dc.curved ? sddf * atan2f(-ddx * s1 + ddy * c1, rho)        // arc length on the cylinder
+                              : sddf * __fdividef(-ddx * s1 + ddy * c1, rho);
+                // z = H + v rho / sdd along the ray: rho = distance along the central ray (flat) or
+                // the in-plane distance from the source (cylindrical detector)
+                const float rz = dc.curved ? sqrtf(ddx * ddx + ddy * ddy) : rho;
+                rmin = fminf(rmin, rz);
+                rmax = fmaxf(rmax, rz);
             }
             umin = fminf(umin, u);
             umax = fmaxf(umax, u);
@@ -895,9 +911,12 @@ __global__ void __launch_bounds__(256) k_gather(const ViewRec* __restrict__ view
                 G1d = 0.0;
                 Td = tb * g.inv_dz;
             } else {
+                // z(sigma) = H + h (lam + sigma_abs kap): flat lam = ca^2, kap = ca / D; curved
+                // (tan(beta) = v / sdd = h / D, z(0) = D ca tan(beta)) lam = ca, kap = 1 / D
+                const double lam = dc.curved ? q4.y : q4.y * q4.y, kap = dc.curved ? dc.inv_D : q4.y * dc.inv_D;
                 Ad = (g.z_hi - V.H) * g.inv_dz;
-                G0d = (q4.y * q4.y + q4.x * q4.y * dc.inv_D) * g.inv_dz;
-                G1d = q4.y * dc.inv_D * g.inv_dz;
+                G0d = (lam + q4.x * kap) * g.inv_dz;
+                G1d = kap * g.inv_dz;
                 Td = 0.0;
             }
             const float A = (float)Ad, G0 = (float)G0d, G1 = (float)G1d, T = (float)Td;

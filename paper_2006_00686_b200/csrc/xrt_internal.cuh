@@ -45,6 +45,7 @@ struct GridC {
 
 struct DetC {
     int beam;                              // xrt_beam
+    int curved;                            // 1: cylindrical detector (equiangular columns, XRT_DET_CURVED)
     double D, sdd;                         // source-to-origin / -detector distances
     double inv_D;                          // 1 / D
     int cols, rows;
@@ -78,11 +79,16 @@ __device__ __forceinline__ void paper_ray(const ViewRec& V, const DetC& dc, int 
             p[0] = -u * V.s1; p[1] = u * V.c1; p[2] = 0.0;
             break;
         }
-        case XRT_FAN2D: {  // equispaced fan, t on the iso plane
-            const double t = u * D / dc.sdd;
-            const double den = sqrt(D * D + t * t);
-            const double cg = D / den, sg = t / den;          // cos/sin(arctan(t/D))
-            const double s = D * t / den;
+        case XRT_FAN2D: {  // fan: equispaced (flat, t on the iso plane) or equiangular (curved)
+            double cg, sg;
+            if (dc.curved) {                                  // gamma = u / sdd
+                sincos(u / dc.sdd, &sg, &cg);
+            } else {
+                const double t = u * D / dc.sdd;
+                const double den = sqrt(D * D + t * t);
+                cg = D / den; sg = t / den;                   // cos/sin(arctan(t/D))
+            }
+            const double s = D * sg;                          // s = D sin(gamma)
             const double cp = V.c1 * cg - V.s1 * sg;          // cos(gamma + alpha - pi/2)
             const double sp = V.s1 * cg + V.c1 * sg;
             th[0] = cp; th[1] = sp; th[2] = 0.0;
@@ -97,16 +103,26 @@ __device__ __forceinline__ void paper_ray(const ViewRec& V, const DetC& dc, int 
             p[2] = v * c2;
             break;
         }
-        default: {  // cone / helical, equispaced flat detector
-            const double t = u * D / dc.sdd;
-            const double h = v * D / dc.sdd;
-            const double q = D * D + t * t;
-            const double sq = sqrt(q);
-            const double ca = D / sq, sa = t / sq;            // alpha = arctan(t / D)
-            const double r3 = sqrt(q + h * h);
-            const double cb = sq / r3, sb = h / r3;           // beta = arctan(h / sqrt(D^2+t^2))
+        default: {  // cone / helical
+            double ca, sa, cb, sb, s2;
+            if (dc.curved) {
+                // equiangular columns alpha = u / sdd, flat rows tan(beta) = v / sdd:
+                // s1 = D sin(alpha), s2 = D cos(alpha) sin(beta) (+ H cos(beta))
+                sincos(u / dc.sdd, &sa, &ca);
+                const double tb = v / dc.sdd, r3 = sqrt(1.0 + tb * tb);
+                cb = 1.0 / r3; sb = tb / r3;
+                s2 = D * ca * sb + V.H * cb;
+            } else {
+                const double t = u * D / dc.sdd;
+                const double h = v * D / dc.sdd;
+                const double q = D * D + t * t;
+                const double sq = sqrt(q);
+                ca = D / sq; sa = t / sq;                     // alpha = arctan(t / D)
+                const double r3 = sqrt(q + h * h);
+                cb = sq / r3; sb = h / r3;                    // beta = arctan(h / sqrt(D^2+t^2))
+                s2 = h * (ca * ca) * cb + V.H * cb;
+            }
             const double s1 = D * sa;
-            const double s2 = h * (ca * ca) * cb + V.H * cb;
             const double c1 = V.c1 * ca - V.s1 * sa;          // phi1 = phi1' + alpha
             const double n1 = V.s1 * ca + V.c1 * sa;
             th[0] = cb * c1; th[1] = cb * n1; th[2] = sb;

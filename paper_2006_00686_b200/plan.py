@@ -19,7 +19,7 @@ def _geometry_struct(g: dict) -> tuple[_lib.XrtGeometry, np.ndarray]:
     angles = np.ascontiguousarray(np.asarray(g["angles"], dtype=np.float64))
     s = _lib.XrtGeometry()
     s.beam = _lib.BEAMS[g["beam"]] if isinstance(g["beam"], str) else int(g["beam"])
-    s.reserved0 = 0
+    s.flags = _lib.DET_CURVED if g.get("det_curved", False) else 0
     for a in range(3):
         s.n[a] = int(g["n"][a])
         s.spacing[a] = float(g["spacing"][a])

@@ -57,6 +57,7 @@ def _geom(**kw):
     dict(angles=np.array([math.inf])), dict(det_cols=0), dict(det_spacing=(0, 1)), dict(sod=0.0),
     dict(sdd=5.0), dict(beam="par2d", n=(8, 8, 2), det_rows=1), dict(beam="fan2d", n=(8, 8, 1), det_rows=3),
     dict(beam="par3d", tilt=2.0), dict(center=(0, math.inf, 0)),
+    dict(beam="par3d", det_curved=True), dict(det_curved=True, det_cols=200, det_spacing=(1, 1)),
 ])
 def test_invalid_geometry_rejected(lib, bad):
     s, keep = _geometry_struct(_geom(**bad))
@@ -65,6 +66,14 @@ def test_invalid_geometry_rejected(lib, bad):
     assert st == _lib.XRT_ERR_INVALID_ARG
     assert h.value is None
     assert lib.xrt_last_error()
+
+
+def test_unknown_flags_rejected(lib):
+    s, keep = _geometry_struct(_geom())
+    s.flags = 6
+    h = ctypes.c_void_p()
+    assert lib.xrt_plan_create(ctypes.byref(s), 0, ctypes.byref(h)) == _lib.XRT_ERR_INVALID_ARG
+    assert b"flags" in lib.xrt_last_error()
 
 
 def test_null_arguments(lib):

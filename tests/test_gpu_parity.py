@@ -364,3 +364,42 @@ def test_forward64_agrees_with_fp32(cuda_ok):
     a = p.forward(img).double()
     b = p.forward64(img.double())
     assert H.fwd_err(a.cpu().numpy().ravel(), b.cpu().numpy().ravel()) <= H.FWD_TOL
+
+
+# ------------------------------------------------------------------- cylindrical detector (N1)
+def _curved(idx):
+    c = H.small_config(idx)
+    c["det_curved"] = True
+    return c
+
+
+@pytest.mark.parametrize("idx", [2, 4, 5])
+def test_curved_csr_every_ray(cuda_ok, idx):
+    c = _curved(idx)
+    p = _plan(c)
+    ids = H.ray_ids_all(c)
+    H.compare_csr(p.ray_units(0, p.n_rays), H.oracle_csr(c, ids), f"curved cfg{idx}")
+
+
+@pytest.mark.parametrize("algo", ALGOS)
+@pytest.mark.parametrize("idx", [2, 4, 5])
+def test_curved_forward_every_ray(cuda_ok, idx, algo):
+    c = _curved(idx)
+    p = _plan(c, algo)
+    img = _image(c)
+    sino = p.forward(img)
+    ref = H.oracle_forward(c, img.cpu(), H.ray_ids_all(c))
+    assert H.fwd_err(sino.cpu().numpy().ravel(), ref) <= H.FWD_TOL
+
+
+@pytest.mark.parametrize("algo", ADJ_ALGOS)
+@pytest.mark.parametrize("idx", [2, 4, 5])
+def test_curved_adjoint_sparse_parity(cuda_ok, idx, algo):
+    c = _curved(idx)
+    p = _plan(c, algo)
+    ids = workloads.sample_rays(c, min(p.n_rays, 2000), seed=950 + idx)
+    y = np.zeros(p.n_rays, dtype=np.float32)
+    y[ids] = np.random.Generator(np.random.PCG64(960 + idx)).uniform(-1, 1, size=ids.size).astype(np.float32)
+    back = p.adjoint(torch.from_numpy(y).reshape(p.sino_shape).cuda())
+    ref = H.oracle_adjoint(c, y[ids].astype(np.float64), ids)
+    assert H.rel_l2(back.cpu().numpy().ravel(), ref) <= H.ADJ_TOL

@@ -267,3 +267,42 @@ def test_canonicalization_same_line():
         assert abs(abs(th @ tc) - 1) < 1e-12
         d = pb - pa
         assert np.linalg.norm(d - (d @ th) * th) < 1e-12
+
+
+def _curved_det_point(c, v, col, row):
+    """Plain vector geometry of the cylindrical detector (XRT_DET_CURVED): radius sdd about the
+    source, column at fan angle u / sdd from the central ray, row at height v (+v = +z)."""
+    ang = c["angles"][v]
+    u = (col - (c["det_cols"] - 1) / 2) * c["det_spacing"][0] + c["det_offset"][0]
+    w = (row - (c["det_rows"] - 1) / 2) * c["det_spacing"][1] + c["det_offset"][1]
+    D, SDD = c["sod"], c["sdd"]
+    g = u / SDD
+    if c["beam"] == "fan2d":
+        S = np.array([-D * math.sin(ang), D * math.cos(ang), 0.0])
+        ew = -S / D
+        eu = np.array([-ew[1], ew[0], 0.0])
+        return S, S + SDD * (math.cos(g) * ew + math.sin(g) * eu)
+    H = c["z0"] + c["pitch"] * ang / (2 * math.pi) if c["beam"] == "helical" else 0.0
+    S = np.array([-D * math.cos(ang), -D * math.sin(ang), H])
+    ew = np.array([math.cos(ang), math.sin(ang), 0.0])
+    eu = np.array([-math.sin(ang), math.cos(ang), 0.0])
+    return S, S + SDD * (math.cos(g) * ew + math.sin(g) * eu) + w * np.array([0, 0, 1.0])
+
+
+@pytest.mark.parametrize("idx", [2, 4, 5])
+def test_curved_rays_pass_through_source_and_cylinder(idx):
+    """Equiangular transforms with alpha = u / sdd and
+    tan(beta) = v / sdd give the line from the source to the cylindrical detector point."""
+    c = workloads.config(idx)
+    c["det_curved"] = True
+    ids = workloads.sample_rays(c, 300, seed=8)
+    p, th = G.rays(c, ids)
+    C, R = c["det_cols"], c["det_rows"]
+    for m, I in enumerate(ids):
+        col, row, v = I % C, (I // C) % R, I // (C * R)
+        S, P = _curved_det_point(c, v, col, row)
+        for X in (S, P):
+            d = X - p[m]
+            perp = d - (d @ th[m]) * th[m]
+            assert np.linalg.norm(perp) < 1e-9 * max(1.0, np.linalg.norm(d))
+    assert np.allclose(np.linalg.norm(th, axis=1), 1.0, atol=1e-15)
