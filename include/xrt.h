@@ -79,7 +79,8 @@ typedef enum {
     XRT_FAN2D = 1,
     XRT_PAR3D = 2,
     XRT_CONE = 3,
-    XRT_HELICAL = 4
+    XRT_HELICAL = 4,
+    XRT_RAYS = 5   /* plan built by xrt_plan_create_rays (not valid in xrt_geometry.beam)         */
 } xrt_beam;
 
 /* Acquisition geometry.  All lengths in the same physical unit (e.g. mm), angles in radians. */
@@ -121,6 +122,24 @@ typedef enum {
  * |tilt| >= pi/2, unknown flags, XRT_DET_CURVED with a parallel beam or a fan half-angle
  * >= pi/2); XRT_ERR_OOM; XRT_ERR_CUDA. */
 xrt_status xrt_plan_create(const xrt_geometry* g, int cuda_device, xrt_plan* out);
+
+/* Explicit ray list (Remark 3.5: any beam reduces to parallel-beam parameters; SURVEY
+ * 8(f) N1).  Each ray is given by the paper's own parameters: dim 2 -> (s, phi, -, -), the line
+ * {t theta + s theta_perp} of P:132-138; dim 3 -> (s1, s2, phi1, phi2), the line
+ * {t theta + s1 theta_1 + s2 theta_2} of P:404-414.  The plan behaves as one view of n_rays detector
+ * columns: sino is [1][1][n_rays] (ray i at index i); forward / adjoint / ray_units / f64 use the RAY
+ * kernel family.  params: HOST [n_rays][4] fp64, copied at create time (unused entries ignored).
+ * Errors: XRT_ERR_INVALID_ARG (dim not 2/3, n_rays < 1, non-finite params, invalid grid, flags). */
+typedef struct {
+    int32_t dim;             /* 2 or 3                                                           */
+    int32_t flags;           /* must be 0                                                        */
+    int64_t n[3];            /* image grid as in xrt_geometry (n[2] = 1 for dim 2)               */
+    double spacing[3];
+    double center[3];
+    int64_t n_rays;          /* >= 1                                                              */
+    const double* params;    /* HOST [n_rays][4]                                                  */
+} xrt_ray_list;
+xrt_status xrt_plan_create_rays(const xrt_ray_list* r, int cuda_device, xrt_plan* out);
 xrt_status xrt_plan_destroy(xrt_plan p);
 
 /* n_rays = n_views*det_rows*det_cols.  n_units (may be NULL) = nnz of the whole projection

@@ -141,6 +141,21 @@ def rays(c: dict, ids) -> tuple[np.ndarray, np.ndarray]:
     the plane z = 0 with theta_z = 0 (the image is one slab thick).
     """
     ids = np.asarray(ids, dtype=np.int64)
+    if c["beam"] == "rays":
+        # explicit paper parameters per ray (Remark 3.5, P:666-668)
+        q = np.asarray(c["ray_params"], dtype=np.float64).reshape(-1, 4)[ids]
+        n = ids.shape[0]
+        p = np.zeros((n, 3))
+        th = np.zeros((n, 3))
+        if int(c["dim"]) == 2:
+            theta, perp = par2d_basis(q[:, 1])
+            p[:, :2] = q[:, 0:1] * perp                      # s theta_perp, P:155
+            th[:, :2] = theta
+        else:
+            theta, th1, th2 = par3d_basis(q[:, 2], q[:, 3])
+            p = q[:, 0:1] * th1 + q[:, 1:2] * th2            # s1 theta_1 + s2 theta_2, P:431
+            th = theta
+        return p, _snap(th)
     C, R = c["det_cols"], c["det_rows"]
     col = ids % C
     row = (ids // C) % R

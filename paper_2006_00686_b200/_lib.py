@@ -16,14 +16,14 @@ LIB_PATH = os.path.join(HERE, "libxrt.so")
 XRT_OK, XRT_ERR_INVALID_ARG, XRT_ERR_UNSUPPORTED, XRT_ERR_CUDA, XRT_ERR_OOM, XRT_ERR_CAPACITY = range(6)
 STATUS_NAMES = {0: "XRT_OK", 1: "XRT_ERR_INVALID_ARG", 2: "XRT_ERR_UNSUPPORTED", 3: "XRT_ERR_CUDA",
                 4: "XRT_ERR_OOM", 5: "XRT_ERR_CAPACITY"}
-BEAMS = {"par2d": 0, "fan2d": 1, "par3d": 2, "cone": 3, "helical": 4}
+BEAMS = {"par2d": 0, "fan2d": 1, "par3d": 2, "cone": 3, "helical": 4, "rays": 5}
 OP_FORWARD, OP_ADJOINT = 0, 1
 DET_CURVED = 1
 ALGO_AUTO, ALGO_RAY, ALGO_COLUMN, ALGO_GATHER = 0, 1, 2, 3
 ALGOS = {"auto": 0, "ray": 1, "column": 2, "gather": 3}
 
 # every symbol include/xrt.h declares (checked by tests/test_abi.py)
-EXPORTS = ("xrt_plan_create", "xrt_plan_destroy", "xrt_plan_query", "xrt_plan_set_algorithm",
+EXPORTS = ("xrt_plan_create", "xrt_plan_create_rays", "xrt_plan_destroy", "xrt_plan_query", "xrt_plan_set_algorithm",
            "xrt_plan_launch_count", "xrt_forward", "xrt_adjoint", "xrt_forward_host",
            "xrt_adjoint_host", "xrt_forward_f64", "xrt_adjoint_f64", "xrt_ray_units", "xrt_last_error", "xrt_version")
 
@@ -37,6 +37,14 @@ class XrtGeometry(ctypes.Structure):
         ("det_spacing", ctypes.c_double * 2), ("det_offset", ctypes.c_double * 2),
         ("sod", ctypes.c_double), ("sdd", ctypes.c_double),
         ("pitch", ctypes.c_double), ("z0", ctypes.c_double), ("tilt", ctypes.c_double),
+    ]
+
+
+class XrtRayList(ctypes.Structure):
+    _fields_ = [
+        ("dim", ctypes.c_int32), ("flags", ctypes.c_int32),
+        ("n", ctypes.c_int64 * 3), ("spacing", ctypes.c_double * 3), ("center", ctypes.c_double * 3),
+        ("n_rays", ctypes.c_int64), ("params", ctypes.POINTER(ctypes.c_double)),
     ]
 
 
@@ -67,6 +75,7 @@ def load(path: str | None = None) -> ctypes.CDLL:
         sig = {
             "xrt_plan_create": (i32, [ctypes.POINTER(XrtGeometry), ctypes.c_int, ctypes.POINTER(vp)]),
             "xrt_plan_destroy": (i32, [vp]),
+            "xrt_plan_create_rays": (i32, [ctypes.POINTER(XrtRayList), ctypes.c_int, ctypes.POINTER(vp)]),
             "xrt_plan_query": (i32, [vp, ip, ip]),
             "xrt_plan_set_algorithm": (i32, [vp, i32, i32]),
             "xrt_plan_launch_count": (i64, [vp]),

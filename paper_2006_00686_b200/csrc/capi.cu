@@ -324,11 +324,14 @@ int32_t xrt_version(void) { return (XRT_VERSION_MAJOR << 16) | XRT_VERSION_MINOR
 
 const char* xrt_last_error(void) { return g_err.c_str(); }
 
-xrt_status xrt_plan_create(const xrt_geometry* g, int cuda_device, xrt_plan* out) {
-    if (!out) return fail(XRT_ERR_INVALID_ARG, "out is NULL");
+}  // extern "C"
+
+namespace {
+// rays != nullptr: an explicit ray list (xrt_plan_create_rays) laid out as one view of n_rays
+// detector columns; only the RAY kernel family serves it.
+xrt_status plan_create_impl(const xrt_geometry* g, int cuda_device, xrt_plan* out, const double* rays,
+                            int ray_dim) {
     *out = nullptr;
-    xrt_status st = validate(g);
-    if (st != XRT_OK) return st;
     int ndev = 0;
     if (cudaGetDeviceCount(&ndev) != cudaSuccess || cuda_device < 0 || cuda_device >= ndev)
         return fail(XRT_ERR_INVALID_ARG, "cuda_device %d not available (%d devices)", cuda_device, ndev);
@@ -378,7 +381,21 @@ xrt_status xrt_plan_create(const xrt_geometry* g, int cuda_device, xrt_plan* out
         xrt_plan_destroy(p);
         return cuda_fail(e, "plan tables");
     }
-    p->column_ok = (g->beam == XRT_PAR3D || g->beam == XRT_CONE || g->beam == XRT_HELICAL) &&
+    if (rays) {
+        // explicit rays (Remark 3.5): per-ray paper parameters in a device table
+        p->beam = XRT_RAYS;
+        D.beam = XRT_RAYS;
+        D.ray_dim = ray_dim;
+        e = cudaMalloc(&p->d_rays, sizeof(double) * 4 * (size_t)p->n_rays);
+        if (e == cudaSuccess)
+            e = cudaMemcpy(p->d_rays, rays, sizeof(double) * 4 * (size_t)p->n_rays, cudaMemcpyHostToDevice);
+        if (e != cudaSuccess) {
+            xrt_plan_destroy(p);
+            return cuda_fail(e, "ray table");
+        }
+        D.rays = p->d_rays;
+    }
+    p->column_ok = !rays && (g->beam == XRT_PAR3D || g->beam == XRT_CONE || g->beam == XRT_HELICAL) &&
                    column_single_crossing(g, G);
     if (p->column_ok) {
         p->zpad = column_zpad(g, G);
@@ -426,6 +443,47 @@ xrt_status xrt_plan_create(const xrt_geometry* g, int cuda_device, xrt_plan* out
     *out = p;
     return XRT_OK;
 }
+}  // namespace
+
+extern "C" {
+
+xrt_status xrt_plan_create(const xrt_geometry* g, int cuda_device, xrt_plan* out) {
+    if (!out) return fail(XRT_ERR_INVALID_ARG, "out is NULL");
+    *out = nullptr;
+    xrt_status st = validate(g);
+    if (st != XRT_OK) return st;
+    return plan_create_impl(g, cuda_device, out, nullptr, 0);
+}
+
+xrt_status xrt_plan_create_rays(const xrt_ray_list* r, int cuda_device, xrt_plan* out) {
+    if (!out) return fail(XRT_ERR_INVALID_ARG, "out is NULL");
+    *out = nullptr;
+    if (!r) return fail(XRT_ERR_INVALID_ARG, "ray list is NULL");
+    if (r->flags != 0) return fail(XRT_ERR_INVALID_ARG, "flags must be 0");
+    if (r->dim != 2 && r->dim != 3) return fail(XRT_ERR_INVALID_ARG, "dim must be 2 or 3");
+    if (r->n_rays < 1 || r->n_rays > INT_MAX) return fail(XRT_ERR_INVALID_ARG, "n_rays must be in [1, 2^31)");
+    if (!r->params) return fail(XRT_ERR_INVALID_ARG, "params is NULL");
+    for (int64_t i = 0; i < 4 * r->n_rays; ++i)
+        if (!std::isfinite(r->params[i])) return fail(XRT_ERR_INVALID_ARG, "params[%lld] not finite", (long long)i);
+    // the grid is validated through an xrt_geometry of the matching parallel beam
+    static const double zero_angle = 0.0;
+    xrt_geometry g;
+    std::memset(&g, 0, sizeof g);
+    g.beam = r->dim == 2 ? XRT_PAR2D : XRT_PAR3D;
+    for (int a = 0; a < 3; ++a) {
+        g.n[a] = r->n[a];
+        g.spacing[a] = r->spacing[a];
+        g.center[a] = r->center[a];
+    }
+    g.n_views = 1;
+    g.angles = &zero_angle;
+    g.det_cols = r->n_rays;
+    g.det_rows = 1;
+    g.det_spacing[0] = g.det_spacing[1] = 1.0;
+    xrt_status st = validate(&g);
+    if (st != XRT_OK) return st;
+    return plan_create_impl(&g, cuda_device, out, r->params, r->dim);
+}
 
 xrt_status xrt_plan_destroy(xrt_plan p) {
     if (!p) return XRT_OK;
@@ -436,6 +494,7 @@ xrt_status xrt_plan_destroy(xrt_plan p) {
     cudaFree(p->d_items);
     cudaFree(p->d_coldesc);
     cudaFree(p->d_gather_y);
+    cudaFree(p->d_rays);
     cudaFree(p->d_stage_img);
     cudaFree(p->d_stage_sino);
     if (p->aux_stream) cudaStreamDestroy((cudaStream_t)p->aux_stream);

@@ -46,6 +46,8 @@ struct GridC {
 struct DetC {
     int beam;                              // xrt_beam
     int curved;                            // 1: cylindrical detector (equiangular columns, XRT_DET_CURVED)
+    int ray_dim;                           // XRT_RAYS: 2 or 3
+    const double* rays;                    // XRT_RAYS: device [n_rays][4] paper parameters
     double D, sdd;                         // source-to-origin / -detector distances
     double inv_D;                          // 1 / D
     int cols, rows;
@@ -74,6 +76,24 @@ __device__ __forceinline__ void paper_ray(const ViewRec& V, const DetC& dc, int 
     const double v = ((double)r - dc.cv) * dc.dv + dc.off_v;
     const double D = dc.D;
     switch (dc.beam) {
+        case XRT_RAYS: {   // explicit ray c of the list (Remark 3.5)
+            const double* q = dc.rays + 4 * (int64_t)c;
+            if (dc.ray_dim == 2) {   // (s, phi): theta = (cos phi, sin phi), point s theta_perp
+                double sp, cp;
+                sincos(q[1], &sp, &cp);
+                th[0] = cp; th[1] = sp; th[2] = 0.0;
+                p[0] = -q[0] * sp; p[1] = q[0] * cp; p[2] = 0.0;
+            } else {                 // (s1, s2, phi1, phi2): theta, theta_1, theta_2 of P:404-412
+                double a1, b1, a2, b2;   // sin/cos phi1, sin/cos phi2
+                sincos(q[2], &a1, &b1);
+                sincos(q[3], &a2, &b2);
+                th[0] = b2 * b1; th[1] = b2 * a1; th[2] = a2;
+                p[0] = q[0] * (-a1) + q[1] * (-a2 * b1);
+                p[1] = q[0] * b1 + q[1] * (-a2 * a1);
+                p[2] = q[1] * b2;
+            }
+            break;
+        }
         case XRT_PAR2D: {  // (s, phi) = (u, angle_v)
             th[0] = V.c1; th[1] = V.s1; th[2] = 0.0;
             p[0] = -u * V.s1; p[1] = u * V.c1; p[2] = 0.0;
@@ -208,6 +228,7 @@ struct xrt_plan_s {
     int col_np = 2;                    // ray pairs per lane of the column kernels (rows per band = 64 col_np)
     void* d_items = nullptr;           // device uint2 work list (tiled) or nullptr
     void* d_coldesc = nullptr;         // per-(view, column) path descriptors (COLUMN, GATHER)
+    double* d_rays = nullptr;          // explicit ray list (XRT_RAYS)
     float* d_gather_y = nullptr;       // GATHER workspace: rescaled, transposed sinogram of one view block
     int64_t gather_views = 0;          // views per GATHER launch
     int64_t n_items = 0;

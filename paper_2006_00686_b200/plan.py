@@ -39,6 +39,22 @@ def _geometry_struct(g: dict) -> tuple[_lib.XrtGeometry, np.ndarray]:
     return s, angles
 
 
+def _ray_list_struct(g: dict):
+    """xrt_ray_list of a {"beam": "rays", "dim": 2|3, "n", "spacing", "center", "ray_params"} dict;
+    ray_params [n_rays][4]: (s, phi, 0, 0) in 2D, (s1, s2, phi1, phi2) in 3D."""
+    params = np.ascontiguousarray(np.asarray(g["ray_params"], dtype=np.float64).reshape(-1, 4))
+    r = _lib.XrtRayList()
+    r.dim = int(g["dim"])
+    r.flags = 0
+    for a in range(3):
+        r.n[a] = int(g["n"][a])
+        r.spacing[a] = float(g["spacing"][a])
+        r.center[a] = float(g.get("center", (0.0, 0.0, 0.0))[a])
+    r.n_rays = int(params.shape[0])
+    r.params = params.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
+    return r, params
+
+
 def _stream_handle(stream) -> int:
     if stream is None:
         stream = torch.cuda.current_stream()
@@ -54,9 +70,17 @@ class Plan:
             device = torch.cuda.current_device()
         self.device = int(device)
         self.geometry = dict(geometry)
-        s, self._angles = _geometry_struct(geometry)
         h = ctypes.c_void_p()
-        check(lib.xrt_plan_create(ctypes.byref(s), self.device, ctypes.byref(h)))
+        if geometry.get("beam") == "rays":
+            # explicit ray list: xrt_plan_create_rays (Remark 3.5)
+            r, self._angles = _ray_list_struct(geometry)
+            check(lib.xrt_plan_create_rays(ctypes.byref(r), self.device, ctypes.byref(h)))
+            s, _ = _geometry_struct(dict(geometry, beam="par2d" if r.dim == 2 else "par3d",
+                                         angles=np.zeros(1), det_cols=r.n_rays, det_rows=1,
+                                         det_spacing=(1.0, 1.0)))
+        else:
+            s, self._angles = _geometry_struct(geometry)
+            check(lib.xrt_plan_create(ctypes.byref(s), self.device, ctypes.byref(h)))
         self._h = h
         self._lib = lib
         n = ctypes.c_int64()

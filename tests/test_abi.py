@@ -82,3 +82,23 @@ def test_null_arguments(lib):
     assert lib.xrt_forward(None, None, None, None) == _lib.XRT_ERR_INVALID_ARG
     assert lib.xrt_plan_destroy(None) == _lib.XRT_OK
     assert lib.xrt_plan_launch_count(None) == -1
+
+
+@pytest.mark.parametrize("bad", [dict(dim=4), dict(n_rays=0), dict(nan=True), dict(flags=1), dict(n=(0, 4, 4))])
+def test_ray_list_rejected(lib, bad):
+    """xrt_plan_create_rays validates before touching a device."""
+    r = _lib.XrtRayList()
+    r.dim = bad.get("dim", 3)
+    r.flags = bad.get("flags", 0)
+    for a in range(3):
+        r.n[a] = bad.get("n", (4, 4, 4))[a]
+        r.spacing[a] = 1.0
+        r.center[a] = 0.0
+    params = np.zeros((2, 4))
+    if bad.get("nan"):
+        params[1, 2] = math.nan
+    r.n_rays = bad.get("n_rays", 2)
+    r.params = params.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
+    h = ctypes.c_void_p()
+    assert lib.xrt_plan_create_rays(ctypes.byref(r), 0, ctypes.byref(h)) == _lib.XRT_ERR_INVALID_ARG
+    assert h.value is None
