@@ -79,3 +79,53 @@ def gather_sinogram(slab: torch.Tensor, n_views_total: int, rank: int, world: in
     if world > 1:
         dist.all_reduce(full, op=dist.ReduceOp.SUM, group=group)
     return full
+
+
+# --------------------------------------------------------------------- z-slab sharding (par3d)
+def zslab_partition(geometry: dict, world: int) -> list[tuple[int, int, int, int]]:
+    """Zero-communication partition of a 3D parallel beam WITHOUT tilt (every ray horizontal:
+    z = v_r, fixed z cell k(r) = floor((z_hi - v_r) / d_z), DESIGN reading 5): rank r owns the
+    image slab k in [k0, k1) and exactly the detector rows whose rays lie in it, [r0, r1).
+    Rows outside the image in z (no unit) go to the nearest slab.  Returns [(k0, k1, r0, r1)].
+    (the forward and adjoint of a slab need no exchange at all.)"""
+    if geometry["beam"] != "par3d" or abs(float(geometry.get("tilt", 0.0))) != 0.0:
+        raise ValueError("z-slab sharding needs a 3D parallel beam with tilt 0")
+    nz = int(geometry["n"][2])
+    dz = float(geometry["spacing"][2])
+    z_hi = float(geometry.get("center", (0, 0, 0))[2]) + nz * dz / 2.0
+    R = int(geometry["det_rows"])
+    dv = float(geometry["det_spacing"][1])
+    off = float(geometry.get("det_offset", (0.0, 0.0))[1])
+    v = (np.arange(R) - (R - 1) / 2.0) * dv + off
+    kr = np.clip(np.floor((z_hi - v * np.cos(0.0)) / dz), 0, nz - 1).astype(np.int64)   # as ray_z
+    if world < 1 or world > nz:
+        raise ValueError(f"world {world} must be in [1, N_z={nz}]")
+    out = []
+    for r in range(world):
+        k0, k1 = nz * r // world, nz * (r + 1) // world
+        rows = np.nonzero((kr >= k0) & (kr < k1))[0]
+        r0, r1 = (int(rows.min()), int(rows.max()) + 1) if rows.size else (0, 0)
+        out.append((k0, k1, r0, r1))
+    return out
+
+
+def zslab_geometry(geometry: dict, k0: int, k1: int, r0: int, r1: int) -> dict:
+    """Sub-geometry of one slab: image rows k0..k1 (same x, y; centre moved in z) and detector rows
+    r0..r1 (same physical row positions: the detector offset absorbs the shift).  The slab box
+    z_hi - k0 d_z is exact when d_z and z_hi are dyadic (cfg 3: 1.0, 128); otherwise a row lying
+    exactly on a z plane may round into the neighbouring cell (DESIGN reading 2 ties)."""
+    g = dict(geometry)
+    nx, ny, nz = geometry["n"]
+    dz = float(geometry["spacing"][2])
+    cx, cy, cz = geometry.get("center", (0.0, 0.0, 0.0))
+    z_hi = cz + nz * dz / 2.0
+    g["n"] = (nx, ny, k1 - k0)
+    g["center"] = (cx, cy, z_hi - (k0 + k1) * dz / 2.0)        # slab [z_hi - k1 dz, z_hi - k0 dz]
+    R = int(geometry["det_rows"])
+    dv = float(geometry["det_spacing"][1])
+    off_u, off_v = geometry.get("det_offset", (0.0, 0.0))
+    Rn = r1 - r0
+    g["det_rows"] = Rn
+    g["det_offset"] = (off_u, off_v + (r0 - (R - 1) / 2.0 + (Rn - 1) / 2.0) * dv)
+    g["zslab"] = (k0, k1, r0, r1)
+    return g

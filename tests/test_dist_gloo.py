@@ -114,3 +114,29 @@ def test_sharded_equals_unsharded_gloo(cfg_idx):
     assert status == "ok", fwd_err
     assert fwd_err == 0.0              # rays are independent: sharded forward is bitwise equal
     assert adj_err < 1e-6              # adjoint: fp32 reassociation of the all_reduce only
+
+
+def test_zslab_partition_par3d():
+    """Every detector row belongs to exactly one slab, rows are contiguous per slab, and the
+    sub-geometry reproduces the rows' physical positions and the slab's z range."""
+    import math
+    import workloads
+    from paper_2006_00686_b200.dist import zslab_geometry, zslab_partition
+    from oracle import geometry as G
+    c = workloads.scaled(3, n=(24, 24, 30), n_views=4, det_cols=33, det_rows=41)
+    for world in (1, 2, 3, 4):
+        parts = zslab_partition(c, world)
+        assert parts[0][0] == 0 and parts[-1][1] == 30
+        covered = []
+        for (k0, k1, r0, r1) in parts:
+            covered += list(range(r0, r1))
+            g = zslab_geometry(c, k0, k1, r0, r1)
+            # same physical row positions
+            assert np.allclose(G.det_v(g, np.arange(r1 - r0)), G.det_v(c, np.arange(r0, r1)), atol=1e-12)
+            # slab box
+            _, _, zt = G.grid_bounds(g)
+            _, _, zt0 = G.grid_bounds(c)
+            assert math.isclose(zt, zt0 - k0 * c["spacing"][2], abs_tol=1e-12)
+        assert sorted(covered) == list(range(41))
+    with pytest.raises(ValueError):
+        zslab_partition(workloads.config(4), 2)
