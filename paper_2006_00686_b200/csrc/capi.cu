@@ -267,8 +267,12 @@ xrt_status adjoint_range(xrt_plan p, const float* sino, float* img, int64_t v0, 
         e = xrt::launch_adjoint_column(p, sino, p->d_work_adj, v0, v1, s);
     } else if (algo == XRT_ALGO_GATHER) {
         if (!(v0 == 0 && v1 == p->n_views)) return fail(XRT_ERR_UNSUPPORTED, "gather adjoint runs all views at once");
-        e = xrt::launch_adjoint_gather(p, sino, p->d_work_adj, s);
-        p->launches += xrt::gather_launches(p) - 1;
+        if (p->dim == 2) {
+            e = xrt::launch_adjoint_gather2d(p, sino, img, s);
+        } else {
+            e = xrt::launch_adjoint_gather(p, sino, p->d_work_adj, s);
+            p->launches += xrt::gather_launches(p) - 1;
+        }
     } else {
         return fail(XRT_ERR_UNSUPPORTED, "adjoint algorithm %d not built", algo);
     }
@@ -279,7 +283,7 @@ xrt_status adjoint_range(xrt_plan p, const float* sino, float* img, int64_t v0, 
 
 xrt_status adj_finish(xrt_plan p, float* img, cudaStream_t s) {
     const int algo = resolve(p->algo_adj, p->column_ok);
-    if (algo != XRT_ALGO_COLUMN && algo != XRT_ALGO_GATHER) return XRT_OK;
+    if (algo != XRT_ALGO_COLUMN && !(algo == XRT_ALGO_GATHER && p->dim == 3)) return XRT_OK;
     cudaError_t e = xrt::launch_from_zfast(p, p->d_work_adj, img, s);
     p->launches += 1;
     if (e != cudaSuccess) return cuda_fail(e, "transpose launch");
@@ -395,6 +399,16 @@ xrt_status plan_create_impl(const xrt_geometry* g, int cuda_device, xrt_plan* ou
         }
         D.rays = p->d_rays;
     }
+    if (!rays && (g->beam == XRT_PAR2D || g->beam == XRT_FAN2D)) {
+        // 2D gather: per-(view, column) rays in index space
+        e = cudaMalloc(&p->d_raydesc2d, xrt::raydesc2d_bytes() * (size_t)(p->n_views * D.cols));
+        if (e == cudaSuccess) e = xrt::launch_raydesc2d(p, (cudaStream_t)0);
+        if (e == cudaSuccess) e = cudaDeviceSynchronize();
+        if (e != cudaSuccess) {
+            xrt_plan_destroy(p);
+            return cuda_fail(e, "2D ray descriptors");
+        }
+    }
     p->column_ok = !rays && (g->beam == XRT_PAR3D || g->beam == XRT_CONE || g->beam == XRT_HELICAL) &&
                    column_single_crossing(g, G);
     if (p->column_ok) {
@@ -495,6 +509,7 @@ xrt_status xrt_plan_destroy(xrt_plan p) {
     cudaFree(p->d_coldesc);
     cudaFree(p->d_gather_y);
     cudaFree(p->d_rays);
+    cudaFree(p->d_raydesc2d);
     cudaFree(p->d_stage_img);
     cudaFree(p->d_stage_sino);
     if (p->aux_stream) cudaStreamDestroy((cudaStream_t)p->aux_stream);
@@ -522,7 +537,7 @@ xrt_status xrt_plan_set_algorithm(xrt_plan p, int32_t op, int32_t algo) {
     if (algo < XRT_ALGO_AUTO || algo > XRT_ALGO_GATHER) return fail(XRT_ERR_INVALID_ARG, "bad algo %d", algo);
     if (algo == XRT_ALGO_GATHER && op != XRT_OP_ADJOINT)
         return fail(XRT_ERR_UNSUPPORTED, "the gather algorithm is an adjoint");
-    if (algo == XRT_ALGO_GATHER && (!p->column_ok || p->det.rows > 12288))
+    if (algo == XRT_ALGO_GATHER && !(p->d_raydesc2d || (p->column_ok && p->det.rows <= 12288)))
         return fail(XRT_ERR_UNSUPPORTED, "gather algorithm does not serve this geometry");
     if (algo == XRT_ALGO_COLUMN && !p->column_ok)
         return fail(XRT_ERR_UNSUPPORTED, "column algorithm does not serve this geometry");
