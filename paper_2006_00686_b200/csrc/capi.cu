@@ -213,15 +213,27 @@ xrt_status alloc_stage(xrt_plan p) {
     return XRT_OK;
 }
 
-int resolve(int want, bool column_ok) {
-    if (want == XRT_ALGO_AUTO) return column_ok ? XRT_ALGO_COLUMN : XRT_ALGO_RAY;
-    return want;
+// AUTO, by measurement: 3D beams whose rays share an xy line per detector
+// column -> COLUMN for both operators; 2D beams -> RAY forward (0.45 vs 0.51 ms, cfg 2) and the
+// lockstep slice adjoint (0.50 vs 1.35 ms); anything else (ray lists, steep rays) -> RAY.
+int resolve(const xrt_plan_s* p, int op) {
+    const int want = op == XRT_OP_FORWARD ? p->algo_fwd : p->algo_adj;
+    if (want != XRT_ALGO_AUTO) return want;
+    if (p->column_ok) return XRT_ALGO_COLUMN;
+    if (p->d_img_t && op == XRT_OP_ADJOINT) return XRT_ALGO_COLUMN;
+    return XRT_ALGO_RAY;
 }
 
 // Forward over views [v0, v1).  COLUMN reads the plan's z-fastest copy of the image, which
 // fwd_prepare() builds once per call (img -> work_fwd transpose).
 xrt_status fwd_prepare(xrt_plan p, const float* img, cudaStream_t s) {
-    if (resolve(p->algo_fwd, p->column_ok) != XRT_ALGO_COLUMN) return XRT_OK;
+    if (resolve(p, XRT_OP_FORWARD) != XRT_ALGO_COLUMN) return XRT_OK;
+    if (p->dim == 2) {   // slice kernels: x-major warps read the transposed image
+        cudaError_t e = xrt::launch_transpose2d(img, p->d_img_t, p->grid.n[1], p->grid.n[0], false, s);
+        p->launches += 1;
+        if (e != cudaSuccess) return cuda_fail(e, "transpose launch");
+        return XRT_OK;
+    }
     cudaError_t e = xrt::launch_to_zfast(p, img, p->d_work_fwd, s);
     p->launches += 1;
     if (e != cudaSuccess) return cuda_fail(e, "transpose launch");
@@ -231,10 +243,13 @@ xrt_status fwd_prepare(xrt_plan p, const float* img, cudaStream_t s) {
 xrt_status forward_range(xrt_plan p, const float* img, float* sino, int64_t v0, int64_t v1,
                          cudaStream_t s) {
     const int64_t pv = p->det.per_view;
-    const int algo = resolve(p->algo_fwd, p->column_ok);
+    const int algo = resolve(p, XRT_OP_FORWARD);
     cudaError_t e = cudaSuccess;
     if (algo == XRT_ALGO_RAY) {
         e = xrt::launch_forward_ray(p, img, sino, v0 * pv, v1 * pv, s);
+    } else if (algo == XRT_ALGO_COLUMN && p->dim == 2) {
+        if (!(v0 == 0 && v1 == p->n_views)) return fail(XRT_ERR_UNSUPPORTED, "2D slice kernels run all views at once");
+        e = xrt::launch_slice2d(p, false, img, p->d_img_t, nullptr, sino, nullptr, nullptr, s);
     } else if (algo == XRT_ALGO_COLUMN) {
         e = xrt::launch_forward_column(p, p->d_work_fwd, sino, v0, v1, s);
     } else {
@@ -248,9 +263,11 @@ xrt_status forward_range(xrt_plan p, const float* img, float* sino, int64_t v0, 
 // Adjoint: adj_begin() clears the accumulator, adjoint_range() adds views [v0, v1),
 // adj_finish() writes the caller's image (COLUMN: work_adj -> img transpose).
 xrt_status adj_begin(xrt_plan p, float* img, cudaStream_t s) {
-    const int algo = resolve(p->algo_adj, p->column_ok);
+    const int algo = resolve(p, XRT_OP_ADJOINT);
     if (algo == XRT_ALGO_GATHER) return XRT_OK;   // the gather writes every interior voxel
-    const bool col = algo == XRT_ALGO_COLUMN;
+    const bool col = algo == XRT_ALGO_COLUMN && p->dim == 3;
+    if (algo == XRT_ALGO_COLUMN && p->dim == 2)
+        XRT_CUDA(cudaMemsetAsync(p->d_img_t, 0, sizeof(float) * (size_t)p->grid.nxy, s));
     if (col) XRT_CUDA(cudaMemsetAsync(p->d_work_adj, 0, sizeof(float) * (size_t)(p->grid.nxy * p->nzp), s));
     else XRT_CUDA(cudaMemsetAsync(img, 0, sizeof(float) * (size_t)p->grid.nxyz, s));
     return XRT_OK;
@@ -259,10 +276,13 @@ xrt_status adj_begin(xrt_plan p, float* img, cudaStream_t s) {
 xrt_status adjoint_range(xrt_plan p, const float* sino, float* img, int64_t v0, int64_t v1,
                          cudaStream_t s) {
     const int64_t pv = p->det.per_view;
-    const int algo = resolve(p->algo_adj, p->column_ok);
+    const int algo = resolve(p, XRT_OP_ADJOINT);
     cudaError_t e = cudaSuccess;
     if (algo == XRT_ALGO_RAY) {
         e = xrt::launch_adjoint_ray(p, sino, img, v0 * pv, v1 * pv, s);
+    } else if (algo == XRT_ALGO_COLUMN && p->dim == 2) {
+        if (!(v0 == 0 && v1 == p->n_views)) return fail(XRT_ERR_UNSUPPORTED, "2D slice kernels run all views at once");
+        e = xrt::launch_slice2d(p, true, nullptr, nullptr, sino, nullptr, img, p->d_img_t, s);
     } else if (algo == XRT_ALGO_COLUMN) {
         e = xrt::launch_adjoint_column(p, sino, p->d_work_adj, v0, v1, s);
     } else if (algo == XRT_ALGO_GATHER) {
@@ -282,7 +302,13 @@ xrt_status adjoint_range(xrt_plan p, const float* sino, float* img, int64_t v0, 
 }
 
 xrt_status adj_finish(xrt_plan p, float* img, cudaStream_t s) {
-    const int algo = resolve(p->algo_adj, p->column_ok);
+    const int algo = resolve(p, XRT_OP_ADJOINT);
+    if (algo == XRT_ALGO_COLUMN && p->dim == 2) {   // img += transpose(x-major accumulator)
+        cudaError_t e = xrt::launch_transpose2d(p->d_img_t, img, p->grid.n[0], p->grid.n[1], true, s);
+        p->launches += 1;
+        if (e != cudaSuccess) return cuda_fail(e, "transpose launch");
+        return XRT_OK;
+    }
     if (algo != XRT_ALGO_COLUMN && !(algo == XRT_ALGO_GATHER && p->dim == 3)) return XRT_OK;
     cudaError_t e = xrt::launch_from_zfast(p, p->d_work_adj, img, s);
     p->launches += 1;
@@ -402,6 +428,7 @@ xrt_status plan_create_impl(const xrt_geometry* g, int cuda_device, xrt_plan* ou
     if (!rays && (g->beam == XRT_PAR2D || g->beam == XRT_FAN2D)) {
         // 2D gather: per-(view, column) rays in index space
         e = cudaMalloc(&p->d_raydesc2d, xrt::raydesc2d_bytes() * (size_t)(p->n_views * D.cols));
+        if (e == cudaSuccess) e = cudaMalloc(&p->d_img_t, sizeof(float) * (size_t)G.nxy);
         if (e == cudaSuccess) e = xrt::launch_raydesc2d(p, (cudaStream_t)0);
         if (e == cudaSuccess) e = cudaDeviceSynchronize();
         if (e != cudaSuccess) {
@@ -510,6 +537,7 @@ xrt_status xrt_plan_destroy(xrt_plan p) {
     cudaFree(p->d_gather_y);
     cudaFree(p->d_rays);
     cudaFree(p->d_raydesc2d);
+    cudaFree(p->d_img_t);
     cudaFree(p->d_stage_img);
     cudaFree(p->d_stage_sino);
     if (p->aux_stream) cudaStreamDestroy((cudaStream_t)p->aux_stream);
@@ -539,7 +567,7 @@ xrt_status xrt_plan_set_algorithm(xrt_plan p, int32_t op, int32_t algo) {
         return fail(XRT_ERR_UNSUPPORTED, "the gather algorithm is an adjoint");
     if (algo == XRT_ALGO_GATHER && !(p->d_raydesc2d || (p->column_ok && p->det.rows <= 12288)))
         return fail(XRT_ERR_UNSUPPORTED, "gather algorithm does not serve this geometry");
-    if (algo == XRT_ALGO_COLUMN && !p->column_ok)
+    if (algo == XRT_ALGO_COLUMN && !p->column_ok && !p->d_img_t)
         return fail(XRT_ERR_UNSUPPORTED, "column algorithm does not serve this geometry");
     if (op == XRT_OP_FORWARD) p->algo_fwd = algo; else p->algo_adj = algo;
     return XRT_OK;
@@ -598,7 +626,7 @@ xrt_status xrt_forward_host(xrt_plan p, const float* img_host, float* sino_host,
                              cudaMemcpyHostToDevice, s));
     st = fwd_prepare(p, p->d_stage_img, s);
     if (st != XRT_OK) return st;
-    if (resolve(p->algo_fwd, p->column_ok) == XRT_ALGO_COLUMN) {
+    if (resolve(p, XRT_OP_FORWARD) == XRT_ALGO_COLUMN && p->dim == 3) {
         // COLUMN: one launch per band of detector rows; the band's sinogram rows (every view) go
         // back on the aux stream while the next band computes
         const int nb = xrt::column_bands(p), rb = xrt::column_band_rows(p);
@@ -626,7 +654,7 @@ xrt_status xrt_forward_host(xrt_plan p, const float* img_host, float* sino_host,
         if (e2 != cudaSuccess) return cuda_fail(e2, "forward_host sync");
         return XRT_OK;
     }
-    const bool whole = false;
+    const bool whole = resolve(p, XRT_OP_FORWARD) == XRT_ALGO_COLUMN;   // 2D slice kernels
     const int64_t nchunk = whole ? 1 : std::min<int64_t>(8, p->n_views);
     const int64_t pv = p->det.per_view;
     std::vector<cudaEvent_t> ev((size_t)nchunk);
@@ -661,7 +689,7 @@ xrt_status xrt_adjoint_host(xrt_plan p, const float* sino_host, float* img_host,
     cudaStream_t s = (cudaStream_t)cuda_stream, a = (cudaStream_t)p->aux_stream;
     st = adj_begin(p, p->d_stage_img, s);
     if (st != XRT_OK) return st;
-    if (resolve(p->algo_adj, p->column_ok) == XRT_ALGO_COLUMN) {
+    if (resolve(p, XRT_OP_ADJOINT) == XRT_ALGO_COLUMN && p->dim == 3) {
         // COLUMN: the sinogram rows of band b (every view) are uploaded on the aux stream while
         // band b - 1 computes; one launch per band
         const int nb = xrt::column_bands(p), rb = xrt::column_band_rows(p);
@@ -694,7 +722,8 @@ xrt_status xrt_adjoint_host(xrt_plan p, const float* sino_host, float* img_host,
         if (e2 != cudaSuccess) return cuda_fail(e2, "adjoint_host sync");
         return XRT_OK;
     }
-    const bool whole = resolve(p->algo_adj, p->column_ok) == XRT_ALGO_GATHER;
+    const bool whole = resolve(p, XRT_OP_ADJOINT) == XRT_ALGO_GATHER ||
+                       resolve(p, XRT_OP_ADJOINT) == XRT_ALGO_COLUMN;   // 2D slice kernels
     const int64_t nchunk = whole ? 1 : std::min<int64_t>(8, p->n_views);
     const int64_t pv = p->det.per_view;
     std::vector<cudaEvent_t> ev((size_t)nchunk);

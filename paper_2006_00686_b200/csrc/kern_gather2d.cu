@@ -139,4 +139,183 @@ cudaError_t launch_adjoint_gather2d(const xrt_plan_s* p, const float* sino, floa
     return cudaGetLastError();
 }
 
+// ============================================================================ 2D slice kernels
+// Forward and adjoint of the 2D beams with the 32 rays of a warp (32 adjacent detector columns of
+// one view) walking the image in LOCKSTEP by major-axis slice (the paper's Algorithm 2.1 loop over
+// the slices of one axis, with the valid band of the other index, eq:restriction_j
+// P:197-212, found from the merged crossing values).  At every trip the lanes are in one slice, in
+// adjacent cells of the minor axis, so their loads / reductions fall on consecutive addresses: the
+// image is read (the adjoint accumulated) row-major for y-major warps and through a transposed copy
+// for x-major warps.  Per ray the walk is the RAY kernel's: crossing values T(m) = t1 + m dt (FFMA)
+// relative to the ray's entry, shared by the two units they separate; fixed axes half-open.
+namespace {
+
+struct Ray2S {
+    float Ta, Tb;     // next crossing of the major / minor axis (relative to the entry)
+    float ta1, tb1;   // first crossings
+    float dta, dtb;   // spacings (0 when fixed)
+    float ma, mb;     // crossings taken
+    float tend;       // end of the chord
+    int ca, cb;       // current major / minor cell
+    int sa, sb;       // +-1 steps (0 when fixed)
+};
+
+template <bool kAdj>
+__device__ __forceinline__ void slice_units(Ray2S& S, float& tc, float thi, const float* src, float* dst,
+                                            int64_t row, float y, float& acc) {
+    // units of one major slice: minor cells between tc and thi (a few; a ray steeper than the
+    // warp's major axis crosses more)
+    for (;;) {
+        const float e = fminf(S.Tb, thi);
+        const float l = e - tc;
+        const int64_t addr = row + S.cb;
+        if (kAdj) { if (l > 0.f) atomicAdd(dst + addr, y * l); }
+        else acc = fmaf(__ldg(src + addr), l, acc);
+        tc = e;
+        if (!(S.Tb < thi)) break;
+        S.mb += 1.f; S.Tb = fmaf(S.mb, S.dtb, S.tb1); S.cb += S.sb;
+    }
+}
+
+template <bool kAdj>
+__global__ void __launch_bounds__(256) k_slice2d(const ViewRec* __restrict__ views, DetC dc, GridC g,
+                                                 const float* __restrict__ img, const float* __restrict__ imgT,
+                                                 const float* __restrict__ y_in, float* __restrict__ sino_out,
+                                                 float* __restrict__ acc_img, float* __restrict__ acc_imgT,
+                                                 int n_views, int groups_per_view) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int gid = blockIdx.x * 8 + warp;
+    const int v = gid / groups_per_view, cgp = gid - v * groups_per_view;
+    if (v >= n_views) return;                              // warp-uniform
+    const int c = cgp * 32 + lane;
+    const bool col_ok = c < dc.cols;
+    Ray64 R;
+    bool hit = false;
+    if (col_ok) hit = setup_ray(views[v], dc, g, 0, c, R);
+    const unsigned bh = __ballot_sync(0xffffffffu, hit);
+    if (bh == 0u) {
+        if (!kAdj && col_ok) sino_out[(int64_t)v * dc.cols + c] = 0.f;
+        return;
+    }
+    // warp major axis by majority of the lanes' |w|
+    const unsigned bx = __ballot_sync(0xffffffffu, hit && fabs(R.w[0]) >= fabs(R.w[1]));
+    const int a = 2 * __popc(bx) >= __popc(bh) ? 0 : 1, b = 1 - a;
+    Ray2S S;
+    float y = 0.f;
+    if (hit) {
+        float T1[2], DT[2];
+        int st[2];
+        float tend = (float)(R.t_out - R.t_in);
+#pragma unroll
+        for (int x = 0; x < 2; ++x) {
+            if (!R.moving[x]) { T1[x] = INFINITY; DT[x] = 0.f; st[x] = 0; continue; }
+            const int pos = R.w[x] > 0.0;
+            const int bf = pos ? R.cell[x] + 1 : R.cell[x];
+            const int mface = pos ? (g.n[x] - bf) : bf;
+            T1[x] = (float)(((double)bf - R.u0[x]) * R.inv_w[x] - R.t_in);
+            DT[x] = (float)fabs(R.inv_w[x]);
+            st[x] = pos ? 1 : -1;
+            tend = fminf(tend, fmaf((float)mface, DT[x], T1[x]));   // never step through a face
+        }
+        S.ta1 = T1[a]; S.tb1 = T1[b]; S.dta = DT[a]; S.dtb = DT[b];
+        S.Ta = S.ta1; S.Tb = S.tb1; S.ma = 0.f; S.mb = 0.f;
+        S.ca = R.cell[a]; S.cb = R.cell[b]; S.sa = st[a]; S.sb = st[b];
+        S.tend = tend;
+        if (kAdj) y = y_in[(int64_t)v * dc.cols + c];
+    }
+    const float* src = a == 1 ? img : imgT;          // y-major: img[j][i]; x-major: imgT[i][j]
+    float* dst = a == 1 ? acc_img : acc_imgT;
+    const int64_t ld = a == 1 ? g.n[0] : g.n[1];
+    // common direction of travel along the major axis
+    const int dir = __shfl_sync(0xffffffffu, hit ? S.sa : 0, __ffs(bh) - 1);
+    float acc = 0.f, tc = 0.f;
+    bool live = hit;
+    // a lane travelling against the warp's direction (or with a fixed major axis) walks its ray alone
+    if (hit && (S.sa != dir || dir == 0)) {
+        while (tc < S.tend) {
+            const float thi = fminf(S.Ta, S.tend);
+            slice_units<kAdj>(S, tc, thi, src, dst, (int64_t)S.ca * ld, y, acc);
+            if (!(S.Ta <= S.tend)) break;
+            S.ma += 1.f; S.Ta = fmaf(S.ma, S.dta, S.ta1); S.ca += S.sa;
+        }
+        live = false;
+    }
+    // lockstep range of major cells: the warp's entry cells to its exit cells (+-1)
+    int kmin = INT_MAX, kmax = INT_MIN;
+    if (live) {
+        const int steps = S.tend > S.ta1 ? (int)floorf(__fdividef(S.tend - S.ta1, S.dta)) + 1 : 0;
+        const int ex = max(0, min(g.n[a] - 1, S.ca + S.sa * steps));
+        kmin = min(S.ca, ex); kmax = max(S.ca, ex);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        kmin = min(kmin, __shfl_xor_sync(0xffffffffu, kmin, o));
+        kmax = max(kmax, __shfl_xor_sync(0xffffffffu, kmax, o));
+    }
+    if (kmin <= kmax) {
+        kmin = max(kmin - 1, 0);
+        kmax = min(kmax + 1, g.n[a] - 1);
+        const int ns = kmax - kmin + 1;
+        const int k0 = dir > 0 ? kmin : kmax;
+        for (int k = 0; k < ns; ++k) {
+            const int M = k0 + dir * k;
+            if (live && S.ca == M) {
+                const float thi = fminf(S.Ta, S.tend);
+                slice_units<kAdj>(S, tc, thi, src, dst, (int64_t)M * ld, y, acc);
+                if (S.Ta <= S.tend && tc < S.tend) {
+                    S.ma += 1.f; S.Ta = fmaf(S.ma, S.dta, S.ta1); S.ca += S.sa;
+                } else {
+                    live = false;
+                }
+            }
+        }
+    }
+    if (!kAdj && col_ok) sino_out[(int64_t)v * dc.cols + c] = acc;
+}
+
+}  // namespace
+
+namespace {
+// out[cols][rows] (+)= in[rows][cols]
+template <bool kAdd>
+__global__ void k_transpose2d(const float* __restrict__ in, float* __restrict__ out, int rows, int cols) {
+    __shared__ float tile[32][33];
+    const int bx = blockIdx.x * 32, by = blockIdx.y * 32;
+    for (int j = threadIdx.y; j < 32; j += 8) {
+        const int r = by + j, c = bx + threadIdx.x;
+        if (r < rows && c < cols) tile[j][threadIdx.x] = in[(int64_t)r * cols + c];
+    }
+    __syncthreads();
+    for (int j = threadIdx.y; j < 32; j += 8) {
+        const int r = bx + j, c = by + threadIdx.x;   // out row r (= in column), out column c
+        if (r < cols && c < rows) {
+            float* o = out + (int64_t)r * rows + c;
+            *o = kAdd ? *o + tile[threadIdx.x][j] : tile[threadIdx.x][j];
+        }
+    }
+}
+}  // namespace
+
+cudaError_t launch_transpose2d(const float* in, float* out, int rows, int cols, bool add, cudaStream_t s) {
+    dim3 grid((unsigned)((cols + 31) / 32), (unsigned)((rows + 31) / 32));
+    if (add) k_transpose2d<true><<<grid, dim3(32, 8), 0, s>>>(in, out, rows, cols);
+    else k_transpose2d<false><<<grid, dim3(32, 8), 0, s>>>(in, out, rows, cols);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_slice2d(const xrt_plan_s* p, bool adjoint, const float* img, const float* imgT,
+                           const float* y_in, float* sino_out, float* acc_img, float* acc_imgT,
+                           cudaStream_t s) {
+    const int gpv = (p->det.cols + 31) / 32;
+    const int64_t warps = p->n_views * (int64_t)gpv;
+    const unsigned blocks = (unsigned)((warps + 7) / 8);
+    if (adjoint)
+        k_slice2d<true><<<blocks, 256, 0, s>>>(p->d_views, p->det, p->grid, nullptr, nullptr, y_in, nullptr,
+                                               acc_img, acc_imgT, (int)p->n_views, gpv);
+    else
+        k_slice2d<false><<<blocks, 256, 0, s>>>(p->d_views, p->det, p->grid, img, imgT, nullptr, sino_out,
+                                                nullptr, nullptr, (int)p->n_views, gpv);
+    return cudaGetLastError();
+}
+
 }  // namespace xrt

@@ -230,6 +230,7 @@ struct xrt_plan_s {
     void* d_coldesc = nullptr;         // per-(view, column) path descriptors (COLUMN, GATHER)
     double* d_rays = nullptr;          // explicit ray list (XRT_RAYS)
     void* d_raydesc2d = nullptr;       // per-(view, column) rays in index space (2D GATHER)
+    float* d_img_t = nullptr;          // 2D COLUMN (slice) kernels: transposed image / accumulator
     float* d_gather_y = nullptr;       // GATHER workspace: rescaled, transposed sinogram of one view block
     int64_t gather_views = 0;          // views per GATHER launch
     int64_t n_items = 0;
@@ -278,6 +279,10 @@ int column_band_rows(const xrt_plan_s* p);
 size_t raydesc2d_bytes();
 cudaError_t launch_raydesc2d(const xrt_plan_s* p, cudaStream_t s);
 cudaError_t launch_adjoint_gather2d(const xrt_plan_s* p, const float* sino, float* img, cudaStream_t s);
+cudaError_t launch_transpose2d(const float* in, float* out, int rows, int cols, bool add, cudaStream_t s);
+cudaError_t launch_slice2d(const xrt_plan_s* p, bool adjoint, const float* img, const float* imgT,
+                           const float* y_in, float* sino_out, float* acc_img, float* acc_imgT,
+                           cudaStream_t s);
 int column_bands(const xrt_plan_s* p);
 cudaError_t launch_forward_column_bands(const xrt_plan_s* p, const float* vol_zfast, float* sino, int b0,
                                         int b1, cudaStream_t s);
