@@ -197,11 +197,6 @@ __device__ __forceinline__ void column_path(const ViewRec& V, const DetC& dc, co
     P.n_slices = m + 1;
 }
 
-// Sigma at which slice n starts (slice 0 starts at the square entry, 0).
-__device__ __forceinline__ float slice_start(const ColumnPath& P, int n) {
-    return n == 0 ? 0.f : (n >= P.n_slices ? P.L : fminf(fmaf((float)(n - 1), P.dta, P.t0a), P.L));
-}
-
 // Segments of major slice n: 1 or 2 in-plane units (cell, sigma_start, sigma_end), keeping only
 // those whose cell lies in the tile [ti0, ti1) x [tj0, tj1).  The minor crossings at or before the
 // slice start are counted against the SAME fmaf expression the neighbouring slices use, so every
