@@ -135,9 +135,25 @@ def cpu_baseline(c: dict, budget_s: float = 12.0):
         done += ids.size
         if t_used < budget_s / 8:
             batch *= 2
-    return {"value": done / t_used, "unit": "rays/s", "cores": oracle.threads(), "kind": "oracle",
-            "sample": f"{done} seeded rays of {c['name']} (stratified over views), fp64 brute-force forward "
-                      f"(separable early-out mode), {t_used:.1f} s"}
+    out = {"value": done / t_used, "unit": "rays/s", "cores": oracle.threads(), "kind": "oracle",
+           "sample": f"{done} seeded rays of {c['name']} (stratified over views), fp64 brute-force forward "
+                     f"(separable early-out mode), {t_used:.1f} s"}
+    # context: the paper's own O(N)-per-ray enumeration on the same host cores (cpu_method/, N3)
+    try:
+        import cpu_method
+        n = 200000
+        ids = workloads.sample_rays(c, n, seed=9500)
+        p, th = G.rays(c, ids)
+        cpu_method.forward(c, img, p[:1000], th[:1000])
+        t0 = time.perf_counter()
+        cpu_method.forward(c, img, p, th)
+        dt = time.perf_counter() - t0
+        out["paper_method_cpu"] = {"value": n / dt, "unit": "rays/s", "cores": cpu_method.threads(),
+                                   "sample": f"{n} seeded rays of {c['name']}, fp64 incremental enumeration "
+                                             f"(Algorithm 3.1), {dt:.2f} s"}
+    except Exception as e:  # context only
+        out["paper_method_cpu"] = {"value": None, "error": str(e)}
+    return out
 
 
 def run_reference(args, c, rank, world):
