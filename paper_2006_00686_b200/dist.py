@@ -129,3 +129,41 @@ def zslab_geometry(geometry: dict, k0: int, k1: int, r0: int, r1: int) -> dict:
     g["det_offset"] = (off_u, off_v + (r0 - (R - 1) / 2.0 + (Rn - 1) / 2.0) * dv)
     g["zslab"] = (k0, k1, r0, r1)
     return g
+
+
+class ZSlabShardedPlan:
+    """3D parallel beam without tilt, sharded by z slabs with NO exchange (zslab_partition): rank r
+    owns the image slab x[k0:k1] and the detector rows [r0, r1) of every view; forward maps the slab
+    to those sinogram rows, adjoint maps them back to the slab.  Results stay distributed; gather
+    helpers assemble them (tests / I/O, not the hot path)."""
+
+    def __init__(self, geometry: dict, rank: int | None = None, world: int | None = None,
+                 device: int | None = None, group=None, plan_factory=None):
+        if rank is None:
+            rank = dist.get_rank(group) if dist.is_initialized() else 0
+        if world is None:
+            world = dist.get_world_size(group) if dist.is_initialized() else 1
+        self.rank, self.world, self.group = rank, world, group
+        self.parts = zslab_partition(geometry, world)
+        k0, k1, r0, r1 = self.parts[rank]
+        self.slab, self.rows = (k0, k1), (r0, r1)
+        self.geometry = zslab_geometry(geometry, k0, k1, r0, r1)
+        if plan_factory is None:
+            from .plan import Plan
+            plan_factory = Plan
+        self.plan = plan_factory(self.geometry, device=device)
+
+    def forward(self, img_slab: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
+        """Sinogram rows [views][r0:r1][cols] of A x from this rank's slab x[k0:k1] alone."""
+        return self.plan.forward(img_slab, out=out)
+
+    def adjoint(self, sino_rows: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
+        """Slab [k0:k1] of A^T y from this rank's sinogram rows alone."""
+        return self.plan.adjoint(sino_rows, out=out)
+
+    def gather_image(self, slab: torch.Tensor, nz: int) -> torch.Tensor:
+        full = torch.zeros((nz,) + tuple(slab.shape[1:]), dtype=slab.dtype, device=slab.device)
+        full[self.slab[0]:self.slab[1]] = slab
+        if self.world > 1:
+            dist.all_reduce(full, op=dist.ReduceOp.SUM, group=self.group)
+        return full

@@ -140,3 +140,43 @@ def test_zslab_partition_par3d():
         assert sorted(covered) == list(range(41))
     with pytest.raises(ValueError):
         zslab_partition(workloads.config(4), 2)
+
+
+def _zslab_worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import workloads
+        from paper_2006_00686_b200.dist import ZSlabShardedPlan
+        c = workloads.scaled(3, n=(16, 16, 16), n_views=3, det_cols=19, det_rows=24)
+        sp = ZSlabShardedPlan(c, rank=rank, world=world, plan_factory=OraclePlan)
+        x = workloads.make_image(c)
+        k0, k1 = sp.slab
+        r0, r1 = sp.rows
+        rows = sp.forward(x[k0:k1].contiguous())
+        # the rows of the full forward come from this rank's slab alone
+        full = OraclePlan(c).forward(x)
+        err_f = float((rows - full[:, r0:r1]).abs().max())
+        y = workloads.make_sino_input(c)
+        back = sp.gather_image(sp.adjoint(y[:, r0:r1].contiguous()), 16)
+        ref = OraclePlan(c).adjoint(y)
+        err_b = float((back - ref).norm() / ref.norm())
+        q.put((rank, err_f, err_b))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_zslab_sharded_plan_gloo():
+    """World size 2 (gloo, CPU, oracle-backed plans): no exchange in forward / adjoint; the
+    assembled results equal the unsharded operator."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_zslab_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=240) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+    for rank, ef, eb in res:
+        assert ef <= 1e-5 and eb <= 1e-6, (rank, ef, eb)
