@@ -141,7 +141,7 @@ def cpu_baseline(c: dict, budget_s: float = 12.0):
     # context: the paper's own O(N)-per-ray enumeration on the same host cores (cpu_method/, N3)
     try:
         import cpu_method
-        n = 200000
+        n = 2000000
         ids = workloads.sample_rays(c, n, seed=9500)
         p, th = G.rays(c, ids)
         cpu_method.forward(c, img, p[:1000], th[:1000])
