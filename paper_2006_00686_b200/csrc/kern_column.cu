@@ -529,6 +529,43 @@ __device__ __forceinline__ void column_segments_fwd(unsigned seg, int total, Ray
     }
 }
 
+// Every ray of the warp keeps one z cell (horizontal rays: the 3D parallel beam without tilt,
+// reading 5): each segment is one unit per ray, l = d_sigma, no z state to advance.
+template <int NP>
+__device__ __forceinline__ void column_segments_fwd_flat(unsigned seg, int total, RayPair (&P)[NP]) {
+#pragma unroll 4
+    for (int s = 0; s < total; ++s) {
+        const uint4 raw = lds128(seg + 16u * (unsigned)s);
+        const float qds = __uint_as_float(raw.w);
+        const float2 ds2 = make_float2(qds, qds);
+#pragma unroll
+        for (int p = 0; p < NP; ++p) {
+            const float* a0 = (const float*)(seg_ptr(raw) + 4ull * __float_as_uint(P[p].kpf.x));
+            const float* a1 = (const float*)(seg_ptr(raw) + 4ull * __float_as_uint(P[p].kpf.y));
+            P[p].acc0 = __ffma2_rn(make_float2(__ldg(a0), __ldg(a1)), ds2, P[p].acc0);
+        }
+    }
+}
+
+template <int NP>
+__device__ __forceinline__ void column_segments_adj_flat(unsigned seg, int total, RayPair (&P)[NP]) {
+    const unsigned long long pol = l2_evict_last();
+#pragma unroll 4
+    for (int s = 0; s < total; ++s) {
+        const uint4 raw = lds128(seg + 16u * (unsigned)s);
+        const float qds = __uint_as_float(raw.w);
+        const float2 ds2 = make_float2(qds, qds);
+#pragma unroll
+        for (int p = 0; p < NP; ++p) {
+            float* a0 = (float*)(seg_ptr(raw) + 4ull * __float_as_uint(P[p].kpf.x));
+            float* a1 = (float*)(seg_ptr(raw) + 4ull * __float_as_uint(P[p].kpf.y));
+            const float2 ws = __fmul2_rn(P[p].w, ds2);
+            if (P[p].live0) red_add(a0, ws.x, pol);
+            if (P[p].live1) red_add(a1, ws.y, pol);
+        }
+    }
+}
+
 // Adjoint: the same units, y l scattered with red.global.add (the second unit only when the z
 // crossing lies inside the segment).
 template <int NP, int DK>
@@ -639,8 +676,9 @@ __global__ void __launch_bounds__(kWarps * 32, XRT_COL_MINB) k_column(const View
         neg &= Za.dk <= 0 && Zb.dk <= 0;
     }
     if (!__any_sync(0xffffffffu, any_live)) return;
-    // warp-uniform z stepping direction
-    const int mode = __all_sync(0xffffffffu, pos) ? 1 : (__all_sync(0xffffffffu, neg) ? -1 : 0);
+    // warp-uniform z stepping direction (2: every ray keeps its z cell)
+    const bool all_pos = __all_sync(0xffffffffu, pos), all_neg = __all_sync(0xffffffffu, neg);
+    const int mode = all_pos && all_neg ? 2 : (all_pos ? 1 : (all_neg ? -1 : 0));
     Seg* seg = s_seg[warp];
     const unsigned seg_s = (unsigned)__cvta_generic_to_shared(seg);
     // segment pointers pre-offset by -4 kMagicBits bytes (see RayPair)
@@ -688,7 +726,10 @@ __global__ void __launch_bounds__(kWarps * 32, XRT_COL_MINB) k_column(const View
                     z_skip(P[p].kpf.y, P[p].dk1, P[p].mz.y, P[p].ntz.y, P[p].ndtz.y, P[p].nt0z.y, sf);
                 }
             }
-            if (kAdjoint) {
+            if (mode == 2) {
+                if (kAdjoint) column_segments_adj_flat<NP>(seg_s, total, P);
+                else column_segments_fwd_flat<NP>(seg_s, total, P);
+            } else if (kAdjoint) {
                 if (mode > 0) column_segments_adj<NP, 1>(seg_s, total, P);
                 else if (mode < 0) column_segments_adj<NP, -1>(seg_s, total, P);
                 else column_segments_adj<NP, 0>(seg_s, total, P);
