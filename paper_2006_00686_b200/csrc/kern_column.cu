@@ -548,7 +548,8 @@ __device__ __forceinline__ void column_segments_fwd_flat(unsigned seg, int total
 }
 
 template <int NP>
-__device__ __forceinline__ void column_segments_adj_flat(unsigned seg, int total, RayPair (&P)[NP]) {
+__device__ __forceinline__ void column_segments_adj_flat(unsigned seg, int total, RayPair (&P)[NP], unsigned klo,
+                                                         unsigned kn) {
     const unsigned long long pol = l2_evict_last();
 #pragma unroll 4
     for (int s = 0; s < total; ++s) {
@@ -560,8 +561,8 @@ __device__ __forceinline__ void column_segments_adj_flat(unsigned seg, int total
             float* a0 = (float*)(seg_ptr(raw) + 4ull * __float_as_uint(P[p].kpf.x));
             float* a1 = (float*)(seg_ptr(raw) + 4ull * __float_as_uint(P[p].kpf.y));
             const float2 ws = __fmul2_rn(P[p].w, ds2);
-            if (P[p].live0) red_add(a0, ws.x, pol);
-            if (P[p].live1) red_add(a1, ws.y, pol);
+            if (P[p].live0 && __float_as_uint(P[p].kpf.x) - klo < kn) red_add(a0, ws.x, pol);
+            if (P[p].live1 && __float_as_uint(P[p].kpf.y) - klo < kn) red_add(a1, ws.y, pol);
         }
     }
 }
@@ -569,9 +570,11 @@ __device__ __forceinline__ void column_segments_adj_flat(unsigned seg, int total
 // Adjoint: the same units, y l scattered with red.global.add (the second unit only when the z
 // crossing lies inside the segment).
 template <int NP, int DK>
-__device__ __forceinline__ void column_segments_adj(unsigned seg, int total, RayPair (&P)[NP]) {
+__device__ __forceinline__ void column_segments_adj(unsigned seg, int total, RayPair (&P)[NP], unsigned klo,
+                                                    unsigned kn) {
     const float2 m1 = make_float2(-1.f, -1.f);
     const unsigned long long pol = l2_evict_last();
+    float kpf_in0[NP], kpf_in1[NP];
 #pragma unroll 2
     for (int s = 0; s < total; ++s) {
         const uint4 raw = lds128(seg + 16u * (unsigned)s);
@@ -582,14 +585,20 @@ __device__ __forceinline__ void column_segments_adj(unsigned seg, int total, Ray
             float* a0 = (float*)(seg_ptr(raw) + 4ull * __float_as_uint(P[p].kpf.x));
             float* a1 = (float*)(seg_ptr(raw) + 4ull * __float_as_uint(P[p].kpf.y));
             const int o0 = DK != 0 ? DK : P[p].dk0, o1 = DK != 0 ? DK : P[p].dk1;
+            kpf_in0[p] = P[p].kpf.x;
+            kpf_in1[p] = P[p].kpf.y;
             float2 cr, lm;
             z_step<DK>(P[p], se2, cr, lm);
             const float2 ls = __ffma2_rn(lm, m1, ds2);               // l_s = d_sigma - l_e
             const float2 ws = __fmul2_rn(P[p].w, ls), we = __fmul2_rn(P[p].w, lm);
-            if (P[p].live0) red_add(a0, ws.x, pol);
-            if (P[p].live1) red_add(a1, ws.y, pol);
-            if (P[p].live0 && cr.x != 0.f) red_add(a0 + o0, we.x, pol);
-            if (P[p].live1 && cr.y != 0.f) red_add(a1 + o1, we.y, pol);
+            // only cells inside the image: a ray outside the z range (its start cell in the zero
+            // padding) adds nothing the caller keeps, so it must not cost an L2 reduction.
+            // (bits(kpf) - kMagicBits - pad) < N_z as unsigned <=> pad <= k < pad + N_z
+            const unsigned kb0 = __float_as_uint(kpf_in0[p]) - klo, kb1 = __float_as_uint(kpf_in1[p]) - klo;
+            if (P[p].live0 && kb0 < kn) red_add(a0, ws.x, pol);
+            if (P[p].live1 && kb1 < kn) red_add(a1, ws.y, pol);
+            if (P[p].live0 && cr.x != 0.f && kb0 + o0 < kn) red_add(a0 + o0, we.x, pol);
+            if (P[p].live1 && cr.y != 0.f && kb1 + o1 < kn) red_add(a1 + o1, we.y, pol);
         }
     }
 }
@@ -686,6 +695,7 @@ __global__ void __launch_bounds__(kWarps * 32, XRT_COL_MINB) k_column(const View
                                     4ull * kMagicBits;
     const unsigned long long cstride = 4ull * (unsigned long long)L.nzp;
     bool zinit = !tiled;  // untiled: the z state at sigma = 0 is the initial one
+    const unsigned klo = kMagicBits + (unsigned)L.pad, kn = (unsigned)g.n[2];   // interior z cells
     for (int n0 = na; n0 < nb; n0 += 32 * kPasses) {
         // ---- warp-cooperative: kPasses passes of 32 slices (slice n = n0 + 32 pass + lane) ->
         //      in-tile segments, in path order
@@ -727,12 +737,12 @@ __global__ void __launch_bounds__(kWarps * 32, XRT_COL_MINB) k_column(const View
                 }
             }
             if (mode == 2) {
-                if (kAdjoint) column_segments_adj_flat<NP>(seg_s, total, P);
+                if (kAdjoint) column_segments_adj_flat<NP>(seg_s, total, P, klo, kn);
                 else column_segments_fwd_flat<NP>(seg_s, total, P);
             } else if (kAdjoint) {
-                if (mode > 0) column_segments_adj<NP, 1>(seg_s, total, P);
-                else if (mode < 0) column_segments_adj<NP, -1>(seg_s, total, P);
-                else column_segments_adj<NP, 0>(seg_s, total, P);
+                if (mode > 0) column_segments_adj<NP, 1>(seg_s, total, P, klo, kn);
+                else if (mode < 0) column_segments_adj<NP, -1>(seg_s, total, P, klo, kn);
+                else column_segments_adj<NP, 0>(seg_s, total, P, klo, kn);
             } else {
                 if (mode > 0) column_segments_fwd<NP, 1>(seg_s, total, P);
                 else if (mode < 0) column_segments_fwd<NP, -1>(seg_s, total, P);
