@@ -462,6 +462,13 @@ __device__ __forceinline__ uint4 lds128(unsigned saddr) {
     return raw;
 }
 
+// one 128-bit shared store of a segment record (32-bit shared address: no generic conversion)
+__device__ __forceinline__ void sts_seg(unsigned saddr, unsigned long long ptr, float se, float ds) {
+    asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};"
+                 :: "r"(saddr), "r"((unsigned)ptr), "r"((unsigned)(ptr >> 32)), "r"(__float_as_uint(se)),
+                    "r"(__float_as_uint(ds)) : "memory");
+}
+
 __device__ __forceinline__ unsigned long long seg_ptr(const uint4& raw) {
     return ((unsigned long long)raw.y << 32) | raw.x;
 }
@@ -715,13 +722,11 @@ __global__ void __launch_bounds__(kWarps * 32, XRT_COL_MINB) k_column(const View
             }
             const int b = total + incl - cnt;
             if (cnt > 0) {
-                Seg q; q.ptr = base + cstride * (unsigned)c0; q.se = a0e; q.ds = a0e - a0s;
-                seg[b] = q;
+                sts_seg(seg_s + 16u * (unsigned)b, base + cstride * (unsigned)c0, a0e, a0e - a0s);
                 if (b == 0) s_first[warp] = a0s;
             }
             if (cnt > 1) {
-                Seg q; q.ptr = base + cstride * (unsigned)c1; q.se = a1e; q.ds = a1e - a1s;
-                seg[b + 1] = q;
+                sts_seg(seg_s + 16u * (unsigned)(b + 1), base + cstride * (unsigned)c1, a1e, a1e - a1s);
             }
             total += __shfl_sync(0xffffffffu, incl, 31);
         }
