@@ -441,7 +441,7 @@ xrt_status plan_create_impl(const xrt_geometry* g, int cuda_device, xrt_plan* ou
     if (p->column_ok) {
         p->zpad = column_zpad(g, G);
         p->col_np = xrt::choose_col_np(D.rows);
-        p->nzp = G.n[2] + 2 * p->zpad;
+        p->nzp = (G.n[2] + 2 * p->zpad + 3) / 4 * 4;   // 16-byte cell columns (vector reds); tail rows stay 0
         const size_t bytes = sizeof(float) * (size_t)(G.nxy * p->nzp);
         e = cudaMalloc(&p->d_work_fwd, bytes);
         if (e == cudaSuccess) e = cudaMalloc(&p->d_work_adj, bytes);

@@ -604,8 +604,8 @@ __device__ __forceinline__ void column_segments_adj(unsigned seg, int total, Ray
             const unsigned kb0 = __float_as_uint(kpf_in0[p]) - klo, kb1 = __float_as_uint(kpf_in1[p]) - klo;
             if (P[p].live0 && kb0 < kn) red_add(a0, ws.x, pol);
             if (P[p].live1 && kb1 < kn) red_add(a1, ws.y, pol);
-            if (P[p].live0 && cr.x != 0.f && kb0 + o0 < kn) red_add(a0 + o0, we.x, pol);
-            if (P[p].live1 && cr.y != 0.f && kb1 + o1 < kn) red_add(a1 + o1, we.y, pol);
+            if (P[p].live0 && cr.x != 0.f && kb0 + (unsigned)o0 < kn) red_add(a0 + o0, we.x, pol);
+            if (P[p].live1 && cr.y != 0.f && kb1 + (unsigned)o1 < kn) red_add(a1 + o1, we.y, pol);
         }
     }
 }
