@@ -169,6 +169,23 @@ xrt_status xrt_adjoint(xrt_plan p, const float* sino, float* img, void* cuda_str
 xrt_status xrt_forward_f64(xrt_plan p, const double* img, double* sino, void* cuda_stream);
 xrt_status xrt_adjoint_f64(xrt_plan p, const double* sino, double* img, void* cuda_stream);
 
+/* Attenuated X-ray transform (the generalized transform R_Phi of eq:generalizedRadontransform,
+ * P:36-40, with the SPECT weight Phi(theta, x, t) = exp(-int_t^inf mu(x + s theta) ds); SURVEY 8(f)
+ * N4, reading 23).  f = img and mu are unit-basis images on the plan's grid (eq:f_represent,
+ * P:42-50), so per ray, with the units I in the order of t along theta (from the source towards the
+ * detector; parallel beams: the paper's theta, P:132-138 / P:404-412):
+ *     sino = sum_I f_I exp(-A_I) g(mu_I, l_I),   g(mu, l) = (1 - exp(-mu l)) / mu  (= l at mu = 0),
+ * A_I = sum over the units J after I of mu_J l_J, l the intersection lengths of xrt_forward.
+ * mu = 0 everywhere gives xrt_forward.  The adjoint is img_I = sum_m y_m exp(-A_mI) g(mu_I, l_mI).
+ *   img, mu, sino: device fp32, layouts as xrt_forward (mu read only, same shape as img); the
+ *   output is fully overwritten.  mu in physical 1/length (any finite value; mu >= 0 physically).
+ * One thread per ray (RAY family), every geometry including ray lists; fp32 arithmetic, the
+ * attenuation running product in path order.  Errors: XRT_ERR_INVALID_ARG on NULL pointers. */
+xrt_status xrt_forward_attenuated(xrt_plan p, const float* img, const float* mu, float* sino,
+                                  void* cuda_stream);
+xrt_status xrt_adjoint_attenuated(xrt_plan p, const float* sino, const float* mu, float* img,
+                                  void* cuda_stream);
+
 /* As xrt_forward / xrt_adjoint but with HOST buffers (pageable or pinned): the host->device copy
  * of the input, the kernels and the device->host copy of the output all run inside the call,
  * pipelined over view chunks; returns after the output is in host memory. */

@@ -11,6 +11,8 @@ shares no code with it.
 * ``oracle/geometry.py`` the paper's beam -> parallel-beam transforms, literally
   (P:260-272, P:404-412, P:615-664).
 * ``oracle/core.py``   ctypes wrapper: rows (CSR), forward, adjoint.
+* ``oracle/attenuated.py`` the attenuated transform (SPECT weight of P:36-40),
+  numpy fp64, units ordered along the ray.
 
 Pins (tests/test_oracle_*.py, ``-m "not gpu"``): Tables 1-5 (tests/golden/),
 closed forms, the Section 4.1 ambiguity examples, constructed edge / diagonal
@@ -23,3 +25,4 @@ from .core import (  # noqa: F401
     TAU_FACTOR, OracleGrid, grid_of, rows, forward, adjoint, threads, set_threads, build_oracle,
 )
 from . import geometry  # noqa: F401
+from .attenuated import forward_attenuated, adjoint_attenuated, ray_units_t  # noqa: F401

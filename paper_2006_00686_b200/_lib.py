@@ -25,7 +25,8 @@ ALGOS = {"auto": 0, "ray": 1, "column": 2, "gather": 3}
 # every symbol include/xrt.h declares (checked by tests/test_abi.py)
 EXPORTS = ("xrt_plan_create", "xrt_plan_create_rays", "xrt_plan_destroy", "xrt_plan_query", "xrt_plan_set_algorithm",
            "xrt_plan_launch_count", "xrt_forward", "xrt_adjoint", "xrt_forward_host",
-           "xrt_adjoint_host", "xrt_forward_f64", "xrt_adjoint_f64", "xrt_ray_units", "xrt_last_error", "xrt_version")
+           "xrt_adjoint_host", "xrt_forward_f64", "xrt_adjoint_f64",
+           "xrt_forward_attenuated", "xrt_adjoint_attenuated", "xrt_ray_units", "xrt_last_error", "xrt_version")
 
 
 class XrtGeometry(ctypes.Structure):
@@ -84,6 +85,8 @@ def load(path: str | None = None) -> ctypes.CDLL:
             "xrt_forward_host": (i32, [vp, vp, vp, vp]),
             "xrt_forward_f64": (i32, [vp, vp, vp, vp]),
             "xrt_adjoint_f64": (i32, [vp, vp, vp, vp]),
+            "xrt_forward_attenuated": (i32, [vp, vp, vp, vp, vp]),
+            "xrt_adjoint_attenuated": (i32, [vp, vp, vp, vp, vp]),
             "xrt_adjoint_host": (i32, [vp, vp, vp, vp]),
             "xrt_ray_units": (i32, [vp, i64, i64, vp, vp, vp, i64, ip, vp]),
             "xrt_last_error": (ctypes.c_char_p, []),

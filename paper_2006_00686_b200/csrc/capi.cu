@@ -614,6 +614,27 @@ xrt_status xrt_adjoint_f64(xrt_plan p, const double* sino, double* img, void* cu
     return XRT_OK;
 }
 
+// Attenuated transform: RAY family, every geometry.
+xrt_status xrt_forward_attenuated(xrt_plan p, const float* img, const float* mu, float* sino, void* cuda_stream) {
+    if (!p || !img || !mu || !sino) return fail(XRT_ERR_INVALID_ARG, "NULL argument");
+    DevGuard guard(p->device);
+    cudaError_t e = xrt::launch_forward_att(p, img, mu, sino, 0, p->n_rays, (cudaStream_t)cuda_stream);
+    p->launches += 1;
+    if (e != cudaSuccess) return cuda_fail(e, "forward_attenuated launch");
+    return XRT_OK;
+}
+
+xrt_status xrt_adjoint_attenuated(xrt_plan p, const float* sino, const float* mu, float* img, void* cuda_stream) {
+    if (!p || !img || !mu || !sino) return fail(XRT_ERR_INVALID_ARG, "NULL argument");
+    DevGuard guard(p->device);
+    cudaStream_t s = (cudaStream_t)cuda_stream;
+    XRT_CUDA(cudaMemsetAsync(img, 0, sizeof(float) * (size_t)p->grid.nxyz, s));
+    cudaError_t e = xrt::launch_adjoint_att(p, sino, mu, img, 0, p->n_rays, s);
+    p->launches += 1;
+    if (e != cudaSuccess) return cuda_fail(e, "adjoint_attenuated launch");
+    return XRT_OK;
+}
+
 // Host-buffer forward: H2D(image) -> per view chunk: kernel, then D2H of that chunk on the aux
 // stream, so the sinogram download overlaps the next chunk's kernel.
 xrt_status xrt_forward_host(xrt_plan p, const float* img_host, float* sino_host, void* cuda_stream) {

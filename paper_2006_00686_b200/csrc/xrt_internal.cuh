@@ -252,6 +252,10 @@ cudaError_t launch_adjoint_ray(const xrt_plan_s* p, const float* sino, float* im
                                int64_t ray1, cudaStream_t s);
 cudaError_t launch_units_count(const xrt_plan_s* p, int64_t ray0, int64_t ray1, int64_t* counts,
                                cudaStream_t s);
+cudaError_t launch_forward_att(const xrt_plan_s* p, const float* img, const float* mu, float* sino, int64_t ray0,
+                               int64_t ray1, cudaStream_t s);
+cudaError_t launch_adjoint_att(const xrt_plan_s* p, const float* sino, const float* mu, float* img, int64_t ray0,
+                               int64_t ray1, cudaStream_t s);
 cudaError_t launch_forward64(const xrt_plan_s* p, const double* img, double* sino, int64_t ray0,
                              int64_t ray1, cudaStream_t s);
 cudaError_t launch_adjoint64(const xrt_plan_s* p, const double* sino, double* img, int64_t ray0,

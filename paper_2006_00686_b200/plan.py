@@ -165,6 +165,31 @@ class Plan:
         check(self._lib.xrt_adjoint_f64(self._h, sino.data_ptr(), out.data_ptr(), _stream_handle(stream)))
         return out
 
+    def forward_attenuated(self, img: torch.Tensor, mu: torch.Tensor, out: torch.Tensor | None = None,
+                           stream=None) -> torch.Tensor:
+        """xrt_forward_attenuated: sino[m] = sum_I img[I] exp(-A_mI) (1 - exp(-mu_I l_mI)) / mu_I
+        (SPECT weight of P:36-40; A_mI = attenuation of the units after I along the ray)."""
+        self._check_dev(img, self.image_shape, "img")
+        self._check_dev(mu, self.image_shape, "mu")
+        if out is None:
+            out = torch.empty(self.sino_shape, dtype=torch.float32, device=img.device)
+        self._check_dev(out, self.sino_shape, "sino")
+        check(self._lib.xrt_forward_attenuated(self._h, img.data_ptr(), mu.data_ptr(), out.data_ptr(),
+                                               _stream_handle(stream)))
+        return out
+
+    def adjoint_attenuated(self, sino: torch.Tensor, mu: torch.Tensor, out: torch.Tensor | None = None,
+                           stream=None) -> torch.Tensor:
+        """xrt_adjoint_attenuated: the transpose of forward_attenuated."""
+        self._check_dev(sino, self.sino_shape, "sino")
+        self._check_dev(mu, self.image_shape, "mu")
+        if out is None:
+            out = torch.empty(self.image_shape, dtype=torch.float32, device=sino.device)
+        self._check_dev(out, self.image_shape, "img")
+        check(self._lib.xrt_adjoint_attenuated(self._h, sino.data_ptr(), mu.data_ptr(), out.data_ptr(),
+                                               _stream_handle(stream)))
+        return out
+
     def forward_host(self, img: torch.Tensor, out: torch.Tensor | None = None, stream=None) -> torch.Tensor:
         """xrt_forward_host: host (ideally pinned) fp32 buffers, copies inside the call."""
         if img.is_cuda or img.dtype != torch.float32 or not img.is_contiguous():

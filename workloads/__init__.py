@@ -10,4 +10,4 @@ lengths), so the oracle (``oracle/``) and the product
 method's code.
 """
 from .configs import CONFIGS, config, view_angles, scaled  # noqa: F401
-from .phantoms import make_image, make_sino_input, sample_rays  # noqa: F401
+from .phantoms import make_image, make_sino_input, make_attenuation, sample_rays  # noqa: F401

@@ -10,6 +10,9 @@ Recipe (DESIGN.md §4 "Inputs"), following BASELINE.json ``configs``:
   containing the unit CENTRE (reading 19).  W_a = N_a * d_a is the field width.
   Evaluated in fp64, stored as fp32.
 * adjoint input y ~ U[-1, 1) per ray from PCG64(adj_seed).
+* attenuation map mu (the attenuated transform): the config's phantom with its
+  densities' absolute values, |f_I|, scaled by 2 / W_max (W_max the widest field width), so a
+  chord through the densest region attenuates by exp(-O(1)) as in SPECT; fp32.
 
 Unit centres are the paper's shifted by the image centre and
 scaled by the spacing: x_i = x_lo + (i + 1/2) d_x, y_j = y_hi - (j + 1/2) d_y,
@@ -119,6 +122,12 @@ def make_sino_input(c: dict, device="cpu", seed: int | None = None) -> torch.Ten
     gen = torch.Generator(device="cpu").manual_seed(int(s))
     y = torch.rand((V, R, C), generator=gen, dtype=torch.float32) * 2 - 1
     return y.to(device)
+
+
+def make_attenuation(c: dict, device="cpu") -> torch.Tensor:
+    """Attenuation map mu >= 0 on the image grid (fp32, same shape as make_image), 1/length."""
+    w = max(float(c["n"][a]) * float(c["spacing"][a]) for a in range(3) if int(c["n"][a]) > 1)
+    return (make_image(c).abs() * (2.0 / w)).to(device)
 
 
 def sample_rays(c: dict, count: int, seed: int) -> np.ndarray:
