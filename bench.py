@@ -202,6 +202,8 @@ def main():
                     help="adjoint kernel family (default: --algo)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-attenuated", action="store_true",
+                    help="skip the attenuated-transform side measurement (SURVEY 8(f) N4)")
     ap.add_argument("--ref-rays", type=int, default=256)
     args = ap.parse_args()
 
@@ -311,6 +313,33 @@ def main():
                "h2d_bytes_per_step": img_b + sino_b, "d2h_bytes_per_step": sino_b + img_b,
                "note": "xrt_forward_host + xrt_adjoint_host, pinned host buffers, per-rank bytes"}
 
+    # ---------------- attenuated transform (N4): side measurement, outside the timed step
+    att = None
+    if world == 1 and not args.no_attenuated:
+        mu = workloads.make_attenuation(c, device=dev)
+        y = sino.clone()
+
+        def att_ms(fn, reps=2):
+            fn()
+            torch.cuda.synchronize()
+            a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a0.record(s)
+            for _ in range(reps):
+                fn()
+            a1.record(s)
+            torch.cuda.synchronize()
+            return a0.elapsed_time(a1) / reps
+
+        la0 = plan.launch_count
+        f_ms = att_ms(lambda: plan.forward_attenuated(x, mu, out=sino))
+        b_ms = att_ms(lambda: plan.adjoint_attenuated(y, mu, out=xo))
+        att = {"forward_ms": f_ms, "adjoint_ms": b_ms,
+               "forward_rays_per_s": M / (f_ms / 1e3), "adjoint_rays_per_s": M / (b_ms / 1e3),
+               "forward_intersections_per_s": nnz_local / (f_ms / 1e3),
+               "gpu_launches": plan.launch_count - la0,
+               "note": "xrt_forward_attenuated / xrt_adjoint_attenuated (SPECT weight, DESIGN reading 23), "
+                       "RAY family, mu = workloads.make_attenuation; 1 warm-up + 2 timed calls each, not in the step"}
+
     if rank != 0:
         if world > 1:
             dist.destroy_process_group()
@@ -354,6 +383,8 @@ def main():
     }
     if e2e is not None:
         line["e2e"] = e2e
+    if att is not None:
+        line["attenuated"] = att
     if world == 1 and not args.no_cpu:
         try:
             line["cpu_baseline"] = cpu_baseline(c)
