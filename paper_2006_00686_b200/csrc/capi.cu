@@ -441,6 +441,7 @@ xrt_status plan_create_impl(const xrt_geometry* g, int cuda_device, xrt_plan* ou
     if (p->column_ok) {
         p->zpad = column_zpad(g, G);
         p->col_np = xrt::choose_col_np(D.rows);
+        p->col_np_adj = std::getenv("XRT_COL_NP_ADJ") ? std::atoi(std::getenv("XRT_COL_NP_ADJ")) : 1;
         p->nzp = (G.n[2] + 2 * p->zpad + 3) / 4 * 4;   // 16-byte cell columns (vector reds); tail rows stay 0
         const size_t bytes = sizeof(float) * (size_t)(G.nxy * p->nzp);
         e = cudaMalloc(&p->d_work_fwd, bytes);
@@ -650,7 +651,7 @@ xrt_status xrt_forward_host(xrt_plan p, const float* img_host, float* sino_host,
     if (resolve(p, XRT_OP_FORWARD) == XRT_ALGO_COLUMN && p->dim == 3) {
         // COLUMN: one launch per band of detector rows; the band's sinogram rows (every view) go
         // back on the aux stream while the next band computes
-        const int nb = xrt::column_bands(p), rb = xrt::column_band_rows(p);
+        const int nb = xrt::column_bands(p, false), rb = xrt::column_band_rows(p, false);
         const size_t pitch = sizeof(float) * (size_t)p->det.per_view;
         std::vector<cudaEvent_t> ev((size_t)nb);
         for (auto& x : ev) XRT_CUDA(cudaEventCreateWithFlags(&x, cudaEventDisableTiming));
@@ -713,7 +714,7 @@ xrt_status xrt_adjoint_host(xrt_plan p, const float* sino_host, float* img_host,
     if (resolve(p, XRT_OP_ADJOINT) == XRT_ALGO_COLUMN && p->dim == 3) {
         // COLUMN: the sinogram rows of band b (every view) are uploaded on the aux stream while
         // band b - 1 computes; one launch per band
-        const int nb = xrt::column_bands(p), rb = xrt::column_band_rows(p);
+        const int nb = xrt::column_bands(p, true), rb = xrt::column_band_rows(p, true);
         const size_t pitch = sizeof(float) * (size_t)p->det.per_view;
         std::vector<cudaEvent_t> ev((size_t)nb);
         for (auto& x : ev) XRT_CUDA(cudaEventCreateWithFlags(&x, cudaEventDisableTiming));

@@ -620,7 +620,7 @@ __device__ __forceinline__ void column_segments_adj(unsigned seg, int total, Ray
 #endif
 
 template <bool kAdjoint, int NP>
-__global__ void __launch_bounds__(kWarps * 32, XRT_COL_MINB) k_column(const ViewRec* __restrict__ views, DetC dc, GridC g,
+__global__ void __launch_bounds__(kWarps * 32, NP >= 4 ? 2 : XRT_COL_MINB) k_column(const ViewRec* __restrict__ views, DetC dc, GridC g,
                                                        const float* __restrict__ vol, float* __restrict__ volw,
                                                        const float* __restrict__ sino_in,
                                                        float* __restrict__ sino_out, int view0,
@@ -1076,9 +1076,9 @@ cudaError_t launch_from_zfast(const xrt_plan_s* p, const float* work, float* img
     return transpose(work, img, p->grid.nxy, p->grid.n[2], p->nzp, p->zpad, p->grid.nxy, 0, s);
 }
 
-ColumnLaunch make_launch(const xrt_plan_s* p, int64_t v0, int64_t v1, int& nblk) {
+ColumnLaunch make_launch(const xrt_plan_s* p, int64_t v0, int64_t v1, int& nblk, bool adj) {
     ColumnLaunch L;
-    const int rows_per_band = 64 * p->col_np;
+    const int rows_per_band = column_band_rows(p, adj);
     L.n_views = (int)(v1 - v0);
     L.n_cgroups = (p->det.cols + kWarps - 1) / kWarps;
     L.n_bands = (p->det.rows + rows_per_band - 1) / rows_per_band;
@@ -1103,8 +1103,11 @@ cudaError_t launch_column(const xrt_plan_s* p, const float* vol, float* volw, co
                           float* sino_out, int64_t v0, const ColumnLaunch& L, int nblk, cudaStream_t s) {
     const ColDesc* d = (const ColDesc*)p->d_coldesc;
     if (nblk <= 0) return cudaSuccess;
-    if (p->col_np == 1)
+    const int np = kAdj ? p->col_np_adj : p->col_np;
+    if (np == 1)
         k_column<kAdj, 1><<<nblk, kWarps * 32, 0, s>>>(p->d_views, p->det, p->grid, vol, volw, sino_in, sino_out, (int)v0, d, L);
+    else if (np == 4)
+        k_column<kAdj, 4><<<nblk, kWarps * 32, 0, s>>>(p->d_views, p->det, p->grid, vol, volw, sino_in, sino_out, (int)v0, d, L);
     else
         k_column<kAdj, 2><<<nblk, kWarps * 32, 0, s>>>(p->d_views, p->det, p->grid, vol, volw, sino_in, sino_out, (int)v0, d, L);
     return cudaGetLastError();
@@ -1114,7 +1117,7 @@ cudaError_t launch_forward_column(const xrt_plan_s* p, const float* vol_zfast, f
                                   int64_t v0, int64_t v1, cudaStream_t s) {
     if (v1 <= v0) return cudaSuccess;
     int nblk = 0;
-    ColumnLaunch L = make_launch(p, v0, v1, nblk);
+    ColumnLaunch L = make_launch(p, v0, v1, nblk, false);
     if (L.items && !(v0 == 0 && v1 == p->n_views)) return cudaErrorInvalidValue;
     // rays whose column misses the image (or, tiled, every ray: partial sums) need zeros
     cudaError_t e = cudaMemsetAsync(sino + v0 * p->det.per_view, 0, sizeof(float) * (size_t)((v1 - v0) * p->det.per_view), s);
@@ -1124,14 +1127,17 @@ cudaError_t launch_forward_column(const xrt_plan_s* p, const float* vol_zfast, f
 
 // All views, detector-row bands [b0, b1) only (host pipelines: the sinogram rows of one band are
 // transferred while the next band computes).  Rows of band b: [b * rows_per_band, ...).
-int column_band_rows(const xrt_plan_s* p) { return 64 * p->col_np; }
-int column_bands(const xrt_plan_s* p) { return (p->det.rows + 64 * p->col_np - 1) / (64 * p->col_np); }
+int column_band_rows(const xrt_plan_s* p, bool adj) { return 64 * (adj ? p->col_np_adj : p->col_np); }
+int column_bands(const xrt_plan_s* p, bool adj) {
+    const int rb = column_band_rows(p, adj);
+    return (p->det.rows + rb - 1) / rb;
+}
 
 cudaError_t launch_forward_column_bands(const xrt_plan_s* p, const float* vol_zfast, float* sino, int b0,
                                         int b1, cudaStream_t s) {
     int nblk = 0;
-    ColumnLaunch L = make_launch(p, 0, p->n_views, nblk);
-    const int rb = column_band_rows(p);
+    ColumnLaunch L = make_launch(p, 0, p->n_views, nblk, false);
+    const int rb = column_band_rows(p, false);
     const int r0 = b0 * rb, r1 = std::min(p->det.rows, b1 * rb);
     if (r1 <= r0) return cudaSuccess;
     const size_t pitch = sizeof(float) * (size_t)p->det.per_view;
@@ -1145,7 +1151,7 @@ cudaError_t launch_forward_column_bands(const xrt_plan_s* p, const float* vol_zf
 cudaError_t launch_adjoint_column_bands(const xrt_plan_s* p, const float* sino, float* vol_zfast, int b0,
                                         int b1, cudaStream_t s) {
     int nblk = 0;
-    ColumnLaunch L = make_launch(p, 0, p->n_views, nblk);
+    ColumnLaunch L = make_launch(p, 0, p->n_views, nblk, true);
     L.band0 = b0;
     return launch_column<true>(p, nullptr, vol_zfast, sino, nullptr, 0, L, L.n_items * (b1 - b0), s);
 }
@@ -1154,7 +1160,7 @@ cudaError_t launch_adjoint_column(const xrt_plan_s* p, const float* sino, float*
                                   int64_t v0, int64_t v1, cudaStream_t s) {
     if (v1 <= v0) return cudaSuccess;
     int nblk = 0;
-    ColumnLaunch L = make_launch(p, v0, v1, nblk);
+    ColumnLaunch L = make_launch(p, v0, v1, nblk, true);
     if (L.items && !(v0 == 0 && v1 == p->n_views)) return cudaErrorInvalidValue;
     return launch_column<true>(p, nullptr, vol_zfast, sino, nullptr, v0, L, nblk, s);
 }
@@ -1162,6 +1168,7 @@ cudaError_t launch_adjoint_column(const xrt_plan_s* p, const float* sino, float*
 // Rays per lane 2 NP, NP in {1, 2}: the fewest idle rows in the last band of 64 NP rows (ties:
 // more rays per lane, i.e. each segment descriptor shared by more rays).
 int choose_col_np(int rows) {
+    if (const char* e = std::getenv("XRT_COL_NP")) return std::atoi(e);   // experiments
     int best = 1, best_waste = 1 << 30;
     for (int np = 1; np <= 2; ++np) {
         const int per = 64 * np;

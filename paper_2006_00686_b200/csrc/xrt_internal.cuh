@@ -225,7 +225,8 @@ struct xrt_plan_s {
     float* d_work_adj = nullptr;       // z-fastest, z-padded adjoint accumulator (COLUMN)
     int64_t zpad = 0, nzp = 0;         // z padding per side and padded column length
     int tile = 0, n_tx = 1, n_ty = 1;  // xy tiling of the column kernels (L2 residency)
-    int col_np = 2;                    // ray pairs per lane of the column kernels (rows per band = 64 col_np)
+    int col_np = 2;                    // ray pairs per lane of the forward column kernel (rows per band = 64 col_np)
+    int col_np_adj = 1;                // ... of the adjoint column kernel (measured: 1 pair is faster, cfg 3 / 4)
     void* d_items = nullptr;           // device uint2 work list (tiled) or nullptr
     void* d_coldesc = nullptr;         // per-(view, column) path descriptors (COLUMN, GATHER)
     double* d_rays = nullptr;          // explicit ray list (XRT_RAYS)
@@ -279,7 +280,7 @@ int column_cta_columns();
 cudaError_t launch_col_desc(const xrt_plan_s* p, cudaStream_t s);
 cudaError_t launch_adjoint_gather(const xrt_plan_s* p, const float* sino, float* vol_zfast, cudaStream_t s);
 int64_t gather_launches(const xrt_plan_s* p);
-int column_band_rows(const xrt_plan_s* p);
+int column_band_rows(const xrt_plan_s* p, bool adj);
 size_t raydesc2d_bytes();
 cudaError_t launch_raydesc2d(const xrt_plan_s* p, cudaStream_t s);
 cudaError_t launch_adjoint_gather2d(const xrt_plan_s* p, const float* sino, float* img, cudaStream_t s);
@@ -287,7 +288,7 @@ cudaError_t launch_transpose2d(const float* in, float* out, int rows, int cols, 
 cudaError_t launch_slice2d(const xrt_plan_s* p, bool adjoint, const float* img, const float* imgT,
                            const float* y_in, float* sino_out, float* acc_img, float* acc_imgT,
                            cudaStream_t s);
-int column_bands(const xrt_plan_s* p);
+int column_bands(const xrt_plan_s* p, bool adj);
 cudaError_t launch_forward_column_bands(const xrt_plan_s* p, const float* vol_zfast, float* sino, int b0,
                                         int b1, cudaStream_t s);
 cudaError_t launch_adjoint_column_bands(const xrt_plan_s* p, const float* sino, float* vol_zfast, int b0,
