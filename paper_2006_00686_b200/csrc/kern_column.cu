@@ -620,7 +620,13 @@ __device__ __forceinline__ void column_segments_adj(unsigned seg, int total, Ray
 #endif
 
 template <bool kAdjoint, int NP>
-__global__ void __launch_bounds__(kWarps * 32, NP >= 4 ? 2 : XRT_COL_MINB) k_column(const ViewRec* __restrict__ views, DetC dc, GridC g,
+#ifndef XRT_COL_MINB_ADJ1
+#define XRT_COL_MINB_ADJ1 4    // adjoint, 1 pair per lane: 64 registers, 4 CTAs / SM (measured faster than 3)
+#endif
+#ifndef XRT_COL_MINB_FWD1
+#define XRT_COL_MINB_FWD1 3
+#endif
+__global__ void __launch_bounds__(kWarps * 32, NP >= 4 ? 2 : (NP == 1 ? (kAdjoint ? XRT_COL_MINB_ADJ1 : XRT_COL_MINB_FWD1) : XRT_COL_MINB)) k_column(const ViewRec* __restrict__ views, DetC dc, GridC g,
                                                        const float* __restrict__ vol, float* __restrict__ volw,
                                                        const float* __restrict__ sino_in,
                                                        float* __restrict__ sino_out, int view0,
