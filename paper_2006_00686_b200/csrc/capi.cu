@@ -456,26 +456,35 @@ xrt_status plan_create_impl(const xrt_geometry* g, int cuda_device, xrt_plan* ou
         if (e == cudaSuccess)
             e = cudaMalloc(&p->d_gather_y, sizeof(float) * (size_t)(p->gather_views * D.per_view));
         if (e == cudaSuccess) e = cudaDeviceSynchronize();
-        // xy tiling: largest power-of-two tile whose z-fastest columns, restricted to the z slab one
-        // band of detector rows can reach (the kernels run band-major), fit the L2 budget
-        const double budget = 64.0 * 1024 * 1024;
-        const double slab = std::min((double)p->nzp, column_band_slab(g, G, 64 * p->col_np) + 2.0);
-        int ts = 32;
-        while ((double)(2 * ts) * (2 * ts) * slab * 4.0 <= budget) ts *= 2;
-        if (const char* f = std::getenv("XRT_COLUMN_TILE")) ts = std::max(4, std::atoi(f));  // testing
-        if (ts >= std::max(G.n[0], G.n[1])) {
-            p->tile = std::max(G.n[0], G.n[1]);
-            p->n_tx = p->n_ty = 1;
-        } else {
-            p->tile = ts;
-            p->n_tx = (G.n[0] + ts - 1) / ts;
-            p->n_ty = (G.n[1] + ts - 1) / ts;
-            std::vector<uint2> items;
-            xrt::build_column_items(p, views.data(), items);
-            p->n_items = (int64_t)items.size();
-            if (e == cudaSuccess && !items.empty()) e = cudaMalloc(&p->d_items, sizeof(uint2) * items.size());
-            if (e == cudaSuccess && !items.empty())
-                e = cudaMemcpy(p->d_items, items.data(), sizeof(uint2) * items.size(), cudaMemcpyHostToDevice);
+        // xy tiling, per operator: the largest power-of-two tile whose z-fastest columns, restricted
+        // to the z slab one band of detector rows can reach (the kernels run band-major), fit the
+        // operator's budget: forward 64 MB (cfg 4: 256^2 tiles); adjoint 320 MB, i.e. in practice
+        // untiled in xy -- its bands are half as tall and its reductions are not re-read, and the
+        // band-major order alone measured fastest (cfg 4: 197.6 ms vs 203.8 ms at 64 MB; cfg 5
+        // 23.4 vs 24.0 ms; cfg 3 equal)
+        for (int op = 0; op < 2 && e == cudaSuccess; ++op) {
+            const char* env = std::getenv(op ? "XRT_ADJ_L2_MB" : "XRT_FWD_L2_MB");
+            const double budget = (env ? std::atof(env) : (op ? 320.0 : 64.0)) * 1024 * 1024;
+            const int rows = 64 * (op ? p->col_np_adj : p->col_np);
+            const double slab = std::min((double)p->nzp, column_band_slab(g, G, rows) + 2.0);
+            int ts = 32;
+            while ((double)(2 * ts) * (2 * ts) * slab * 4.0 <= budget) ts *= 2;
+            if (const char* f = std::getenv("XRT_COLUMN_TILE")) ts = std::max(4, std::atoi(f));  // testing
+            xrt_plan_s::ColTiling& T = p->ct[op];
+            if (ts >= std::max(G.n[0], G.n[1])) {
+                T.tile = std::max(G.n[0], G.n[1]);
+                T.n_tx = T.n_ty = 1;
+            } else {
+                T.tile = ts;
+                T.n_tx = (G.n[0] + ts - 1) / ts;
+                T.n_ty = (G.n[1] + ts - 1) / ts;
+                std::vector<uint2> items;
+                xrt::build_column_items(p, views.data(), T.tile, T.n_tx, T.n_ty, items);
+                T.n_items = (int64_t)items.size();
+                if (!items.empty()) e = cudaMalloc(&T.d_items, sizeof(uint2) * items.size());
+                if (e == cudaSuccess && !items.empty())
+                    e = cudaMemcpy(T.d_items, items.data(), sizeof(uint2) * items.size(), cudaMemcpyHostToDevice);
+            }
         }
         if (e != cudaSuccess) {
             xrt_plan_destroy(p);
@@ -533,7 +542,8 @@ xrt_status xrt_plan_destroy(xrt_plan p) {
     cudaFree(p->d_views);
     cudaFree(p->d_work_fwd);
     cudaFree(p->d_work_adj);
-    cudaFree(p->d_items);
+    cudaFree(p->ct[0].d_items);
+    cudaFree(p->ct[1].d_items);
     cudaFree(p->d_coldesc);
     cudaFree(p->d_gather_y);
     cudaFree(p->d_rays);

@@ -1090,11 +1090,12 @@ ColumnLaunch make_launch(const xrt_plan_s* p, int64_t v0, int64_t v1, int& nblk,
     L.n_bands = (p->det.rows + rows_per_band - 1) / rows_per_band;
     L.nzp = (int)p->nzp;
     L.pad = (int)p->zpad;
-    L.tile = p->tile;
-    L.n_tx = p->n_tx;
-    if (p->d_items) {
-        L.items = (const uint2*)p->d_items;
-        L.n_items = (int)p->n_items;
+    const xrt_plan_s::ColTiling& T = p->ct[adj ? 1 : 0];
+    L.tile = T.tile;
+    L.n_tx = T.n_tx;
+    if (T.d_items) {
+        L.items = (const uint2*)T.d_items;
+        L.n_items = (int)T.n_items;
     } else {
         L.items = nullptr;
         L.n_items = L.n_views * L.n_cgroups;
@@ -1197,10 +1198,10 @@ cudaError_t launch_col_desc(const xrt_plan_s* p, cudaStream_t s) {
 
 // Host: work list of the tiled launch.  For every view and column group, the tiles crossed by
 // any of the group's in-plane lines (walked in fp64 over the tile grid); items sorted by tile.
-int build_column_items(const xrt_plan_s* p, const ViewRec* views_host, std::vector<uint2>& items) {
+int build_column_items(const xrt_plan_s* p, const ViewRec* views_host, int ts, int ntx, int nty,
+                       std::vector<uint2>& items) {
     const GridC& g = p->grid;
     const DetC& dc = p->det;
-    const int ts = p->tile, ntx = p->n_tx, nty = p->n_ty;
     const int C = kWarps;
     const int ncg = (dc.cols + C - 1) / C;
     std::vector<std::vector<uint2>> per_tile((size_t)ntx * nty);

@@ -224,17 +224,20 @@ struct xrt_plan_s {
     float* d_work_fwd = nullptr;       // z-fastest, z-padded copy of the forward input (COLUMN)
     float* d_work_adj = nullptr;       // z-fastest, z-padded adjoint accumulator (COLUMN)
     int64_t zpad = 0, nzp = 0;         // z padding per side and padded column length
-    int tile = 0, n_tx = 1, n_ty = 1;  // xy tiling of the column kernels (L2 residency)
+    // xy tiling of the column kernels (L2 residency), per operator: [0] forward, [1] adjoint
+    struct ColTiling {
+        int tile = 0, n_tx = 1, n_ty = 1;
+        void* d_items = nullptr;       // device uint2 work list (tiled) or nullptr (one tile)
+        int64_t n_items = 0;
+    } ct[2];
     int col_np = 2;                    // ray pairs per lane of the forward column kernel (rows per band = 64 col_np)
     int col_np_adj = 1;                // ... of the adjoint column kernel (measured: 1 pair is faster, cfg 3 / 4)
-    void* d_items = nullptr;           // device uint2 work list (tiled) or nullptr
     void* d_coldesc = nullptr;         // per-(view, column) path descriptors (COLUMN, GATHER)
     double* d_rays = nullptr;          // explicit ray list (XRT_RAYS)
     void* d_raydesc2d = nullptr;       // per-(view, column) rays in index space (2D GATHER)
     float* d_img_t = nullptr;          // 2D COLUMN (slice) kernels: transposed image / accumulator
     float* d_gather_y = nullptr;       // GATHER workspace: rescaled, transposed sinogram of one view block
     int64_t gather_views = 0;          // views per GATHER launch
-    int64_t n_items = 0;
     // host-pipeline staging (allocated on first *_host call)
     float* d_stage_img = nullptr;
     float* d_stage_sino = nullptr;
@@ -273,7 +276,8 @@ cudaError_t launch_adjoint_column(const xrt_plan_s* p, const float* sino, float*
 }  // namespace xrt
 #include <vector>
 namespace xrt {
-int build_column_items(const xrt_plan_s* p, const ViewRec* views_host, std::vector<uint2>& items);
+int build_column_items(const xrt_plan_s* p, const ViewRec* views_host, int ts, int ntx, int nty,
+                       std::vector<uint2>& items);
 size_t column_desc_bytes();
 int choose_col_np(int rows);
 int column_cta_columns();
