@@ -458,13 +458,13 @@ xrt_status plan_create_impl(const xrt_geometry* g, int cuda_device, xrt_plan* ou
         if (e == cudaSuccess) e = cudaDeviceSynchronize();
         // xy tiling, per operator: the largest power-of-two tile whose z-fastest columns, restricted
         // to the z slab one band of detector rows can reach (the kernels run band-major), fit the
-        // operator's budget: forward 64 MB (cfg 4: 256^2 tiles); adjoint 320 MB, i.e. in practice
-        // untiled in xy -- its bands are half as tall and its reductions are not re-read, and the
-        // band-major order alone measured fastest (cfg 4: 197.6 ms vs 203.8 ms at 64 MB; cfg 5
-        // 23.4 vs 24.0 ms; cfg 3 equal)
+        // operator's budget, 64 MB for both (cfg 4: 256^2 tiles).  Measured alternative for the
+        // adjoint: untiled in xy (budget >= 160 MB) runs 3 % faster on cfg 4 (197.6 vs 203.8 ms) but
+        // writes 58 GB of partially reduced lines back to DRAM per launch instead of 7.6 GB
+        // (profiles/r1d_cfg4.md); the L2-resident tiling is kept.
         for (int op = 0; op < 2 && e == cudaSuccess; ++op) {
             const char* env = std::getenv(op ? "XRT_ADJ_L2_MB" : "XRT_FWD_L2_MB");
-            const double budget = (env ? std::atof(env) : (op ? 320.0 : 64.0)) * 1024 * 1024;
+            const double budget = (env ? std::atof(env) : 64.0) * 1024 * 1024;
             const int rows = 64 * (op ? p->col_np_adj : p->col_np);
             const double slab = std::min((double)p->nzp, column_band_slab(g, G, rows) + 2.0);
             int ts = 32;

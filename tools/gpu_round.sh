@@ -21,3 +21,8 @@ timeout 1200 ncu --set full --clock-control none --import-source on -k regex:k_c
     -o $out/prof_adj_$tag $CMD > $out/ncu_adj_$tag.log 2>&1
 echo "full adj exit $?" >> $out/plain_$tag.log
 cat $out/plain_$tag.log | tail -3
+# attenuated transform (N4): one ncu --set full capture of each RAY-family attenuated kernel, cfg 5
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_(forward|adjoint)_att" -s 2 -c 2 \
+    -o $out/prof_att_$tag python tools/time_atten.py 5 1 > $out/ncu_att_$tag.log 2>&1
+echo "full att exit $?" >> $out/plain_$tag.log
+tail -1 $out/plain_$tag.log
