@@ -338,7 +338,8 @@ def main():
                "forward_intersections_per_s": nnz_local / (f_ms / 1e3),
                "gpu_launches": plan.launch_count - la0,
                "note": "xrt_forward_attenuated / xrt_adjoint_attenuated (SPECT weight, DESIGN reading 23), "
-                       "RAY family, mu = workloads.make_attenuation; 1 warm-up + 2 timed calls each, not in the step"}
+                       "column kernels on the 3D beams (untiled) else RAY, mu = workloads.make_attenuation; "
+                       "1 warm-up + 2 timed calls each, not in the step"}
 
     if rank != 0:
         if world > 1:

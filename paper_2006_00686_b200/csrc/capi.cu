@@ -542,6 +542,9 @@ xrt_status xrt_plan_destroy(xrt_plan p) {
     cudaFree(p->d_views);
     cudaFree(p->d_work_fwd);
     cudaFree(p->d_work_adj);
+    cudaFree(p->d_work_att);
+    cudaFree(p->d_att_A);
+    cudaFree(p->d_att_mumax);
     cudaFree(p->ct[0].d_items);
     cudaFree(p->ct[1].d_items);
     cudaFree(p->d_coldesc);
@@ -625,12 +628,35 @@ xrt_status xrt_adjoint_f64(xrt_plan p, const double* sino, double* img, void* cu
     return XRT_OK;
 }
 
-// Attenuated transform: RAY family, every geometry.
+// Attenuated transform: the column kernels for the 3D beams they serve (untiled: the
+// attenuation couples a ray's units along its whole path), else the RAY family.
+static cudaError_t att_alloc(xrt_plan p, bool adjoint) {
+    cudaError_t e = cudaSuccess;
+    if (!p->d_att_mumax) e = cudaMalloc(&p->d_att_mumax, sizeof(unsigned));
+    if (e == cudaSuccess && !adjoint && !p->d_work_att) {
+        const size_t bytes = 2 * sizeof(float) * (size_t)(p->grid.nxy * p->nzp);
+        e = cudaMalloc(&p->d_work_att, bytes);
+        if (e == cudaSuccess) e = cudaMemset(p->d_work_att, 0, bytes);   // zero padding stays zero
+    }
+    if (e == cudaSuccess && adjoint && !p->d_att_A)
+        e = cudaMalloc(&p->d_att_A, sizeof(float) * (size_t)(p->n_views * p->det.per_view));
+    return e;
+}
+
 xrt_status xrt_forward_attenuated(xrt_plan p, const float* img, const float* mu, float* sino, void* cuda_stream) {
     if (!p || !img || !mu || !sino) return fail(XRT_ERR_INVALID_ARG, "NULL argument");
     DevGuard guard(p->device);
-    cudaError_t e = xrt::launch_forward_att(p, img, mu, sino, 0, p->n_rays, (cudaStream_t)cuda_stream);
-    p->launches += 1;
+    cudaStream_t s = (cudaStream_t)cuda_stream;
+    cudaError_t e;
+    if (p->dim == 3 && resolve(p, XRT_OP_FORWARD) == XRT_ALGO_COLUMN) {
+        e = att_alloc(p, false);
+        if (e == cudaSuccess) e = xrt::launch_att_prepare(p, img, mu, p->d_work_att, p->d_att_mumax, s);
+        if (e == cudaSuccess) e = xrt::launch_forward_att_column(p, p->d_work_att, p->d_att_mumax, sino, s);
+        p->launches += 4;
+    } else {
+        e = xrt::launch_forward_att(p, img, mu, sino, 0, p->n_rays, s);
+        p->launches += 1;
+    }
     if (e != cudaSuccess) return cuda_fail(e, "forward_attenuated launch");
     return XRT_OK;
 }
@@ -639,9 +665,23 @@ xrt_status xrt_adjoint_attenuated(xrt_plan p, const float* sino, const float* mu
     if (!p || !img || !mu || !sino) return fail(XRT_ERR_INVALID_ARG, "NULL argument");
     DevGuard guard(p->device);
     cudaStream_t s = (cudaStream_t)cuda_stream;
-    XRT_CUDA(cudaMemsetAsync(img, 0, sizeof(float) * (size_t)p->grid.nxyz, s));
-    cudaError_t e = xrt::launch_adjoint_att(p, sino, mu, img, 0, p->n_rays, s);
-    p->launches += 1;
+    cudaError_t e;
+    if (p->dim == 3 && resolve(p, XRT_OP_ADJOINT) == XRT_ALGO_COLUMN) {
+        // mu z-fastest in work_fwd; pass 1: each ray's total attenuation A (plain forward of mu),
+        // pass 2 reduces y e^-(A - A_le) L phi into work_adj
+        e = att_alloc(p, true);
+        if (e == cudaSuccess) e = xrt::launch_to_zfast(p, mu, p->d_work_fwd, s);
+        if (e == cudaSuccess) e = xrt::launch_att_prepare(p, nullptr, mu, nullptr, p->d_att_mumax, s);
+        if (e == cudaSuccess) e = cudaMemsetAsync(p->d_work_adj, 0, sizeof(float) * (size_t)(p->grid.nxy * p->nzp), s);
+        if (e == cudaSuccess)
+            e = xrt::launch_adjoint_att_column(p, p->d_work_fwd, p->d_att_A, p->d_att_mumax, sino, p->d_work_adj, s);
+        if (e == cudaSuccess) e = xrt::launch_from_zfast(p, p->d_work_adj, img, s);
+        p->launches += 5;
+    } else {
+        e = cudaMemsetAsync(img, 0, sizeof(float) * (size_t)p->grid.nxyz, s);
+        if (e == cudaSuccess) e = xrt::launch_adjoint_att(p, sino, mu, img, 0, p->n_rays, s);
+        p->launches += 1;
+    }
     if (e != cudaSuccess) return cuda_fail(e, "adjoint_attenuated launch");
     return XRT_OK;
 }

@@ -36,6 +36,7 @@
 
 #include <algorithm>
 #include <climits>
+#include <cmath>
 #include <cstdlib>
 #include <vector>
 
@@ -381,6 +382,7 @@ struct RayPair {
     float2 dkf;        // +-1 per crossing (0 when fixed), as float
     float2 acc0, acc1; // forward: sum f_s d_sigma, sum (f_e - f_s)(sigma_e - tau)
     float2 w;          // forward: 1 / cos(beta); adjoint: y / cos(beta)
+    float2 sc;         // 1 / cos(beta) (attenuated operators: physical length = sigma length * sc)
     int dk0, dk1;      // +-1 / 0 as int (neighbour offset in the mixed-direction loop)
     bool live0, live1; // ray exists and (adjoint) carries a non-zero value
 };
@@ -397,6 +399,7 @@ __device__ __forceinline__ void pair_init(RayPair& P, const RayZ& Za, const RayZ
     P.acc0 = make_float2(0.f, 0.f);
     P.acc1 = make_float2(0.f, 0.f);
     P.w = kAdj ? make_float2(ya * Za.scale, yb * Zb.scale) : make_float2(Za.scale, Zb.scale);
+    P.sc = make_float2(Za.scale, Zb.scale);
     P.live0 = Za.active && (!kAdj || ya != 0.f);
     P.live1 = Zb.active && (!kAdj || yb != 0.f);
 }
@@ -610,6 +613,119 @@ __device__ __forceinline__ void column_segments_adj(unsigned seg, int total, Ray
     }
 }
 
+// ---------------------------------------------------------------- attenuated operators (N4)
+// The units of a ray in path order (segment start cell, then the crossing cell), each of physical
+// length L = l_sigma / cos(beta): x = mu L, phi(x) = (1 - e^-x) / x, e = e^-x = 1 - x phi, and
+//     forward:  S <- S e + f L phi                       (S = sum_I f_I e^-A_I L_I phi_I at the end)
+//     adjoint:  A_le += x;  img_I += y L phi e^-(A - A_le) (A = the ray's total attenuation)
+// (DESIGN reading 23; the same weights as k_forward_att / k_adjoint_att).  phi by its Taylor series
+// for |x| <= 1/8 (truncation x^5 / 720 < 5e-8 relative); kExact: e^-x by ex2 and the quotient where
+// |x| > 1/8 (chosen per launch from max |mu| * the longest unit).
+template <bool kExact>
+__device__ __forceinline__ float2 att_phi(float2 x, float2& e) {
+    const float2 c5 = make_float2(1.f / 120.f, 1.f / 120.f), c4 = make_float2(-1.f / 24.f, -1.f / 24.f);
+    const float2 c3 = make_float2(1.f / 6.f, 1.f / 6.f), c2 = make_float2(-0.5f, -0.5f), c1 = make_float2(1.f, 1.f);
+    const float2 mx = make_float2(-x.x, -x.y);
+    float2 phi = __ffma2_rn(x, c5, c4);
+    phi = __ffma2_rn(phi, x, c3);
+    phi = __ffma2_rn(phi, x, c2);
+    phi = __ffma2_rn(phi, x, c1);
+    e = __ffma2_rn(mx, phi, c1);                         // 1 - x phi
+    if (kExact) {
+        if (fabsf(x.x) > 0.125f) { e.x = __expf(-x.x); phi.x = __fdividef(1.f - e.x, x.x); }
+        if (fabsf(x.y) > 0.125f) { e.y = __expf(-x.y); phi.y = __fdividef(1.f - e.y, x.y); }
+    }
+    return phi;
+}
+
+// forward: cells are float2 (f, mu) of the interleaved z-fastest buffer (8 bytes per cell)
+template <int NP, int DK, bool kExact>
+__device__ __forceinline__ void column_segments_fwd_att(unsigned seg, int total, RayPair (&P)[NP]) {
+    const float2 m1 = make_float2(-1.f, -1.f);
+#pragma unroll 2
+    for (int s = 0; s < total; ++s) {
+        const uint4 raw = lds128(seg + 16u * (unsigned)s);
+        const float qse = __uint_as_float(raw.z), qds = __uint_as_float(raw.w);
+        const float2 se2 = make_float2(qse, qse), ds2 = make_float2(qds, qds);
+#pragma unroll
+        for (int p = 0; p < NP; ++p) {
+            const float2* a0 = (const float2*)(seg_ptr(raw) + 8ull * __float_as_uint(P[p].kpf.x));
+            const float2* a1 = (const float2*)(seg_ptr(raw) + 8ull * __float_as_uint(P[p].kpf.y));
+            const int o0 = DK != 0 ? DK : P[p].dk0, o1 = DK != 0 ? DK : P[p].dk1;
+            const float2 v00 = __ldg(a0), v01 = __ldg(a1), v10 = __ldg(a0 + o0), v11 = __ldg(a1 + o1);
+            float2 cr, lm;
+            z_step<DK>(P[p], se2, cr, lm);
+            const float2 Ls = __fmul2_rn(__ffma2_rn(lm, m1, ds2), P[p].sc);   // (d_sigma - l_e) / cos(beta)
+            const float2 Le = __fmul2_rn(lm, P[p].sc);
+            float2 es, ee;
+            const float2 xs = __fmul2_rn(make_float2(v00.y, v01.y), Ls);
+            const float2 ps = att_phi<kExact>(xs, es);
+            P[p].acc0 = __ffma2_rn(make_float2(v00.x, v01.x), __fmul2_rn(Ls, ps), __fmul2_rn(P[p].acc0, es));
+            const float2 xe = __fmul2_rn(make_float2(v10.y, v11.y), Le);
+            const float2 pe = att_phi<kExact>(xe, ee);
+            P[p].acc0 = __ffma2_rn(make_float2(v10.x, v11.x), __fmul2_rn(Le, pe), __fmul2_rn(P[p].acc0, ee));
+        }
+    }
+}
+
+// adjoint: cells of mu at the segment pointer (z-fastest float), the accumulator at + dacc bytes;
+// acc0 = A_le (running), acc1 = A (the ray's total attenuation, from the plain forward of mu)
+template <int NP, int DK, bool kExact>
+__device__ __forceinline__ void column_segments_adj_att(unsigned seg, int total, RayPair (&P)[NP], long long dacc,
+                                                        unsigned klo, unsigned kn) {
+    const float2 m1 = make_float2(-1.f, -1.f);
+    const unsigned long long pol = l2_evict_last();
+#pragma unroll 2
+    for (int s = 0; s < total; ++s) {
+        const uint4 raw = lds128(seg + 16u * (unsigned)s);
+        const float qse = __uint_as_float(raw.z), qds = __uint_as_float(raw.w);
+        const float2 se2 = make_float2(qse, qse), ds2 = make_float2(qds, qds);
+#pragma unroll
+        for (int p = 0; p < NP; ++p) {
+            const float* a0 = (const float*)(seg_ptr(raw) + 4ull * __float_as_uint(P[p].kpf.x));
+            const float* a1 = (const float*)(seg_ptr(raw) + 4ull * __float_as_uint(P[p].kpf.y));
+            const int o0 = DK != 0 ? DK : P[p].dk0, o1 = DK != 0 ? DK : P[p].dk1;
+            const float2 mus = make_float2(__ldg(a0), __ldg(a1)), mue = make_float2(__ldg(a0 + o0), __ldg(a1 + o1));
+            const unsigned kb0 = __float_as_uint(P[p].kpf.x) - klo, kb1 = __float_as_uint(P[p].kpf.y) - klo;
+            float2 cr, lm;
+            z_step<DK>(P[p], se2, cr, lm);
+            const float2 ls = __ffma2_rn(lm, m1, ds2);
+            const float2 Ls = __fmul2_rn(ls, P[p].sc), Le = __fmul2_rn(lm, P[p].sc);
+            float2 es, ee;
+            const float2 xs = __fmul2_rn(mus, Ls);
+            const float2 ps = att_phi<kExact>(xs, es);
+            P[p].acc0 = __fadd2_rn(P[p].acc0, xs);
+            const float2 ts = __fadd2_rn(P[p].acc0, __fmul2_rn(P[p].acc1, m1));   // A_le - A
+            const float2 vs = __fmul2_rn(__fmul2_rn(P[p].w, ls), ps);             // y L phi
+            const float2 xe = __fmul2_rn(mue, Le);
+            const float2 pe = att_phi<kExact>(xe, ee);
+            P[p].acc0 = __fadd2_rn(P[p].acc0, xe);
+            const float2 te = __fadd2_rn(P[p].acc0, __fmul2_rn(P[p].acc1, m1));
+            const float2 ve = __fmul2_rn(__fmul2_rn(P[p].w, lm), pe);
+            float* w0 = (float*)((const char*)a0 + dacc);
+            float* w1 = (float*)((const char*)a1 + dacc);
+            if (P[p].live0 && kb0 < kn) red_add(w0, vs.x * __expf(ts.x), pol);
+            if (P[p].live1 && kb1 < kn) red_add(w1, vs.y * __expf(ts.y), pol);
+            if (P[p].live0 && cr.x != 0.f && kb0 + (unsigned)o0 < kn) red_add(w0 + o0, ve.x * __expf(te.x), pol);
+            if (P[p].live1 && cr.y != 0.f && kb1 + (unsigned)o1 < kn) red_add(w1 + o1, ve.y * __expf(te.y), pol);
+        }
+    }
+}
+
+template <int NP, int kOp, bool kExact>
+__device__ __forceinline__ void att_walk(unsigned seg, int total, RayPair (&P)[NP], int mode, long long dacc,
+                                         unsigned klo, unsigned kn) {
+    if (kOp == 3) {
+        if (mode == 1) column_segments_adj_att<NP, 1, kExact>(seg, total, P, dacc, klo, kn);
+        else if (mode == -1) column_segments_adj_att<NP, -1, kExact>(seg, total, P, dacc, klo, kn);
+        else column_segments_adj_att<NP, 0, kExact>(seg, total, P, dacc, klo, kn);
+    } else {
+        if (mode == 1) column_segments_fwd_att<NP, 1, kExact>(seg, total, P);
+        else if (mode == -1) column_segments_fwd_att<NP, -1, kExact>(seg, total, P);
+        else column_segments_fwd_att<NP, 0, kExact>(seg, total, P);
+    }
+}
+
 // CTA = kWarps adjacent detector columns of one view, one band of 64 NP rows, one xy tile.  Each
 // warp owns one column: it generates the column's in-plane path chunk by chunk (lane = one major
 // slice, warp scan, segments in its own shared-memory buffer; no CTA barrier) and walks it for its
@@ -619,18 +735,23 @@ __device__ __forceinline__ void column_segments_adj(unsigned seg, int total, Ray
 #define XRT_COL_MINB 3
 #endif
 
-template <bool kAdjoint, int NP>
+// kOp: 0 forward, 1 adjoint, 2 attenuated forward, 3 attenuated adjoint (N4)
+template <int kOp, int NP>
 #ifndef XRT_COL_MINB_ADJ1
 #define XRT_COL_MINB_ADJ1 4    // adjoint, 1 pair per lane: 64 registers, 4 CTAs / SM (measured faster than 3)
 #endif
 #ifndef XRT_COL_MINB_FWD1
 #define XRT_COL_MINB_FWD1 3
 #endif
-__global__ void __launch_bounds__(kWarps * 32, NP >= 4 ? 2 : (NP == 1 ? (kAdjoint ? XRT_COL_MINB_ADJ1 : XRT_COL_MINB_FWD1) : XRT_COL_MINB)) k_column(const ViewRec* __restrict__ views, DetC dc, GridC g,
+__global__ void __launch_bounds__(kWarps * 32, NP >= 4 ? 2 : (kOp >= 2 ? 2 : (NP == 1 ? (kOp == 1 ? XRT_COL_MINB_ADJ1 : XRT_COL_MINB_FWD1) : XRT_COL_MINB))) k_column(const ViewRec* __restrict__ views, DetC dc, GridC g,
                                                        const float* __restrict__ vol, float* __restrict__ volw,
                                                        const float* __restrict__ sino_in,
                                                        float* __restrict__ sino_out, int view0,
-                                                       const ColDesc* __restrict__ desc, ColumnLaunch L) {
+                                                       const ColDesc* __restrict__ desc, ColumnLaunch L,
+                                                       const float* __restrict__ sino_aux, const float* __restrict__ att_mumax,
+                                                       float att_lmax) {
+    constexpr bool kAdjoint = kOp == 1 || kOp == 3;
+    constexpr bool kAtt = kOp >= 2;
     constexpr int R = 2 * NP;
     __shared__ Seg s_seg[kWarps][2 * 32 * kPasses];
     __shared__ float s_first[kWarps];
@@ -693,6 +814,10 @@ __global__ void __launch_bounds__(kWarps * 32, NP >= 4 ? 2 : (NP == 1 ? (kAdjoin
         const float ya = (kAdjoint && Za.active) ? ld_stream(sino_in + ((int64_t)v * dc.rows + ra) * dc.cols + c, l2_evict_first()) : 0.f;
         const float yb = (kAdjoint && Zb.active) ? ld_stream(sino_in + ((int64_t)v * dc.rows + rb) * dc.cols + c, l2_evict_first()) : 0.f;
         pair_init(P[p], Za, Zb, ya, yb, kAdjoint);
+        if (kOp == 3) {   // the ray's total attenuation (plain forward of mu)
+            P[p].acc1 = make_float2(Za.active ? sino_aux[((int64_t)v * dc.rows + ra) * dc.cols + c] : 0.f,
+                                    Zb.active ? sino_aux[((int64_t)v * dc.rows + rb) * dc.cols + c] : 0.f);
+        }
         any_live |= P[p].live0 | P[p].live1;
         pos &= Za.dk >= 0 && Zb.dk >= 0;
         neg &= Za.dk <= 0 && Zb.dk <= 0;
@@ -704,9 +829,14 @@ __global__ void __launch_bounds__(kWarps * 32, NP >= 4 ? 2 : (NP == 1 ? (kAdjoin
     Seg* seg = s_seg[warp];
     const unsigned seg_s = (unsigned)__cvta_generic_to_shared(seg);
     // segment pointers pre-offset by -4 kMagicBits bytes (see RayPair)
-    const unsigned long long base = (unsigned long long)(kAdjoint ? (const float*)volw : vol) -
-                                    4ull * kMagicBits;
-    const unsigned long long cstride = 4ull * (unsigned long long)L.nzp;
+    // attenuated: the forward reads (f, mu) float2 cells; the adjoint reads mu at the pointer and
+    // reduces into volw at + dacc
+    constexpr unsigned long long kEsz = kOp == 2 ? 8ull : 4ull;
+    const unsigned long long base = (unsigned long long)((kAdjoint && !kAtt) ? (const float*)volw : vol) -
+                                    kEsz * kMagicBits;
+    const unsigned long long cstride = kEsz * (unsigned long long)L.nzp;
+    const long long dacc = kOp == 3 ? (long long)((const char*)volw - (const char*)vol) : 0ll;
+    const bool exact = kAtt && (*att_mumax) * att_lmax > 0.125f;
     bool zinit = !tiled;  // untiled: the z state at sigma = 0 is the initial one
     const unsigned klo = kMagicBits + (unsigned)L.pad, kn = (unsigned)g.n[2];   // interior z cells
     for (int n0 = na; n0 < nb; n0 += 32 * kPasses) {
@@ -747,7 +877,10 @@ __global__ void __launch_bounds__(kWarps * 32, NP >= 4 ? 2 : (NP == 1 ? (kAdjoin
                     z_skip(P[p].kpf.y, P[p].dk1, P[p].mz.y, P[p].ntz.y, P[p].ndtz.y, P[p].nt0z.y, sf);
                 }
             }
-            if (mode == 2) {
+            if (kAtt) {
+                if (exact) att_walk<NP, kOp, true>(seg_s, total, P, mode == 2 ? 0 : mode, dacc, klo, kn);
+                else att_walk<NP, kOp, false>(seg_s, total, P, mode == 2 ? 0 : mode, dacc, klo, kn);
+            } else if (mode == 2) {
                 if (kAdjoint) column_segments_adj_flat<NP>(seg_s, total, P, klo, kn);
                 else column_segments_fwd_flat<NP>(seg_s, total, P);
             } else if (kAdjoint) {
@@ -768,7 +901,7 @@ __global__ void __launch_bounds__(kWarps * 32, NP >= 4 ? 2 : (NP == 1 ? (kAdjoin
             const RayPair& Q = P[q >> 1];
             if (!((q & 1) ? Q.live1 : Q.live0)) continue;
             const float a = (q & 1) ? Q.acc0.y + Q.acc1.y : Q.acc0.x + Q.acc1.x;
-            const float out = a * ((q & 1) ? Q.w.y : Q.w.x);
+            const float out = kAtt ? ((q & 1) ? Q.acc0.y : Q.acc0.x) : a * ((q & 1) ? Q.w.y : Q.w.x);
             const int64_t m = ((int64_t)v * dc.rows + (band * R + q) * 32 + lane) * dc.cols + c;
             if (tiled) { if (out != 0.f) red_sino(sino_out + m, out, l2_evict_first()); }
             else __stcs(sino_out + m, out);
@@ -1082,7 +1215,7 @@ cudaError_t launch_from_zfast(const xrt_plan_s* p, const float* work, float* img
     return transpose(work, img, p->grid.nxy, p->grid.n[2], p->nzp, p->zpad, p->grid.nxy, 0, s);
 }
 
-ColumnLaunch make_launch(const xrt_plan_s* p, int64_t v0, int64_t v1, int& nblk, bool adj) {
+ColumnLaunch make_launch(const xrt_plan_s* p, int64_t v0, int64_t v1, int& nblk, bool adj, bool untiled = false) {
     ColumnLaunch L;
     const int rows_per_band = column_band_rows(p, adj);
     L.n_views = (int)(v1 - v0);
@@ -1090,7 +1223,8 @@ ColumnLaunch make_launch(const xrt_plan_s* p, int64_t v0, int64_t v1, int& nblk,
     L.n_bands = (p->det.rows + rows_per_band - 1) / rows_per_band;
     L.nzp = (int)p->nzp;
     L.pad = (int)p->zpad;
-    const xrt_plan_s::ColTiling& T = p->ct[adj ? 1 : 0];
+    static const xrt_plan_s::ColTiling kUntiled{};
+    const xrt_plan_s::ColTiling& T = untiled ? kUntiled : p->ct[adj ? 1 : 0];
     L.tile = T.tile;
     L.n_tx = T.n_tx;
     if (T.d_items) {
@@ -1105,19 +1239,30 @@ ColumnLaunch make_launch(const xrt_plan_s* p, int64_t v0, int64_t v1, int& nblk,
     return L;
 }
 
-template <bool kAdj>
-cudaError_t launch_column(const xrt_plan_s* p, const float* vol, float* volw, const float* sino_in,
-                          float* sino_out, int64_t v0, const ColumnLaunch& L, int nblk, cudaStream_t s) {
+template <int kOp>
+cudaError_t launch_column_op(const xrt_plan_s* p, const float* vol, float* volw, const float* sino_in,
+                             float* sino_out, int64_t v0, const ColumnLaunch& L, int nblk, cudaStream_t s,
+                             const float* sino_aux = nullptr, const float* att_mumax = nullptr, float att_lmax = 0.f) {
+    constexpr bool kAdj = kOp == 1 || kOp == 3;
     const ColDesc* d = (const ColDesc*)p->d_coldesc;
     if (nblk <= 0) return cudaSuccess;
     const int np = kAdj ? p->col_np_adj : p->col_np;
     if (np == 1)
-        k_column<kAdj, 1><<<nblk, kWarps * 32, 0, s>>>(p->d_views, p->det, p->grid, vol, volw, sino_in, sino_out, (int)v0, d, L);
-    else if (np == 4)
-        k_column<kAdj, 4><<<nblk, kWarps * 32, 0, s>>>(p->d_views, p->det, p->grid, vol, volw, sino_in, sino_out, (int)v0, d, L);
+        k_column<kOp, 1><<<nblk, kWarps * 32, 0, s>>>(p->d_views, p->det, p->grid, vol, volw, sino_in, sino_out, (int)v0, d, L,
+                                                      sino_aux, att_mumax, att_lmax);
+    else if (np == 4 && kOp < 2)
+        k_column<kOp < 2 ? kOp : 0, 4><<<nblk, kWarps * 32, 0, s>>>(p->d_views, p->det, p->grid, vol, volw, sino_in, sino_out, (int)v0,
+                                                                    d, L, sino_aux, att_mumax, att_lmax);
     else
-        k_column<kAdj, 2><<<nblk, kWarps * 32, 0, s>>>(p->d_views, p->det, p->grid, vol, volw, sino_in, sino_out, (int)v0, d, L);
+        k_column<kOp, 2><<<nblk, kWarps * 32, 0, s>>>(p->d_views, p->det, p->grid, vol, volw, sino_in, sino_out, (int)v0, d, L,
+                                                      sino_aux, att_mumax, att_lmax);
     return cudaGetLastError();
+}
+
+template <bool kAdj>
+cudaError_t launch_column(const xrt_plan_s* p, const float* vol, float* volw, const float* sino_in,
+                          float* sino_out, int64_t v0, const ColumnLaunch& L, int nblk, cudaStream_t s) {
+    return launch_column_op<kAdj ? 1 : 0>(p, vol, volw, sino_in, sino_out, v0, L, nblk, s);
 }
 
 cudaError_t launch_forward_column(const xrt_plan_s* p, const float* vol_zfast, float* sino,
@@ -1170,6 +1315,80 @@ cudaError_t launch_adjoint_column(const xrt_plan_s* p, const float* sino, float*
     ColumnLaunch L = make_launch(p, v0, v1, nblk, true);
     if (L.items && !(v0 == 0 && v1 == p->n_views)) return cudaErrorInvalidValue;
     return launch_column<true>(p, nullptr, vol_zfast, sino, nullptr, v0, L, nblk, s);
+}
+
+// ---------------------------------------------------------------- attenuated operators (N4)
+namespace {
+// [rows][cols] -> the .x (comp 0) or .y (comp 1) field of the float2 z-fastest [cols][NzP] buffer
+__global__ void k_transpose_f2(const float* __restrict__ in, float* __restrict__ out2, int64_t rows, int64_t cols,
+                               int64_t out_ld, int64_t out_off, int comp) {
+    __shared__ float tile[32][33];
+    const int64_t bx = (int64_t)blockIdx.x * 32;
+    for (int64_t by = (int64_t)blockIdx.y * 32; by < rows; by += (int64_t)gridDim.y * 32) {
+        for (int j = threadIdx.y; j < 32; j += 8) {
+            const int64_t r = by + j, cc = bx + threadIdx.x;
+            if (r < rows && cc < cols) tile[j][threadIdx.x] = in[r * cols + cc];
+        }
+        __syncthreads();
+        for (int j = threadIdx.y; j < 32; j += 8) {
+            const int64_t r = bx + j, cc = by + threadIdx.x;
+            if (r < cols && cc < rows) out2[2 * (r * out_ld + out_off + cc) + comp] = tile[threadIdx.x][j];
+        }
+        __syncthreads();
+    }
+}
+
+// max |mu| (as the bits of a non-negative float, whose integer order is the float order)
+__global__ void k_absmax(const float* __restrict__ a, int64_t n, unsigned* __restrict__ out) {
+    unsigned m = 0;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        m = max(m, __float_as_uint(fabsf(a[i])));
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if ((threadIdx.x & 31) == 0) atomicMax(out, m);
+}
+}  // namespace
+
+cudaError_t launch_att_prepare(const xrt_plan_s* p, const float* img, const float* mu, float* work2,
+                               unsigned* mumax, cudaStream_t s) {
+    const int64_t rows = p->grid.n[2], cols = p->grid.nxy;
+    const int64_t gy = (rows + 31) / 32;
+    dim3 grid((unsigned)((cols + 31) / 32), (unsigned)(gy < 32768 ? gy : 32768));
+    if (img) {
+        k_transpose_f2<<<grid, dim3(32, 8), 0, s>>>(img, work2, rows, cols, p->nzp, p->zpad, 0);
+        k_transpose_f2<<<grid, dim3(32, 8), 0, s>>>(mu, work2, rows, cols, p->nzp, p->zpad, 1);
+    }
+    cudaError_t e = cudaMemsetAsync(mumax, 0, sizeof(unsigned), s);
+    if (e != cudaSuccess) return e;
+    k_absmax<<<4 * 148, 256, 0, s>>>(mu, p->grid.nxyz, mumax);
+    return cudaGetLastError();
+}
+
+// longest physical unit (the cell diagonal): bounds x = mu l for the choice of the phi evaluation
+static float att_lmax(const xrt_plan_s* p) {
+    return (float)std::sqrt(p->grid.d[0] * p->grid.d[0] + p->grid.d[1] * p->grid.d[1] + p->grid.d[2] * p->grid.d[2]);
+}
+
+cudaError_t launch_forward_att_column(const xrt_plan_s* p, const float* work2, const unsigned* mumax, float* sino,
+                                      cudaStream_t s) {
+    int nblk = 0;
+    ColumnLaunch L = make_launch(p, 0, p->n_views, nblk, false, true);   // untiled: S is not additive over tiles
+    cudaError_t e = cudaMemsetAsync(sino, 0, sizeof(float) * (size_t)(p->n_views * p->det.per_view), s);
+    if (e != cudaSuccess) return e;
+    return launch_column_op<2>(p, work2, nullptr, nullptr, sino, 0, L, nblk, s, nullptr, (const float*)mumax,
+                               att_lmax(p));
+}
+
+cudaError_t launch_adjoint_att_column(const xrt_plan_s* p, const float* mu_zfast, float* sinoA,
+                                      const unsigned* mumax, const float* y, float* acc_zfast, cudaStream_t s) {
+    // pass 1: A per ray = the plain forward of mu (tiled, L2-resident); its rounding differs from the
+    // running sums of pass 2 by ~1e-7 A, i.e. the weights by a factor 1 +- 1e-7 A
+    cudaError_t e = launch_forward_column(p, mu_zfast, sinoA, 0, p->n_views, s);
+    if (e != cudaSuccess) return e;
+    int nblk = 0;
+    ColumnLaunch L = make_launch(p, 0, p->n_views, nblk, true, true);    // untiled: A_le runs from the entry
+    return launch_column_op<3>(p, mu_zfast, acc_zfast, y, nullptr, 0, L, nblk, s, sinoA, (const float*)mumax,
+                               att_lmax(p));
 }
 
 // Rays per lane 2 NP, NP in {1, 2}: the fewest idle rows in the last band of 64 NP rows (ties:

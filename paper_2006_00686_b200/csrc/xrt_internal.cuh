@@ -232,6 +232,10 @@ struct xrt_plan_s {
     } ct[2];
     int col_np = 2;                    // ray pairs per lane of the forward column kernel (rows per band = 64 col_np)
     int col_np_adj = 1;                // ... of the adjoint column kernel (measured: 1 pair is faster, cfg 3 / 4)
+    // attenuated operators on the column path (allocated on first use)
+    float* d_work_att = nullptr;       // z-fastest float2 (f, mu) cells
+    float* d_att_A = nullptr;          // per-ray total attenuation (sinogram-shaped)
+    unsigned* d_att_mumax = nullptr;   // max |mu| (float bits)
     void* d_coldesc = nullptr;         // per-(view, column) path descriptors (COLUMN, GATHER)
     double* d_rays = nullptr;          // explicit ray list (XRT_RAYS)
     void* d_raydesc2d = nullptr;       // per-(view, column) rays in index space (2D GATHER)
@@ -260,6 +264,12 @@ cudaError_t launch_forward_att(const xrt_plan_s* p, const float* img, const floa
                                int64_t ray1, cudaStream_t s);
 cudaError_t launch_adjoint_att(const xrt_plan_s* p, const float* sino, const float* mu, float* img, int64_t ray0,
                                int64_t ray1, cudaStream_t s);
+cudaError_t launch_att_prepare(const xrt_plan_s* p, const float* img, const float* mu, float* work2,
+                               unsigned* mumax, cudaStream_t s);
+cudaError_t launch_forward_att_column(const xrt_plan_s* p, const float* work2, const unsigned* mumax, float* sino,
+                                      cudaStream_t s);
+cudaError_t launch_adjoint_att_column(const xrt_plan_s* p, const float* mu_zfast, float* sinoA,
+                                      const unsigned* mumax, const float* y, float* acc_zfast, cudaStream_t s);
 cudaError_t launch_forward64(const xrt_plan_s* p, const double* img, double* sino, int64_t ray0,
                              int64_t ray1, cudaStream_t s);
 cudaError_t launch_adjoint64(const xrt_plan_s* p, const double* sino, double* img, int64_t ray0,
