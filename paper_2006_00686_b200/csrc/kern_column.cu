@@ -47,7 +47,10 @@ namespace xrt {
 namespace {
 
 constexpr int kWarps = 8;  // warps per CTA = adjacent detector columns per CTA (one per warp)
-constexpr int kPasses = 4; // 32-slice path-generation passes per chunk (chunk = 128 major slices)
+#ifndef XRT_KPASSES
+#define XRT_KPASSES 4
+#endif
+constexpr int kPasses = XRT_KPASSES; // 32-slice path-generation passes per chunk (chunk = 128 major slices)
 
 struct __align__(16) Seg {
     unsigned long long ptr;  // address of (cell, padded k = 0) in the z-fastest volume
