@@ -46,7 +46,10 @@ namespace xrt {
 
 namespace {
 
-constexpr int kWarps = 8;  // warps per CTA = adjacent detector columns per CTA (one per warp)
+#ifndef XRT_COL_WARPS
+#define XRT_COL_WARPS 8
+#endif
+constexpr int kWarps = XRT_COL_WARPS;  // warps per CTA = adjacent detector columns per CTA (one per warp)
 #ifndef XRT_KPASSES
 #define XRT_KPASSES 4
 #endif
