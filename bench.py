@@ -117,6 +117,33 @@ def measured_traffic(workload: str, kernel: str):
         return None
 
 
+def reduction_roofline(workload: str, nnz: int, adj_ms: float):
+    """The adjoint's second roofline: the SM -> L2 reduction path.  peak = the highest reduction
+    sector rate tools/red_peak measured on this GPU type (profiles/red_peak.json); algorithmic
+    sectors = nnz / 8 (every 32-byte sector carrying 8 units); measured sectors per launch from the
+    ncu capture (profiles/traffic.json).  None when either file is missing."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "red_peak.json")) as f:
+            rp = json.load(f)
+        peak = max(rp["coalesced"]["sectors_per_s"], rp["scattered"]["sectors_per_s"])
+    except Exception:
+        return None
+    alg = nnz / 8.0
+    out = {"bound": "l2_reduction", "unit": "sectors/s", "peak": peak,
+           "peak_source": "tools/red_peak (profiles/red_peak.json): red.global.add.f32 from all SMs into an "
+                          "L2-resident buffer, max over the coalesced and scattered patterns",
+           "achieved": alg / (adj_ms / 1e3), "frac": alg / (adj_ms / 1e3) / peak,
+           "algorithmic_sectors": alg}
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            rs = json.load(f)[workload]["adjoint"]["red_sectors"]
+        out["measured_sectors"] = rs
+        out["measured_frac"] = rs / (adj_ms / 1e3) / peak
+    except Exception:
+        pass
+    return out
+
+
 def cpu_baseline(c: dict, budget_s: float = 12.0):
     """The oracle, as it stands, on a bounded sample of the workload's rays (forward)."""
     import oracle
@@ -382,6 +409,10 @@ def main():
         "clocks": clk.summary(),
         "algo": args.algo, "adj_algo": args.adj_algo or args.algo,
     }
+    if world == 1 and args.adj_algo in (None, "auto", "column") and args.algo in ("auto", "column") and dim == 3:
+        rr = reduction_roofline(c["name"], nnz_local, adj_avg)
+        if rr is not None:
+            line["adjoint"]["roofline_reduction"] = rr
     if e2e is not None:
         line["e2e"] = e2e
     if att is not None:

@@ -1,0 +1,59 @@
+// Reduction-path microbenchmark (B200): throughput of red.global.add.f32 from all SMs into an
+// L2-resident buffer, for three warp access patterns:
+//   coalesced  : 32 lanes -> 32 consecutive floats (4 sectors per instruction, 8 elements per sector)
+//   adjoint-like: 32 lanes -> ~21 consecutive cells with duplicates (0.67 cells per lane, as the
+//                 column adjoint's start-cell reductions on cfg 4)
+//   scattered  : 32 lanes -> 32 different sectors (1 element per sector)
+// Prints one JSON line: elements/s, sectors/s and sectors per SM-cycle for each pattern.
+// nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o red_peak tools/red_peak.cu
+#include <cstdio>
+#include <cuda_runtime.h>
+
+__global__ void k_red(float* __restrict__ buf, unsigned mask_floats, int iters, int pattern) {
+    const unsigned lane = threadIdx.x & 31;
+    const unsigned warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    unsigned base = warp * 4096u;
+    for (int it = 0; it < iters; ++it) {
+        unsigned off;
+        if (pattern == 0) off = base + lane;
+        else if (pattern == 1) off = base + (lane * 2u) / 3u;
+        else off = base + lane * 8u;
+        float* a = buf + (off & mask_floats);
+        asm volatile("red.global.add.f32 [%0], %1;" :: "l"(a), "f"(1.0f) : "memory");
+        base += 256u;
+    }
+}
+
+int main() {
+    const size_t n = 8u << 20;                 // 32 MB: L2-resident
+    float* buf;
+    cudaMalloc(&buf, n * sizeof(float));
+    cudaMemset(buf, 0, n * sizeof(float));
+    int sms = 0, clk_khz = 0;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+    cudaDeviceGetAttribute(&clk_khz, cudaDevAttrClockRate, 0);
+    const int blocks = sms * 8, threads = 256, iters = 4096;
+    const double warps = (double)blocks * threads / 32;
+    const double sectors_per_inst[3] = {4.0, 3.0, 32.0};
+    const double elems_per_inst = 32.0;
+    const char* names[3] = {"coalesced", "adjoint_like", "scattered"};
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    printf("{\"sms\": %d, \"clock_mhz_attr\": %.0f", sms, clk_khz / 1e3);
+    for (int p = 0; p < 3; ++p) {
+        k_red<<<blocks, threads>>>(buf, (unsigned)(n - 1), 64, p);   // warm-up
+        cudaEventRecord(e0);
+        for (int r = 0; r < 5; ++r) k_red<<<blocks, threads>>>(buf, (unsigned)(n - 1), iters, p);
+        cudaEventRecord(e1);
+        cudaEventSynchronize(e1);
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, e0, e1);
+        const double insts = 5.0 * warps * iters;
+        const double s = ms / 1e3;
+        printf(", \"%s\": {\"ms\": %.3f, \"elements_per_s\": %.4g, \"sectors_per_s\": %.4g, \"warp_insts_per_s\": %.4g}",
+               names[p], ms, insts * elems_per_inst / s, insts * sectors_per_inst[p] / s, insts / s);
+    }
+    printf(", \"error\": \"%s\"}\n", cudaGetErrorString(cudaGetLastError()));
+    return 0;
+}
