@@ -29,9 +29,15 @@
 // adjacent k) touch consecutive addresses; transposes to / from the caller's [k][j][i] image
 // run inside xrt_forward / xrt_adjoint.
 //
-// Launch order: blockIdx.x = view (fastest), y = column group, z = row band: the CTAs resident at
-// any time are (nearly) all views of one or two column groups, whose in-plane lines all lie in a
-// thin annulus |s1| ~ const of the image -- a small, L2-resident working set reused by every view.
+// CTA = kWarps adjacent detector columns of one view x one band of 64 NP detector rows (warp =
+// column, 2 NP rays per lane) x one xy tile.  1D grid, band-major: blockIdx = band * n_items + item,
+// items = (view, column group, tile) sorted by tile (plan time, build_column_items), so every view
+// and column crossing one tile of one band's z slab runs while that slab is L2-resident.  Tiling
+// and rays per lane are chosen per operator (capi.cu).
+//
+// Operators (template kOp): 0 forward, 1 adjoint (red.global.add), 2 / 3 the attenuated forward /
+// adjoint of the SPECT weight (DESIGN reading 23; untiled).  Also here: the
+// voxel-driven gather adjoint (k_gather, XRT_ALGO_GATHER) and the z-fastest transposes.
 #include <cuda_runtime.h>
 
 #include <algorithm>
