@@ -4,6 +4,7 @@
 //   adjoint-like: 32 lanes -> ~21 consecutive cells with duplicates (0.67 cells per lane, as the
 //                 column adjoint's start-cell reductions on cfg 4)
 //   scattered  : 32 lanes -> 32 different sectors (1 element per sector)
+//   adjoint_dedup: the adjoint-like cells with the duplicate lanes idle (each cell once per warp)
 // Prints one JSON line: elements/s, sectors/s and sectors per SM-cycle for each pattern.
 // nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o red_peak tools/red_peak.cu
 #include <cstdio>
@@ -19,7 +20,14 @@ __global__ void k_red(float* __restrict__ buf, unsigned mask_floats, int iters, 
         else if (pattern == 1) off = base + (lane * 2u) / 3u;
         else off = base + lane * 8u;
         float* a = buf + (off & mask_floats);
-        asm volatile("red.global.add.f32 [%0], %1;" :: "l"(a), "f"(1.0f) : "memory");
+        if (pattern == 3) {
+            off = base + (lane * 2u) / 3u;
+            a = buf + (off & mask_floats);
+            const bool dup = lane > 0 && (lane * 2u) / 3u == ((lane - 1u) * 2u) / 3u;
+            if (!dup) asm volatile("red.global.add.f32 [%0], %1;" :: "l"(a), "f"(2.0f) : "memory");
+        } else {
+            asm volatile("red.global.add.f32 [%0], %1;" :: "l"(a), "f"(1.0f) : "memory");
+        }
         base += 256u;
     }
 }
@@ -34,14 +42,14 @@ int main() {
     cudaDeviceGetAttribute(&clk_khz, cudaDevAttrClockRate, 0);
     const int blocks = sms * 8, threads = 256, iters = 4096;
     const double warps = (double)blocks * threads / 32;
-    const double sectors_per_inst[3] = {4.0, 3.0, 32.0};
-    const double elems_per_inst = 32.0;
-    const char* names[3] = {"coalesced", "adjoint_like", "scattered"};
+    const double sectors_per_inst[4] = {4.0, 3.0, 32.0, 3.0};
+    const double elems_per_inst = 32.0;   // for pattern 3: the 32 lanes' units, carried by 22 lanes
+    const char* names[4] = {"coalesced", "adjoint_like", "scattered", "adjoint_dedup"};
     cudaEvent_t e0, e1;
     cudaEventCreate(&e0);
     cudaEventCreate(&e1);
     printf("{\"sms\": %d, \"clock_mhz_attr\": %.0f", sms, clk_khz / 1e3);
-    for (int p = 0; p < 3; ++p) {
+    for (int p = 0; p < 4; ++p) {
         k_red<<<blocks, threads>>>(buf, (unsigned)(n - 1), 64, p);   // warm-up
         cudaEventRecord(e0);
         for (int r = 0; r < 5; ++r) k_red<<<blocks, threads>>>(buf, (unsigned)(n - 1), iters, p);
