@@ -69,6 +69,23 @@ class ShardedPlan:
             dist.all_reduce(part, op=dist.ReduceOp.SUM, group=self.group)
         return part
 
+    def forward_attenuated(self, img: torch.Tensor, mu: torch.Tensor, out: torch.Tensor | None = None,
+                           broadcast_src: int | None = None):
+        """This rank's slab of the attenuated transform: rays are independent, so
+        the view split is the same as for A; img and mu replicated (broadcast from src if asked)."""
+        if broadcast_src is not None and self.world > 1:
+            dist.broadcast(img, src=broadcast_src, group=self.group)
+            dist.broadcast(mu, src=broadcast_src, group=self.group)
+        return self.plan.forward_attenuated(img, mu, out=out)
+
+    def adjoint_attenuated(self, sino_slab: torch.Tensor, mu: torch.Tensor,
+                           out: torch.Tensor | None = None) -> torch.Tensor:
+        """R_mu^T y of the full sinogram: local partial over this rank's views + all_reduce(sum)."""
+        part = self.plan.adjoint_attenuated(sino_slab, mu, out=out)
+        if self.world > 1:
+            dist.all_reduce(part, op=dist.ReduceOp.SUM, group=self.group)
+        return part
+
 
 def gather_sinogram(slab: torch.Tensor, n_views_total: int, rank: int, world: int, group=None) -> torch.Tensor:
     """Assemble the full sinogram on every rank (testing / I/O helper; not on the hot path)."""
@@ -160,6 +177,16 @@ class ZSlabShardedPlan:
     def adjoint(self, sino_rows: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
         """Slab [k0:k1] of A^T y from this rank's sinogram rows alone."""
         return self.plan.adjoint(sino_rows, out=out)
+
+    def forward_attenuated(self, img_slab: torch.Tensor, mu_slab: torch.Tensor,
+                           out: torch.Tensor | None = None) -> torch.Tensor:
+        """Attenuated transform (N4) of the slab: a horizontal ray never leaves its slab, so its
+        attenuation along the whole ray is the slab's -- no exchange either."""
+        return self.plan.forward_attenuated(img_slab, mu_slab, out=out)
+
+    def adjoint_attenuated(self, sino_rows: torch.Tensor, mu_slab: torch.Tensor,
+                           out: torch.Tensor | None = None) -> torch.Tensor:
+        return self.plan.adjoint_attenuated(sino_rows, mu_slab, out=out)
 
     def gather_image(self, slab: torch.Tensor, nz: int) -> torch.Tensor:
         full = torch.zeros((nz,) + tuple(slab.shape[1:]), dtype=slab.dtype, device=slab.device)

@@ -183,3 +183,24 @@ def test_random_geometries(cuda_ok, beam):
             back = p.adjoint_attenuated(torch.from_numpy(y).reshape(p.sino_shape).cuda(), mu).cpu().numpy().ravel()
             if np.linalg.norm(refb) > 0:
                 assert H.rel_l2(back, refb) <= H.ADJ_TOL, (beam, trial, algo)
+
+
+@pytest.mark.parametrize("idx", [4, 5])
+def test_view_sharding_equivalence(cuda_ok, idx):
+    """Attenuated operators on view shards (the per-rank plans of dist.ShardedPlan, run here on one
+    GPU): forward slabs bitwise equal to the unsharded sinogram, adjoint partials sum to it."""
+    from paper_2006_00686_b200.dist import shard_geometry
+    c = H.small_config(idx)
+    img, mu = _inputs(c)
+    full = Plan(c, device=0)
+    y = workloads.make_sino_input(c, device="cuda")
+    ref_f = full.forward_attenuated(img, mu)
+    ref_b = full.adjoint_attenuated(y, mu)
+    acc = torch.zeros_like(ref_b)
+    for r in range(3):
+        g = shard_geometry(c, r, 3)
+        v0, v1 = g["view_block"]
+        p = Plan(g, device=0)
+        assert torch.equal(p.forward_attenuated(img, mu), ref_f[v0:v1])
+        acc += p.adjoint_attenuated(y[v0:v1].contiguous(), mu)
+    assert H.rel_l2(acc.cpu().numpy(), ref_b.cpu().numpy()) <= 1e-6
