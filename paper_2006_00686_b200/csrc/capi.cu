@@ -441,7 +441,11 @@ xrt_status plan_create_impl(const xrt_geometry* g, int cuda_device, xrt_plan* ou
     if (p->column_ok) {
         p->zpad = column_zpad(g, G);
         p->col_np = xrt::choose_col_np(D.rows);
-        p->col_np_adj = std::getenv("XRT_COL_NP_ADJ") ? std::atoi(std::getenv("XRT_COL_NP_ADJ")) : 1;
+        p->col_np_adj = 1;
+        if (const char* e = std::getenv("XRT_COL_NP_ADJ")) {   // experiments: 1, 2 or 4 pairs per lane
+            const int v = std::atoi(e);
+            if (v == 1 || v == 2 || v == 4) p->col_np_adj = v;
+        }
         p->nzp = (G.n[2] + 2 * p->zpad + 3) / 4 * 4;   // 16-byte cell columns (vector reds); tail rows stay 0
         const size_t bytes = sizeof(float) * (size_t)(G.nxy * p->nzp);
         e = cudaMalloc(&p->d_work_fwd, bytes);

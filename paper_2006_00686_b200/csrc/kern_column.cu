@@ -1406,7 +1406,10 @@ cudaError_t launch_adjoint_att_column(const xrt_plan_s* p, const float* mu_zfast
 // Rays per lane 2 NP, NP in {1, 2}: the fewest idle rows in the last band of 64 NP rows (ties:
 // more rays per lane, i.e. each segment descriptor shared by more rays).
 int choose_col_np(int rows) {
-    if (const char* e = std::getenv("XRT_COL_NP")) return std::atoi(e);   // experiments
+    if (const char* e = std::getenv("XRT_COL_NP")) {   // experiments: 1, 2 or 4 pairs per lane
+        const int v = std::atoi(e);
+        if (v == 1 || v == 2 || v == 4) return v;
+    }
     int best = 1, best_waste = 1 << 30;
     for (int np = 1; np <= 2; ++np) {
         const int per = 64 * np;
