@@ -548,6 +548,7 @@ xrt_status xrt_plan_destroy(xrt_plan p) {
     cudaFree(p->d_work_adj);
     cudaFree(p->d_work_att);
     cudaFree(p->d_att_A);
+    cudaFree(p->d_att_pieces);
     cudaFree(p->d_att_mumax);
     cudaFree(p->ct[0].d_items);
     cudaFree(p->ct[1].d_items);
@@ -642,6 +643,8 @@ static cudaError_t att_alloc(xrt_plan p, bool adjoint) {
         e = cudaMalloc(&p->d_work_att, bytes);
         if (e == cudaSuccess) e = cudaMemset(p->d_work_att, 0, bytes);   // zero padding stays zero
     }
+    if (e == cudaSuccess && !adjoint && !p->d_att_pieces && xrt::att_piece_floats(p) > 0 && !std::getenv("XRT_ATT_UNTILED"))
+        e = cudaMalloc(&p->d_att_pieces, sizeof(float) * (size_t)xrt::att_piece_floats(p));
     if (e == cudaSuccess && adjoint && !p->d_att_A)
         e = cudaMalloc(&p->d_att_A, sizeof(float) * (size_t)(p->n_views * p->det.per_view));
     return e;
@@ -655,7 +658,7 @@ xrt_status xrt_forward_attenuated(xrt_plan p, const float* img, const float* mu,
     if (p->dim == 3 && resolve(p, XRT_OP_FORWARD) == XRT_ALGO_COLUMN) {
         e = att_alloc(p, false);
         if (e == cudaSuccess) e = xrt::launch_att_prepare(p, img, mu, p->d_work_att, p->d_att_mumax, s);
-        if (e == cudaSuccess) e = xrt::launch_forward_att_column(p, p->d_work_att, p->d_att_mumax, sino, s);
+        if (e == cudaSuccess) e = xrt::launch_forward_att_column(p, p->d_work_att, p->d_att_mumax, sino, p->d_att_pieces, s);
         p->launches += 4;
     } else {
         e = xrt::launch_forward_att(p, img, mu, sino, 0, p->n_rays, s);

@@ -674,6 +674,7 @@ __device__ __forceinline__ void column_segments_fwd_att(unsigned seg, int total,
             const float2 ps = att_phi<kExact>(xs, es);
             P[p].acc0 = __ffma2_rn(make_float2(v00.x, v01.x), __fmul2_rn(Ls, ps), __fmul2_rn(P[p].acc0, es));
             const float2 xe = __fmul2_rn(make_float2(v10.y, v11.y), Le);
+            P[p].acc1 = __fadd2_rn(P[p].acc1, __fadd2_rn(xs, xe));   // the piece's attenuation (tiled)
             const float2 pe = att_phi<kExact>(xe, ee);
             P[p].acc0 = __ffma2_rn(make_float2(v10.x, v11.x), __fmul2_rn(Le, pe), __fmul2_rn(P[p].acc0, ee));
         }
@@ -850,6 +851,7 @@ __global__ void __launch_bounds__(kWarps * 32, NP >= 4 ? 2 : (kOp >= 2 ? 2 : (NP
     const long long dacc = kOp == 3 ? (long long)((const char*)volw - (const char*)vol) : 0ll;
     const bool exact = kAtt && (*att_mumax) * att_lmax > 0.125f;
     bool zinit = !tiled;  // untiled: the z state at sigma = 0 is the initial one
+    float sig_piece = 0.f;  // attenuated, tiled: sigma where this tile's piece of the path starts
     const unsigned klo = kMagicBits + (unsigned)L.pad, kn = (unsigned)g.n[2];   // interior z cells
     for (int n0 = na; n0 < nb; n0 += 32 * kPasses) {
         // ---- warp-cooperative: kPasses passes of 32 slices (slice n = n0 + 32 pass + lane) ->
@@ -883,6 +885,7 @@ __global__ void __launch_bounds__(kWarps * 32, NP >= 4 ? 2 : (kOp >= 2 ? 2 : (NP
             if (!zinit) {
                 zinit = true;
                 const float sf = s_first[warp];
+                sig_piece = sf;
 #pragma unroll
                 for (int p = 0; p < NP; ++p) {
                     z_skip(P[p].kpf.x, P[p].dk0, P[p].mz.x, P[p].ntz.x, P[p].ndtz.x, P[p].nt0z.x, sf);
@@ -915,7 +918,19 @@ __global__ void __launch_bounds__(kWarps * 32, NP >= 4 ? 2 : (kOp >= 2 ? 2 : (NP
             const float a = (q & 1) ? Q.acc0.y + Q.acc1.y : Q.acc0.x + Q.acc1.x;
             const float out = kAtt ? ((q & 1) ? Q.acc0.y : Q.acc0.x) : a * ((q & 1) ? Q.w.y : Q.w.x);
             const int64_t m = ((int64_t)v * dc.rows + (band * R + q) * 32 + lane) * dc.cols + c;
-            if (tiled) { if (out != 0.f) red_sino(sino_out + m, out, l2_evict_first()); }
+            if (kAtt && tiled) {
+                // (sigma_start, S_t, A_t) of this tile's piece, slot (ray of the band, tile); the
+                // pieces are combined in path order by k_att_combine (rays that miss the tile keep
+                // the zero slot, which the combine treats as the identity)
+                if (!zinit) continue;
+                const int t = (int)(L.items[it].y >> 16);
+                const int n_ty = (g.n[1] + L.tile - 1) / L.tile;
+                const int64_t rib = ((int64_t)v * (R * 32) + q * 32 + lane) * dc.cols + c;   // ray in band
+                float* slot = volw + 3 * (rib * (L.n_tx * n_ty) + t);
+                slot[0] = sig_piece;
+                slot[1] = out;
+                slot[2] = (q & 1) ? Q.acc1.y : Q.acc1.x;
+            } else if (tiled) { if (out != 0.f) red_sino(sino_out + m, out, l2_evict_first()); }
             else __stcs(sino_out + m, out);
         }
     }
@@ -1381,14 +1396,75 @@ static float att_lmax(const xrt_plan_s* p) {
     return (float)std::sqrt(p->grid.d[0] * p->grid.d[0] + p->grid.d[1] * p->grid.d[1] + p->grid.d[2] * p->grid.d[2]);
 }
 
+namespace {
+// S of every ray of band `band` from its tile pieces: sorted by the piece's start sigma, then
+// S <- S e^-A_t + S_t (the unit recurrence at piece level).  Zero slots (tiles the ray misses) are
+// identities wherever they sort.
+__global__ void k_att_combine(const float* __restrict__ pieces, int n_tiles, int rows_band, int band, DetC dc,
+                              int64_t n_views, float* __restrict__ sino) {
+    const int64_t rib = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t per_view = (int64_t)rows_band * dc.cols;
+    if (rib >= n_views * per_view) return;
+    const int64_t v = rib / per_view;
+    const int64_t rem = rib - v * per_view;
+    const int rr = (int)(rem / dc.cols), c = (int)(rem - (int64_t)rr * dc.cols);
+    const int row = band * rows_band + rr;
+    if (row >= dc.rows) return;
+    float sg[16], S[16], A[16];
+    const int nt = min(n_tiles, 16);
+    for (int t = 0; t < nt; ++t) {
+        const float* q = pieces + 3 * (rib * n_tiles + t);
+        sg[t] = q[0]; S[t] = q[1]; A[t] = q[2];
+    }
+    for (int i = 1; i < nt; ++i)            // insertion sort by sigma (at most a handful of pieces)
+        for (int j = i; j > 0 && sg[j] < sg[j - 1]; --j) {
+            float a = sg[j]; sg[j] = sg[j - 1]; sg[j - 1] = a;
+            a = S[j]; S[j] = S[j - 1]; S[j - 1] = a;
+            a = A[j]; A[j] = A[j - 1]; A[j - 1] = a;
+        }
+    float T = 0.f;
+    for (int t = 0; t < nt; ++t) T = fmaf(T, __expf(-A[t]), S[t]);
+    sino[(v * dc.rows + row) * dc.cols + c] = T;
+}
+}  // namespace
+
 cudaError_t launch_forward_att_column(const xrt_plan_s* p, const float* work2, const unsigned* mumax, float* sino,
-                                      cudaStream_t s) {
+                                      float* pieces, cudaStream_t s) {
     int nblk = 0;
-    ColumnLaunch L = make_launch(p, 0, p->n_views, nblk, false, true);   // untiled: S is not additive over tiles
-    cudaError_t e = cudaMemsetAsync(sino, 0, sizeof(float) * (size_t)(p->n_views * p->det.per_view), s);
-    if (e != cudaSuccess) return e;
-    return launch_column_op<2>(p, work2, nullptr, nullptr, sino, 0, L, nblk, s, nullptr, (const float*)mumax,
-                               att_lmax(p));
+    const xrt_plan_s::ColTiling& T = p->ct[0];
+    if (!T.d_items || !pieces) {
+        // untiled: every ray's whole path in one CTA
+        ColumnLaunch L = make_launch(p, 0, p->n_views, nblk, false, true);
+        cudaError_t e = cudaMemsetAsync(sino, 0, sizeof(float) * (size_t)(p->n_views * p->det.per_view), s);
+        if (e != cudaSuccess) return e;
+        return launch_column_op<2>(p, work2, nullptr, nullptr, sino, 0, L, nblk, s, nullptr, (const float*)mumax,
+                                   att_lmax(p));
+    }
+    // tiled (L2-resident slabs): per band, each tile piece's (sigma, S_t, A_t), then the combine
+    ColumnLaunch L = make_launch(p, 0, p->n_views, nblk, false);
+    const int rb = column_band_rows(p, false), nb = column_bands(p, false);
+    const int n_tiles = T.n_tx * T.n_ty;
+    const int64_t rays_band = p->n_views * (int64_t)rb * p->det.cols;
+    cudaError_t e = cudaSuccess;
+    for (int b = 0; b < nb && e == cudaSuccess; ++b) {
+        e = cudaMemsetAsync(pieces, 0, sizeof(float) * 3 * (size_t)(rays_band * n_tiles), s);
+        L.band0 = b;
+        if (e == cudaSuccess)
+            e = launch_column_op<2>(p, work2, pieces, nullptr, nullptr, 0, L, L.n_items, s, nullptr,
+                                    (const float*)mumax, att_lmax(p));
+        if (e == cudaSuccess) {
+            k_att_combine<<<(unsigned)((rays_band + 255) / 256), 256, 0, s>>>(pieces, n_tiles, rb, b, p->det,
+                                                                            p->n_views, sino);
+            e = cudaGetLastError();
+        }
+    }
+    return e;
+}
+
+int64_t att_piece_floats(const xrt_plan_s* p) {
+    const xrt_plan_s::ColTiling& T = p->ct[0];
+    if (!T.d_items) return 0;
+    return 3 * p->n_views * (int64_t)column_band_rows(p, false) * p->det.cols * T.n_tx * T.n_ty;
 }
 
 cudaError_t launch_adjoint_att_column(const xrt_plan_s* p, const float* mu_zfast, float* sinoA,

@@ -235,6 +235,7 @@ struct xrt_plan_s {
     // attenuated operators on the column path (allocated on first use)
     float* d_work_att = nullptr;       // z-fastest float2 (f, mu) cells
     float* d_att_A = nullptr;          // per-ray total attenuation (sinogram-shaped)
+    float* d_att_pieces = nullptr;     // tiled attenuated forward: (sigma, S_t, A_t) per ray of a band and tile
     unsigned* d_att_mumax = nullptr;   // max |mu| (float bits)
     void* d_coldesc = nullptr;         // per-(view, column) path descriptors (COLUMN, GATHER)
     double* d_rays = nullptr;          // explicit ray list (XRT_RAYS)
@@ -267,7 +268,8 @@ cudaError_t launch_adjoint_att(const xrt_plan_s* p, const float* sino, const flo
 cudaError_t launch_att_prepare(const xrt_plan_s* p, const float* img, const float* mu, float* work2,
                                unsigned* mumax, cudaStream_t s);
 cudaError_t launch_forward_att_column(const xrt_plan_s* p, const float* work2, const unsigned* mumax, float* sino,
-                                      cudaStream_t s);
+                                      float* pieces, cudaStream_t s);
+int64_t att_piece_floats(const xrt_plan_s* p);
 cudaError_t launch_adjoint_att_column(const xrt_plan_s* p, const float* mu_zfast, float* sinoA,
                                       const unsigned* mumax, const float* y, float* acc_zfast, cudaStream_t s);
 cudaError_t launch_forward64(const xrt_plan_s* p, const double* img, double* sino, int64_t ray0,

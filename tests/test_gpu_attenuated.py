@@ -204,3 +204,26 @@ def test_view_sharding_equivalence(cuda_ok, idx):
         assert torch.equal(p.forward_attenuated(img, mu), ref_f[v0:v1])
         acc += p.adjoint_attenuated(y[v0:v1].contiguous(), mu)
     assert H.rel_l2(acc.cpu().numpy(), ref_b.cpu().numpy()) <= 1e-6
+
+
+@pytest.mark.parametrize("idx", [4, 5])
+def test_tiled_pieces_combine(cuda_ok, idx, monkeypatch):
+    """Forced xy tiling (XRT_COLUMN_TILE=16 at plan creation): the attenuated forward runs per tile
+    piece, (sigma, S_t, A_t), and combines the pieces in path order -- against the oracle and the
+    RAY kernel (no tiling) on the whole sinogram."""
+    c = H.small_config(idx)
+    monkeypatch.setenv("XRT_COLUMN_TILE", "16")
+    pt = Plan(c, device=0)
+    monkeypatch.delenv("XRT_COLUMN_TILE")
+    pr = _plan(c, "ray")
+    img, mu = _inputs(c)
+    for scale in (1.0, 40.0):
+        m = (mu * scale).contiguous()
+        a = pt.forward_attenuated(img, m).cpu().numpy().ravel()
+        if scale == 1.0:   # (at x40 both kernels sit near the bar from opposite sides: oracle only)
+            b = pr.forward_attenuated(img, m).cpu().numpy().ravel()
+            assert H.fwd_err(a, b) <= H.FWD_TOL, scale
+        ids = workloads.sample_rays(c, 200, seed=950 + idx)
+        pp, th = G.rays(c, ids)
+        ref = oracle.forward_attenuated(c, img.cpu().numpy().ravel(), m.cpu().numpy().ravel(), pp, th)
+        assert H.fwd_err(a[ids], ref) <= H.FWD_TOL, scale
