@@ -674,14 +674,21 @@ xrt_status xrt_adjoint_attenuated(xrt_plan p, const float* sino, const float* mu
     cudaStream_t s = (cudaStream_t)cuda_stream;
     cudaError_t e;
     if (p->dim == 3 && resolve(p, XRT_OP_ADJOINT) == XRT_ALGO_COLUMN) {
-        // mu z-fastest in work_fwd; pass 1: each ray's total attenuation A (plain forward of mu),
-        // pass 2 reduces y e^-(A - A_le) L phi into work_adj
-        e = att_alloc(p, true);
+        // mu z-fastest in work_fwd; tiled plans: per band, the pieces' attenuation A_t (the plain
+        // forward of mu per piece), their suffix sums B_t, then the scatter y e^-(B_t - A_le) L phi
+        // with A_le from each piece's start; untiled: A = X mu per ray, then the untiled scatter
+        const bool tiled = p->ct[0].d_items && !std::getenv("XRT_ATT_UNTILED");
+        e = att_alloc(p, !tiled);
         if (e == cudaSuccess) e = xrt::launch_to_zfast(p, mu, p->d_work_fwd, s);
         if (e == cudaSuccess) e = xrt::launch_att_prepare(p, nullptr, mu, nullptr, p->d_att_mumax, s);
         if (e == cudaSuccess) e = cudaMemsetAsync(p->d_work_adj, 0, sizeof(float) * (size_t)(p->grid.nxy * p->nzp), s);
-        if (e == cudaSuccess)
+        if (tiled) {
+            if (e == cudaSuccess)
+                e = xrt::launch_adjoint_att_tiled(p, p->d_work_fwd, p->d_att_pieces, p->d_att_mumax, sino,
+                                                  p->d_work_adj, s);
+        } else if (e == cudaSuccess) {
             e = xrt::launch_adjoint_att_column(p, p->d_work_fwd, p->d_att_A, p->d_att_mumax, sino, p->d_work_adj, s);
+        }
         if (e == cudaSuccess) e = xrt::launch_from_zfast(p, p->d_work_adj, img, s);
         p->launches += 5;
     } else {

@@ -827,9 +827,16 @@ __global__ void __launch_bounds__(kWarps * 32, NP >= 4 ? 2 : (kOp >= 2 ? 2 : (NP
         const float ya = (kAdjoint && Za.active) ? ld_stream(sino_in + ((int64_t)v * dc.rows + ra) * dc.cols + c, l2_evict_first()) : 0.f;
         const float yb = (kAdjoint && Zb.active) ? ld_stream(sino_in + ((int64_t)v * dc.rows + rb) * dc.cols + c, l2_evict_first()) : 0.f;
         pair_init(P[p], Za, Zb, ya, yb, kAdjoint);
-        if (kOp == 3) {   // the ray's total attenuation (plain forward of mu)
+        if (kOp == 3 && !tiled) {   // the ray's total attenuation (plain forward of mu)
             P[p].acc1 = make_float2(Za.active ? sino_aux[((int64_t)v * dc.rows + ra) * dc.cols + c] : 0.f,
                                     Zb.active ? sino_aux[((int64_t)v * dc.rows + rb) * dc.cols + c] : 0.f);
+        } else if (kOp == 3) {      // tiled: the attenuation from this tile's piece to the ray's end
+            const int t = (int)(L.items[it].y >> 16);
+            const int ntile = L.n_tx * ((g.n[1] + L.tile - 1) / L.tile);
+            const int64_t ia = ((int64_t)v * (R * 32) + 2 * p * 32 + lane) * dc.cols + c;
+            const int64_t ib = ia + 32 * (int64_t)dc.cols;
+            P[p].acc1 = make_float2(Za.active ? sino_aux[3 * (ia * ntile + t) + 2] : 0.f,
+                                    Zb.active ? sino_aux[3 * (ib * ntile + t) + 2] : 0.f);
         }
         any_live |= P[p].live0 | P[p].live1;
         pos &= Za.dk >= 0 && Zb.dk >= 0;
@@ -918,7 +925,10 @@ __global__ void __launch_bounds__(kWarps * 32, NP >= 4 ? 2 : (kOp >= 2 ? 2 : (NP
             const float a = (q & 1) ? Q.acc0.y + Q.acc1.y : Q.acc0.x + Q.acc1.x;
             const float out = kAtt ? ((q & 1) ? Q.acc0.y : Q.acc0.x) : a * ((q & 1) ? Q.w.y : Q.w.x);
             const int64_t m = ((int64_t)v * dc.rows + (band * R + q) * 32 + lane) * dc.cols + c;
-            if (kAtt && tiled) {
+            if ((kAtt || volw != nullptr) && tiled) {
+                // kOp 2: the attenuated piece (sigma, S_t, A_t); kOp 0 with volw = a pieces buffer:
+                // the plain forward of mu per piece, (sigma, -, A_t) -- pass 1 of the tiled
+                // attenuated adjoint
                 // (sigma_start, S_t, A_t) of this tile's piece, slot (ray of the band, tile); the
                 // pieces are combined in path order by k_att_combine (rays that miss the tile keep
                 // the zero slot, which the combine treats as the identity)
@@ -928,8 +938,12 @@ __global__ void __launch_bounds__(kWarps * 32, NP >= 4 ? 2 : (kOp >= 2 ? 2 : (NP
                 const int64_t rib = ((int64_t)v * (R * 32) + q * 32 + lane) * dc.cols + c;   // ray in band
                 float* slot = volw + 3 * (rib * (L.n_tx * n_ty) + t);
                 slot[0] = sig_piece;
-                slot[1] = out;
-                slot[2] = (q & 1) ? Q.acc1.y : Q.acc1.x;
+                if (kAtt) {
+                    slot[1] = out;
+                    slot[2] = (q & 1) ? Q.acc1.y : Q.acc1.x;
+                } else {
+                    slot[2] = out;
+                }
             } else if (tiled) { if (out != 0.f) red_sino(sino_out + m, out, l2_evict_first()); }
             else __stcs(sino_out + m, out);
         }
@@ -1269,11 +1283,12 @@ ColumnLaunch make_launch(const xrt_plan_s* p, int64_t v0, int64_t v1, int& nblk,
 template <int kOp>
 cudaError_t launch_column_op(const xrt_plan_s* p, const float* vol, float* volw, const float* sino_in,
                              float* sino_out, int64_t v0, const ColumnLaunch& L, int nblk, cudaStream_t s,
-                             const float* sino_aux = nullptr, const float* att_mumax = nullptr, float att_lmax = 0.f) {
+                             const float* sino_aux = nullptr, const float* att_mumax = nullptr, float att_lmax = 0.f,
+                             int np_override = 0) {
     constexpr bool kAdj = kOp == 1 || kOp == 3;
     const ColDesc* d = (const ColDesc*)p->d_coldesc;
     if (nblk <= 0) return cudaSuccess;
-    const int np = kAdj ? p->col_np_adj : p->col_np;
+    const int np = np_override ? np_override : (kAdj ? p->col_np_adj : p->col_np);
     if (np == 1)
         k_column<kOp, 1><<<nblk, kWarps * 32, 0, s>>>(p->d_views, p->det, p->grid, vol, volw, sino_in, sino_out, (int)v0, d, L,
                                                       sino_aux, att_mumax, att_lmax);
@@ -1465,6 +1480,65 @@ int64_t att_piece_floats(const xrt_plan_s* p) {
     const xrt_plan_s::ColTiling& T = p->ct[0];
     if (!T.d_items) return 0;
     return 3 * p->n_views * (int64_t)column_band_rows(p, false) * p->det.cols * T.n_tx * T.n_ty;
+}
+
+namespace {
+// per ray of a band: the pieces' (sigma, A_t) in path order -> slot[2] = B_t = sum of A over this
+// piece and the later ones (the attenuation from the piece's start to the ray's end)
+__global__ void k_att_suffix(float* __restrict__ pieces, int n_tiles, int64_t rays_band) {
+    const int64_t rib = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (rib >= rays_band) return;
+    float sg[16], A[16];
+    int id[16];
+    const int nt = min(n_tiles, 16);
+    for (int t = 0; t < nt; ++t) {
+        sg[t] = pieces[3 * (rib * n_tiles + t)];
+        A[t] = pieces[3 * (rib * n_tiles + t) + 2];
+        id[t] = t;
+    }
+    for (int i = 1; i < nt; ++i)
+        for (int j = i; j > 0 && sg[j] < sg[j - 1]; --j) {
+            float a = sg[j]; sg[j] = sg[j - 1]; sg[j - 1] = a;
+            a = A[j]; A[j] = A[j - 1]; A[j - 1] = a;
+            const int k = id[j]; id[j] = id[j - 1]; id[j - 1] = k;
+        }
+    float B = 0.f;
+    for (int t = nt - 1; t >= 0; --t) {
+        B += A[t];
+        pieces[3 * (rib * n_tiles + id[t]) + 2] = B;
+    }
+}
+}  // namespace
+
+// tiled attenuated adjoint: per band, pass 1 = the plain forward of mu per piece, (sigma, -, A_t),
+// the suffix sums B_t, then the scatter with A_le running from each piece's start
+cudaError_t launch_adjoint_att_tiled(const xrt_plan_s* p, const float* mu_zfast, float* pieces,
+                                     const unsigned* mumax, const float* y, float* acc_zfast, cudaStream_t s) {
+    const xrt_plan_s::ColTiling& T = p->ct[0];
+    if (!T.d_items) return cudaErrorNotSupported;
+    // both passes on the forward's tiles, bands and rays per lane (the pieces' layout)
+    const int rbf = column_band_rows(p, false);
+    int nblk = 0;
+    ColumnLaunch Lf = make_launch(p, 0, p->n_views, nblk, false);
+    ColumnLaunch La = Lf;
+    const int nb = column_bands(p, false);
+    const int n_tiles = T.n_tx * T.n_ty;
+    const int64_t rays_band = p->n_views * (int64_t)rbf * p->det.cols;
+    cudaError_t e = cudaSuccess;
+    for (int b = 0; b < nb && e == cudaSuccess; ++b) {
+        e = cudaMemsetAsync(pieces, 0, sizeof(float) * 3 * (size_t)(rays_band * n_tiles), s);
+        Lf.band0 = La.band0 = b;
+        if (e == cudaSuccess)
+            e = launch_column_op<0>(p, mu_zfast, pieces, nullptr, nullptr, 0, Lf, Lf.n_items, s);
+        if (e == cudaSuccess) {
+            k_att_suffix<<<(unsigned)((rays_band + 255) / 256), 256, 0, s>>>(pieces, n_tiles, rays_band);
+            e = cudaGetLastError();
+        }
+        if (e == cudaSuccess)
+            e = launch_column_op<3>(p, mu_zfast, acc_zfast, y, nullptr, 0, La, La.n_items, s, pieces,
+                                    (const float*)mumax, att_lmax(p), p->col_np);
+    }
+    return e;
 }
 
 cudaError_t launch_adjoint_att_column(const xrt_plan_s* p, const float* mu_zfast, float* sinoA,

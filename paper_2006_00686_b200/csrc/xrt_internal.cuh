@@ -270,6 +270,8 @@ cudaError_t launch_att_prepare(const xrt_plan_s* p, const float* img, const floa
 cudaError_t launch_forward_att_column(const xrt_plan_s* p, const float* work2, const unsigned* mumax, float* sino,
                                       float* pieces, cudaStream_t s);
 int64_t att_piece_floats(const xrt_plan_s* p);
+cudaError_t launch_adjoint_att_tiled(const xrt_plan_s* p, const float* mu_zfast, float* pieces,
+                                     const unsigned* mumax, const float* y, float* acc_zfast, cudaStream_t s);
 cudaError_t launch_adjoint_att_column(const xrt_plan_s* p, const float* mu_zfast, float* sinoA,
                                       const unsigned* mumax, const float* y, float* acc_zfast, cudaStream_t s);
 cudaError_t launch_forward64(const xrt_plan_s* p, const double* img, double* sino, int64_t ray0,

@@ -227,3 +227,14 @@ def test_tiled_pieces_combine(cuda_ok, idx, monkeypatch):
         pp, th = G.rays(c, ids)
         ref = oracle.forward_attenuated(c, img.cpu().numpy().ravel(), m.cpu().numpy().ravel(), pp, th)
         assert H.fwd_err(a[ids], ref) <= H.FWD_TOL, scale
+    # the tiled adjoint (pieces' suffix attenuation) against the oracle's scatter on a ray sample
+    ids = workloads.sample_rays(c, 300, seed=960 + idx)
+    y_full = workloads.make_sino_input(c).numpy().ravel()
+    y = np.zeros_like(y_full)
+    y[ids] = y_full[ids]
+    pp, th = G.rays(c, ids)
+    for scale in (1.0, 40.0):
+        m = (mu * scale).contiguous()
+        back = pt.adjoint_attenuated(torch.from_numpy(y).reshape(pt.sino_shape).cuda(), m).cpu().numpy().ravel()
+        refb = oracle.adjoint_attenuated(c, y[ids], m.cpu().numpy().ravel(), pp, th)
+        assert H.rel_l2(back, refb) <= H.ADJ_TOL, scale
