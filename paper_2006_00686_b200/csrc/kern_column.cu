@@ -748,7 +748,8 @@ __device__ __forceinline__ void att_walk(unsigned seg, int total, RayPair (&P)[N
 #define XRT_COL_MINB 3
 #endif
 
-// kOp: 0 forward, 1 adjoint, 2 attenuated forward, 3 attenuated adjoint (N4)
+// kOp: 0 forward, 1 adjoint, 2 attenuated forward, 3 attenuated adjoint (N4), 4 the forward per tile
+// piece (pass 1 of the tiled attenuated adjoint)
 template <int kOp, int NP>
 #ifndef XRT_COL_MINB_ADJ1
 #define XRT_COL_MINB_ADJ1 4    // adjoint, 1 pair per lane: 64 registers, 4 CTAs / SM (measured faster than 3)
@@ -756,7 +757,7 @@ template <int kOp, int NP>
 #ifndef XRT_COL_MINB_FWD1
 #define XRT_COL_MINB_FWD1 3
 #endif
-__global__ void __launch_bounds__(kWarps * 32, NP >= 4 ? 2 : (kOp >= 2 ? 2 : (NP == 1 ? (kOp == 1 ? XRT_COL_MINB_ADJ1 : XRT_COL_MINB_FWD1) : XRT_COL_MINB))) k_column(const ViewRec* __restrict__ views, DetC dc, GridC g,
+__global__ void __launch_bounds__(kWarps * 32, NP >= 4 ? 2 : ((kOp == 2 || kOp == 3) ? 2 : (NP == 1 ? (kOp == 1 ? XRT_COL_MINB_ADJ1 : XRT_COL_MINB_FWD1) : XRT_COL_MINB))) k_column(const ViewRec* __restrict__ views, DetC dc, GridC g,
                                                        const float* __restrict__ vol, float* __restrict__ volw,
                                                        const float* __restrict__ sino_in,
                                                        float* __restrict__ sino_out, int view0,
@@ -764,7 +765,7 @@ __global__ void __launch_bounds__(kWarps * 32, NP >= 4 ? 2 : (kOp >= 2 ? 2 : (NP
                                                        const float* __restrict__ sino_aux, const float* __restrict__ att_mumax,
                                                        float att_lmax) {
     constexpr bool kAdjoint = kOp == 1 || kOp == 3;
-    constexpr bool kAtt = kOp >= 2;
+    constexpr bool kAtt = kOp == 2 || kOp == 3;
     constexpr int R = 2 * NP;
     __shared__ Seg s_seg[kWarps][2 * 32 * kPasses];
     __shared__ float s_first[kWarps];
@@ -925,10 +926,9 @@ __global__ void __launch_bounds__(kWarps * 32, NP >= 4 ? 2 : (kOp >= 2 ? 2 : (NP
             const float a = (q & 1) ? Q.acc0.y + Q.acc1.y : Q.acc0.x + Q.acc1.x;
             const float out = kAtt ? ((q & 1) ? Q.acc0.y : Q.acc0.x) : a * ((q & 1) ? Q.w.y : Q.w.x);
             const int64_t m = ((int64_t)v * dc.rows + (band * R + q) * 32 + lane) * dc.cols + c;
-            if ((kAtt || volw != nullptr) && tiled) {
-                // kOp 2: the attenuated piece (sigma, S_t, A_t); kOp 0 with volw = a pieces buffer:
-                // the plain forward of mu per piece, (sigma, -, A_t) -- pass 1 of the tiled
-                // attenuated adjoint
+            if ((kAtt || kOp == 4) && tiled) {
+                // kOp 2: the attenuated piece (sigma, S_t, A_t); kOp 4 (the plain forward with volw =
+                // the pieces buffer): (sigma, -, A_t) of mu -- pass 1 of the tiled attenuated adjoint
                 // (sigma_start, S_t, A_t) of this tile's piece, slot (ray of the band, tile); the
                 // pieces are combined in path order by k_att_combine (rays that miss the tile keep
                 // the zero slot, which the combine treats as the identity)
@@ -1529,7 +1529,7 @@ cudaError_t launch_adjoint_att_tiled(const xrt_plan_s* p, const float* mu_zfast,
         e = cudaMemsetAsync(pieces, 0, sizeof(float) * 3 * (size_t)(rays_band * n_tiles), s);
         Lf.band0 = La.band0 = b;
         if (e == cudaSuccess)
-            e = launch_column_op<0>(p, mu_zfast, pieces, nullptr, nullptr, 0, Lf, Lf.n_items, s);
+            e = launch_column_op<4>(p, mu_zfast, pieces, nullptr, nullptr, 0, Lf, Lf.n_items, s);
         if (e == cudaSuccess) {
             k_att_suffix<<<(unsigned)((rays_band + 255) / 256), 256, 0, s>>>(pieces, n_tiles, rays_band);
             e = cudaGetLastError();
