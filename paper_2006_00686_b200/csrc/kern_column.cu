@@ -53,7 +53,7 @@ namespace xrt {
 namespace {
 
 #ifndef XRT_COL_WARPS
-#define XRT_COL_WARPS 8
+#define XRT_COL_WARPS 4   // measured: 4 columns per CTA 0.5-2 % faster than 8 on cfg 3 / 4 / 5, 2 slower
 #endif
 constexpr int kWarps = XRT_COL_WARPS;  // warps per CTA = adjacent detector columns per CTA (one per warp)
 #ifndef XRT_KPASSES
@@ -747,20 +747,23 @@ __device__ __forceinline__ void att_walk(unsigned seg, int total, RayPair (&P)[N
 // slice, warp scan, segments in its own shared-memory buffer; no CTA barrier) and walks it for its
 // 2 NP rays per lane (rows band*64NP + 32q + lane: adjacent rows in adjacent lanes, so the lanes'
 // loads of one segment fall on consecutive addresses of the z-fastest volume).
+// Occupancy targets as resident threads per SM (the launch bounds' minimum CTAs = threads / CTA size):
+// 2 pairs per lane 768 (80 registers), adjoint with 1 pair 1024 (64 registers), forward with 1 pair
+// 768, attenuated and 4-pair kernels 512.
 #ifndef XRT_COL_MINB
-#define XRT_COL_MINB 3
+#define XRT_COL_MINB (768 / (32 * XRT_COL_WARPS))
 #endif
 
 // kOp: 0 forward, 1 adjoint, 2 attenuated forward, 3 attenuated adjoint (N4), 4 the forward per tile
 // piece (pass 1 of the tiled attenuated adjoint)
 template <int kOp, int NP>
 #ifndef XRT_COL_MINB_ADJ1
-#define XRT_COL_MINB_ADJ1 4    // adjoint, 1 pair per lane: 64 registers, 4 CTAs / SM (measured faster than 3)
+#define XRT_COL_MINB_ADJ1 (1024 / (32 * XRT_COL_WARPS))   // measured faster than 768
 #endif
 #ifndef XRT_COL_MINB_FWD1
-#define XRT_COL_MINB_FWD1 3
+#define XRT_COL_MINB_FWD1 (768 / (32 * XRT_COL_WARPS))
 #endif
-__global__ void __launch_bounds__(kWarps * 32, NP >= 4 ? 2 : ((kOp == 2 || kOp == 3) ? 2 : (NP == 1 ? (kOp == 1 ? XRT_COL_MINB_ADJ1 : XRT_COL_MINB_FWD1) : XRT_COL_MINB))) k_column(const ViewRec* __restrict__ views, DetC dc, GridC g,
+__global__ void __launch_bounds__(kWarps * 32, NP >= 4 ? 512 / (32 * kWarps) : ((kOp == 2 || kOp == 3) ? 512 / (32 * kWarps) : (NP == 1 ? (kOp == 1 ? XRT_COL_MINB_ADJ1 : XRT_COL_MINB_FWD1) : XRT_COL_MINB))) k_column(const ViewRec* __restrict__ views, DetC dc, GridC g,
                                                        const float* __restrict__ vol, float* __restrict__ volw,
                                                        const float* __restrict__ sino_in,
                                                        float* __restrict__ sino_out, int view0,
