@@ -39,12 +39,15 @@
  *
  * Ownership: every image / sinogram / CSR buffer is caller-allocated device memory (e.g. a torch
  * tensor's data_ptr()) unless the function name ends in _host.  The plan owns only its geometry
- * tables and internal workspace (allocated at create time; the _host entry points additionally
- * allocate staging buffers on first use).  Nothing returned to the caller is library-allocated.
+ * tables and internal workspace (allocated at create time; the _host and _attenuated entry
+ * points additionally allocate staging / attenuation buffers on first use).  Nothing returned to
+ * the caller is library-allocated.
  *
  * Asynchrony: functions taking a cuda_stream enqueue on that stream (NULL = legacy default stream)
  * and return; kernel faults surface as XRT_ERR_CUDA from a later call.  Functions that return a
  * host-side count (xrt_ray_units' nnz_out, xrt_plan_query's n_units) synchronise the stream.
+ * Concurrency: calls on one plan share its workspace, so they must be ordered (one stream, or
+ * streams the caller serialises); independent plans may run concurrently on different streams.
  *
  * Errors: every function returns an xrt_status; on a non-OK status xrt_last_error() returns a
  * thread-local human-readable message.  Invalid arguments never launch work.

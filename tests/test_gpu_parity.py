@@ -608,3 +608,31 @@ def test_degenerate_grids(cuda_ok, beam, n):
         if np.linalg.norm(refb) > 0:
             assert H.rel_l2(back, refb) <= H.ADJ_TOL, (beam, n, algo)
         assert torch.count_nonzero(p.adjoint(torch.zeros(p.sino_shape, device="cuda"))) == 0
+
+
+@pytest.mark.parametrize("idx", [2, 4])
+def test_user_streams(cuda_ok, idx):
+    """Every entry point enqueues on the caller's stream (xrt.h): results on two side streams, two
+    plans running concurrently, equal the default-stream results bitwise."""
+    c = H.small_config(idx)
+    p1, p2 = Plan(c, device=0), Plan(c, device=0)
+    img = _image(c)
+    mu = workloads.make_attenuation(c, device="cuda")
+    y = workloads.make_sino_input(c, device="cuda")
+    ref = [p1.forward(img), p1.adjoint(y), p1.forward_attenuated(img, mu), p1.adjoint_attenuated(y, mu)]
+    torch.cuda.synchronize()
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    s1.wait_stream(torch.cuda.current_stream())
+    s2.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s1):
+        r1 = [p1.forward(img, stream=s1), p1.adjoint(y, stream=s1),
+              p1.forward_attenuated(img, mu, stream=s1), p1.adjoint_attenuated(y, mu, stream=s1)]
+    with torch.cuda.stream(s2):
+        r2 = [p2.forward(img, stream=s2), p2.adjoint(y, stream=s2),
+              p2.forward_attenuated(img, mu, stream=s2), p2.adjoint_attenuated(y, mu, stream=s2)]
+    torch.cuda.synchronize()
+    for a, b, r in zip(r1, r2, ref):
+        # forwards are deterministic (bitwise); adjoints reduce with atomics (last-bit order effects)
+        assert H.rel_l2(a.cpu().numpy(), r.cpu().numpy()) <= 1e-6
+        assert H.rel_l2(b.cpu().numpy(), r.cpu().numpy()) <= 1e-6
+    assert torch.equal(r1[0], ref[0]) and torch.equal(r2[0], ref[0])
