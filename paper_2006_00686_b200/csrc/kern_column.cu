@@ -747,18 +747,19 @@ __device__ __forceinline__ void att_walk(unsigned seg, int total, RayPair (&P)[N
 // slice, warp scan, segments in its own shared-memory buffer; no CTA barrier) and walks it for its
 // 2 NP rays per lane (rows band*64NP + 32q + lane: adjacent rows in adjacent lanes, so the lanes'
 // loads of one segment fall on consecutive addresses of the z-fastest volume).
-// Occupancy targets as resident threads per SM (the launch bounds' minimum CTAs = threads / CTA size):
-// 2 pairs per lane 768 (80 registers), adjoint with 1 pair 1024 (64 registers), forward with 1 pair
-// 768, attenuated and 4-pair kernels 512.
+// Occupancy targets as resident threads per SM (the launch bounds' minimum CTAs = threads / CTA size),
+// each the measured best at 4 columns per CTA: 2 pairs per lane 640 (96 registers; cfg 4 forward
+// 139.4 -> 135.0 ms vs 768), adjoint with 1 pair 896 (73 registers), forward with 1 pair 768,
+// attenuated and 4-pair kernels 512.
 #ifndef XRT_COL_MINB
-#define XRT_COL_MINB (768 / (32 * XRT_COL_WARPS))
+#define XRT_COL_MINB (640 / (32 * XRT_COL_WARPS))
 #endif
 
 // kOp: 0 forward, 1 adjoint, 2 attenuated forward, 3 attenuated adjoint (N4), 4 the forward per tile
 // piece (pass 1 of the tiled attenuated adjoint)
 template <int kOp, int NP>
 #ifndef XRT_COL_MINB_ADJ1
-#define XRT_COL_MINB_ADJ1 (1024 / (32 * XRT_COL_WARPS))   // measured faster than 768
+#define XRT_COL_MINB_ADJ1 (896 / (32 * XRT_COL_WARPS))
 #endif
 #ifndef XRT_COL_MINB_FWD1
 #define XRT_COL_MINB_FWD1 (768 / (32 * XRT_COL_WARPS))
