@@ -515,6 +515,11 @@ __device__ __forceinline__ void z_step(RayPair& P, const float2 se2, float2& cr,
 // immediate offset; DK = 0: per-ray offsets.  Software-pipelined one segment deep: the z state
 // decides the next segment's cells before this segment's arithmetic, so the next loads are in
 // flight while this segment's values are consumed.
+#ifndef XRT_FWD_UNROLL
+#define XRT_FWD_UNROLL 2
+#endif
+constexpr int kFwdUnroll = XRT_FWD_UNROLL;
+
 template <int NP, int DK>
 __device__ __forceinline__ void column_segments_fwd(unsigned seg, int total, RayPair (&P)[NP]) {
     const float2 m1 = make_float2(-1.f, -1.f);
@@ -528,7 +533,7 @@ __device__ __forceinline__ void column_segments_fwd(unsigned seg, int total, Ray
         f0[p] = make_float2(__ldg(a0), __ldg(a1));
         f1[p] = make_float2(__ldg(a0 + o0), __ldg(a1 + o1));
     }
-#pragma unroll 2
+#pragma unroll kFwdUnroll
     for (int s = 0; s < total; ++s) {
         const float qse = __uint_as_float(raw.z), qds = __uint_as_float(raw.w);
         const float2 se2 = make_float2(qse, qse), ds2 = make_float2(qds, qds);
