@@ -763,13 +763,16 @@ __device__ __forceinline__ void att_walk(unsigned seg, int total, RayPair (&P)[N
 // kOp: 0 forward, 1 adjoint, 2 attenuated forward, 3 attenuated adjoint (N4), 4 the forward per tile
 // piece (pass 1 of the tiled attenuated adjoint)
 template <int kOp, int NP>
+#ifndef XRT_ATT_THREADS
+#define XRT_ATT_THREADS 896   // attenuated kernels: cfg 4 forward 344.5 -> 304.5 ms, adjoint 738.8 -> 626.6 ms vs 512
+#endif
 #ifndef XRT_COL_MINB_ADJ1
 #define XRT_COL_MINB_ADJ1 (896 / (32 * XRT_COL_WARPS))
 #endif
 #ifndef XRT_COL_MINB_FWD1
 #define XRT_COL_MINB_FWD1 (768 / (32 * XRT_COL_WARPS))
 #endif
-__global__ void __launch_bounds__(kWarps * 32, NP >= 4 ? 512 / (32 * kWarps) : ((kOp == 2 || kOp == 3) ? 512 / (32 * kWarps) : (NP == 1 ? (kOp == 1 ? XRT_COL_MINB_ADJ1 : XRT_COL_MINB_FWD1) : XRT_COL_MINB))) k_column(const ViewRec* __restrict__ views, DetC dc, GridC g,
+__global__ void __launch_bounds__(kWarps * 32, NP >= 4 ? 512 / (32 * kWarps) : ((kOp == 2 || kOp == 3) ? XRT_ATT_THREADS / (32 * kWarps) : (NP == 1 ? (kOp == 1 ? XRT_COL_MINB_ADJ1 : XRT_COL_MINB_FWD1) : XRT_COL_MINB))) k_column(const ViewRec* __restrict__ views, DetC dc, GridC g,
                                                        const float* __restrict__ vol, float* __restrict__ volw,
                                                        const float* __restrict__ sino_in,
                                                        float* __restrict__ sino_out, int view0,
