@@ -182,8 +182,11 @@ xrt_status xrt_adjoint_f64(xrt_plan p, const double* sino, double* img, void* cu
  * mu = 0 everywhere gives xrt_forward.  The adjoint is img_I = sum_m y_m exp(-A_mI) g(mu_I, l_mI).
  *   img, mu, sino: device fp32, layouts as xrt_forward (mu read only, same shape as img); the
  *   output is fully overwritten.  mu in physical 1/length (any finite value; mu >= 0 physically).
- * One thread per ray (RAY family), every geometry including ray lists; fp32 arithmetic, the
- * attenuation running product in path order.  Errors: XRT_ERR_INVALID_ARG on NULL pointers. */
+ * Kernels: on the 3D beams the column path (AUTO) walks each ray's units in path order, per band
+ * of detector rows and xy tile (L2-resident), and combines a ray's tile pieces in path order
+ * (S <- S exp(-A_t) + S_t); tilings of more than 16 tiles run untiled.  2D beams, ray lists and
+ * steep rays: one thread per ray (RAY family).  fp32 arithmetic, the attenuation running product
+ * in path order.  Errors: XRT_ERR_INVALID_ARG on NULL pointers. */
 xrt_status xrt_forward_attenuated(xrt_plan p, const float* img, const float* mu, float* sino,
                                   void* cuda_stream);
 xrt_status xrt_adjoint_attenuated(xrt_plan p, const float* sino, const float* mu, float* img,

@@ -234,7 +234,7 @@ xrt_status fwd_prepare(xrt_plan p, const float* img, cudaStream_t s) {
         if (e != cudaSuccess) return cuda_fail(e, "transpose launch");
         return XRT_OK;
     }
-    cudaError_t e = xrt::launch_to_zfast(p, img, p->d_work_fwd, s);
+    cudaError_t e = p->fd_forward ? xrt::launch_to_fd(p, img, p->d_work_fd, s) : xrt::launch_to_zfast(p, img, p->d_work_fwd, s);
     p->launches += 1;
     if (e != cudaSuccess) return cuda_fail(e, "transpose launch");
     return XRT_OK;
@@ -250,6 +250,9 @@ xrt_status forward_range(xrt_plan p, const float* img, float* sino, int64_t v0, 
     } else if (algo == XRT_ALGO_COLUMN && p->dim == 2) {
         if (!(v0 == 0 && v1 == p->n_views)) return fail(XRT_ERR_UNSUPPORTED, "2D slice kernels run all views at once");
         e = xrt::launch_slice2d(p, false, img, p->d_img_t, nullptr, sino, nullptr, nullptr, s);
+    } else if (algo == XRT_ALGO_COLUMN && p->fd_forward) {
+        if (!(v0 == 0 && v1 == p->n_views)) return fail(XRT_ERR_UNSUPPORTED, "column forward runs all views at once");
+        e = xrt::launch_forward_fd_bands(p, p->d_work_fd, sino, 0, xrt::column_bands(p, false), s);
     } else if (algo == XRT_ALGO_COLUMN) {
         e = xrt::launch_forward_column(p, p->d_work_fwd, sino, v0, v1, s);
     } else {
@@ -442,15 +445,23 @@ xrt_status plan_create_impl(const xrt_geometry* g, int cuda_device, xrt_plan* ou
         p->zpad = column_zpad(g, G);
         p->col_np = xrt::choose_col_np(D.rows);
         p->col_np_adj = 1;
-        if (const char* e = std::getenv("XRT_COL_NP_ADJ")) {   // experiments: 1, 2 or 4 pairs per lane
+        if (const char* e = std::getenv("XRT_COL_NP_ADJ")) {   // experiments: 1 or 2 pairs per lane
             const int v = std::atoi(e);
-            if (v == 1 || v == 2 || v == 4) p->col_np_adj = v;
+            if (v == 1 || v == 2) p->col_np_adj = v;
         }
         p->nzp = (G.n[2] + 2 * p->zpad + 3) / 4 * 4;   // 16-byte cell columns (vector reds); tail rows stay 0
         const size_t bytes = sizeof(float) * (size_t)(G.nxy * p->nzp);
         e = cudaMalloc(&p->d_work_fwd, bytes);
         if (e == cudaSuccess) e = cudaMalloc(&p->d_work_adj, bytes);
         if (e == cudaSuccess) e = cudaMemset(p->d_work_fwd, 0, bytes);  // zero padding stays zero
+        // forward on the (f, delta f) volume, except where no ray crosses a z plane (3D parallel beam
+        // without tilt: the legacy kernel's flat walk, one 4-byte load per unit, is faster there)
+        p->fd_forward = !std::getenv("XRT_FWD_LEGACY") && !(g->beam == XRT_PAR3D && g->tilt == 0.0);
+        if (e == cudaSuccess && p->fd_forward) {
+            const size_t fdb = 2 * sizeof(float2) * (size_t)(G.nxy * p->nzp);
+            e = cudaMalloc(&p->d_work_fd, fdb);
+            if (e == cudaSuccess) e = cudaMemset(p->d_work_fd, 0, fdb);   // padding beyond the edge rows stays 0
+        }
         if (e == cudaSuccess)
             e = cudaMalloc(&p->d_coldesc, xrt::column_desc_bytes() * (size_t)(p->n_views * D.cols));
         if (e == cudaSuccess) e = xrt::launch_col_desc(p, (cudaStream_t)0);
@@ -471,8 +482,15 @@ xrt_status plan_create_impl(const xrt_geometry* g, int cuda_device, xrt_plan* ou
             const double budget = (env ? std::atof(env) : 64.0) * 1024 * 1024;
             const int rows = 64 * (op ? p->col_np_adj : p->col_np);
             const double slab = std::min((double)p->nzp, column_band_slab(g, G, rows) + 2.0);
-            int ts = 32;
-            while ((double)(2 * ts) * (2 * ts) * slab * 4.0 <= budget) ts *= 2;
+            // bytes per cell one band touches: 8 on the forward's (f, delta f) volume (one half per
+            // row direction), 4 on the float z-fastest copies; the fewest tiles per axis that fit
+            const double cell_bytes = (op == 0 && p->fd_forward) ? 8.0 : 4.0;
+            const int nmax = std::max(G.n[0], G.n[1]);
+            int ts = nmax;
+            for (int nt = 1; ts > 32; ++nt) {
+                ts = (nmax + nt - 1) / nt;
+                if ((double)ts * ts * slab * cell_bytes <= budget) break;
+            }
             if (const char* f = std::getenv("XRT_COLUMN_TILE")) ts = std::max(4, std::atoi(f));  // testing
             xrt_plan_s::ColTiling& T = p->ct[op];
             if (ts >= std::max(G.n[0], G.n[1])) {
@@ -488,6 +506,15 @@ xrt_status plan_create_impl(const xrt_geometry* g, int cuda_device, xrt_plan* ou
                 if (!items.empty()) e = cudaMalloc(&T.d_items, sizeof(uint2) * items.size());
                 if (e == cudaSuccess && !items.empty())
                     e = cudaMemcpy(T.d_items, items.data(), sizeof(uint2) * items.size(), cudaMemcpyHostToDevice);
+                if (op == 0 && p->fd_forward && e == cudaSuccess) {   // the fd forward's CTAs: views x columns
+                    xrt_plan_s::ColTiling& F = p->ct_fd;
+                    F.tile = T.tile; F.n_tx = T.n_tx; F.n_ty = T.n_ty;
+                    xrt::build_column_items(p, views.data(), T.tile, T.n_tx, T.n_ty, items, true);
+                    F.n_items = (int64_t)items.size();
+                    if (!items.empty()) e = cudaMalloc(&F.d_items, sizeof(uint2) * items.size());
+                    if (e == cudaSuccess && !items.empty())
+                        e = cudaMemcpy(F.d_items, items.data(), sizeof(uint2) * items.size(), cudaMemcpyHostToDevice);
+                }
             }
         }
         if (e != cudaSuccess) {
@@ -546,12 +573,14 @@ xrt_status xrt_plan_destroy(xrt_plan p) {
     cudaFree(p->d_views);
     cudaFree(p->d_work_fwd);
     cudaFree(p->d_work_adj);
+    cudaFree(p->d_work_fd);
     cudaFree(p->d_work_att);
     cudaFree(p->d_att_A);
     cudaFree(p->d_att_pieces);
     cudaFree(p->d_att_mumax);
     cudaFree(p->ct[0].d_items);
     cudaFree(p->ct[1].d_items);
+    cudaFree(p->ct_fd.d_items);
     cudaFree(p->d_coldesc);
     cudaFree(p->d_gather_y);
     cudaFree(p->d_rays);
@@ -633,19 +662,22 @@ xrt_status xrt_adjoint_f64(xrt_plan p, const double* sino, double* img, void* cu
     return XRT_OK;
 }
 
-// Attenuated transform: the column kernels for the 3D beams they serve (untiled: the
-// attenuation couples a ray's units along its whole path), else the RAY family.
+// Attenuated transform: the column kernels for the 3D beams they serve (tiled per
+// band with a per-ray combine of the tile pieces, xrt::att_tiled; untiled otherwise), else the RAY
+// family.  Workspace on first use: the forward's interleaved (f, mu) z-fastest volume, the tile
+// pieces (both operators, tiled), the per-ray total attenuation (untiled adjoint only).
 static cudaError_t att_alloc(xrt_plan p, bool adjoint) {
     cudaError_t e = cudaSuccess;
+    const bool tiled = xrt::att_tiled(p);
     if (!p->d_att_mumax) e = cudaMalloc(&p->d_att_mumax, sizeof(unsigned));
     if (e == cudaSuccess && !adjoint && !p->d_work_att) {
         const size_t bytes = 2 * sizeof(float) * (size_t)(p->grid.nxy * p->nzp);
         e = cudaMalloc(&p->d_work_att, bytes);
         if (e == cudaSuccess) e = cudaMemset(p->d_work_att, 0, bytes);   // zero padding stays zero
     }
-    if (e == cudaSuccess && !adjoint && !p->d_att_pieces && xrt::att_piece_floats(p) > 0 && !std::getenv("XRT_ATT_UNTILED"))
+    if (e == cudaSuccess && tiled && !p->d_att_pieces)
         e = cudaMalloc(&p->d_att_pieces, sizeof(float) * (size_t)xrt::att_piece_floats(p));
-    if (e == cudaSuccess && adjoint && !p->d_att_A)
+    if (e == cudaSuccess && adjoint && !tiled && !p->d_att_A)
         e = cudaMalloc(&p->d_att_A, sizeof(float) * (size_t)(p->n_views * p->det.per_view));
     return e;
 }
@@ -677,8 +709,8 @@ xrt_status xrt_adjoint_attenuated(xrt_plan p, const float* sino, const float* mu
         // mu z-fastest in work_fwd; tiled plans: per band, the pieces' attenuation A_t (the plain
         // forward of mu per piece), their suffix sums B_t, then the scatter y e^-(B_t - A_le) L phi
         // with A_le from each piece's start; untiled: A = X mu per ray, then the untiled scatter
-        const bool tiled = p->ct[0].d_items && !std::getenv("XRT_ATT_UNTILED");
-        e = att_alloc(p, !tiled);
+        const bool tiled = xrt::att_tiled(p);
+        e = att_alloc(p, true);
         if (e == cudaSuccess) e = xrt::launch_to_zfast(p, mu, p->d_work_fwd, s);
         if (e == cudaSuccess) e = xrt::launch_att_prepare(p, nullptr, mu, nullptr, p->d_att_mumax, s);
         if (e == cudaSuccess) e = cudaMemsetAsync(p->d_work_adj, 0, sizeof(float) * (size_t)(p->grid.nxy * p->nzp), s);
@@ -721,7 +753,8 @@ xrt_status xrt_forward_host(xrt_plan p, const float* img_host, float* sino_host,
         for (auto& x : ev) XRT_CUDA(cudaEventCreateWithFlags(&x, cudaEventDisableTiming));
         for (int b = 0; b < nb && st == XRT_OK; ++b) {
             const int r0 = b * rb, r1 = std::min(p->det.rows, r0 + rb);
-            cudaError_t e = xrt::launch_forward_column_bands(p, p->d_work_fwd, p->d_stage_sino, b, b + 1, s);
+            cudaError_t e = p->fd_forward ? xrt::launch_forward_fd_bands(p, p->d_work_fd, p->d_stage_sino, b, b + 1, s)
+                                          : xrt::launch_forward_column_bands(p, p->d_work_fwd, p->d_stage_sino, b, b + 1, s);
             p->launches += 1;
             if (e == cudaSuccess) e = cudaEventRecord(ev[b], s);
             if (e == cudaSuccess) e = cudaStreamWaitEvent(a, ev[b], 0);

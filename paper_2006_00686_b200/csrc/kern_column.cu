@@ -56,6 +56,20 @@ namespace {
 #define XRT_COL_WARPS 4   // measured: 4 columns per CTA 0.5-2 % faster than 8 on cfg 3 / 4 / 5, 2 slower
 #endif
 constexpr int kWarps = XRT_COL_WARPS;  // warps per CTA = adjacent detector columns per CTA (one per warp)
+// CTA of the (f, delta f) forward: kFdCols adjacent columns x kFdViews adjacent views, one warp each.
+// Neighbouring views' columns cross nearly the same cells, so the CTA's warps share L1 lines: the
+// compulsory L2 -> L1 traffic per ray-segment of cfg 4 falls from ~5.7 B (4 columns x 1 view) to
+// ~3.4 B (4 x 2) and ~2.5 B (4 x 4) (scratch estimate).
+#ifndef XRT_FD_COLS
+#define XRT_FD_COLS 4
+#endif
+#ifndef XRT_FD_VIEWS
+#define XRT_FD_VIEWS 2
+#endif
+#ifndef XRT_FD_PREFETCH
+#define XRT_FD_PREFETCH 0   // > 0: L1 prefetch that many segments ahead (experiment)
+#endif
+constexpr int kFdCols = XRT_FD_COLS, kFdViews = XRT_FD_VIEWS, kFdWarps = kFdCols * kFdViews;
 #ifndef XRT_KPASSES
 #define XRT_KPASSES 4
 #endif
@@ -772,7 +786,7 @@ template <int kOp, int NP>
 #ifndef XRT_COL_MINB_FWD1
 #define XRT_COL_MINB_FWD1 (768 / (32 * XRT_COL_WARPS))
 #endif
-__global__ void __launch_bounds__(kWarps * 32, NP >= 4 ? 512 / (32 * kWarps) : ((kOp == 2 || kOp == 3) ? XRT_ATT_THREADS / (32 * kWarps) : (NP == 1 ? (kOp == 1 ? XRT_COL_MINB_ADJ1 : XRT_COL_MINB_FWD1) : XRT_COL_MINB))) k_column(const ViewRec* __restrict__ views, DetC dc, GridC g,
+__global__ void __launch_bounds__(kWarps * 32, ((kOp == 2 || kOp == 3) ? XRT_ATT_THREADS / (32 * kWarps) : (NP == 1 ? (kOp == 1 ? XRT_COL_MINB_ADJ1 : XRT_COL_MINB_FWD1) : XRT_COL_MINB))) k_column(const ViewRec* __restrict__ views, DetC dc, GridC g,
                                                        const float* __restrict__ vol, float* __restrict__ volw,
                                                        const float* __restrict__ sino_in,
                                                        float* __restrict__ sino_out, int view0,
@@ -995,6 +1009,328 @@ inline cudaError_t transpose(const float* in, float* out, int64_t rows, int64_t 
     dim3 grid((unsigned)((cols + 31) / 32), (unsigned)(gy < 32768 ? gy : 32768));
     k_transpose<<<grid, dim3(32, 8), 0, s>>>(in, out, rows, cols, in_ld, in_off, out_ld, out_off);
     return cudaGetLastError();
+}
+
+// ================================================================= forward on (f, delta f) cells
+// The forward's volume copy with the crossing cell folded in: cell column c (flat xy index
+// j N_x + i) holds 2 NzP float2,
+//     fd[c][0][kp] = (f[k], f[k+1] - f[k]),    fd[c][1][kp] = (f[k], f[k-1] - f[k]),   kp = k + pad,
+// zero outside the image (the padding next to the image carries +-f of the edge cell).  A ray whose
+// z index steps +1 walks half 0, one stepping -1 walks half 1 (its padded index is offset by NzP),
+// a ray with fixed z half 0.  Per segment and ray ONE 8-byte load gives the start cell's f_s and
+// the difference f_e - f_s to the cell after the ray's z crossing, so the units of
+// eq:range_length_3D accumulate as acc += f_s d_sigma + (f_e - f_s) l_e with
+// l_e = max(sigma_e - tau, 0): one load instead of two (the LSU issue rate bounds the walk:
+// LDG.32 1.69 / LDG.64 2.0 SM-cycles per warp instruction, profiles/issue_peak.json).
+
+// [N_z][N_xy] image -> fd (rows k = -1 .. N_z of every column; the rest of the padding stays 0).
+// Tile of 32 columns x 32 k (+1 halo on each side) through shared memory; writes are coalesced
+// along k (float4 = two float2 cells of one half).
+__global__ void __launch_bounds__(256) k_to_fd(const float* __restrict__ img, float2* __restrict__ fd,
+                                               int64_t nxy, int nz, int64_t nzp, int pad) {
+    __shared__ float t[34][33];
+    const int64_t c0 = (int64_t)blockIdx.x * 32;
+    const int k0 = (int)blockIdx.y * 32 - 1;           // first k of this tile's rows (-1 .. nz)
+    // load k = k0 - 1 .. k0 + 32 (34 rows), columns c0 .. c0 + 31
+    for (int r = threadIdx.y; r < 34; r += 8) {
+        const int k = k0 - 1 + r;
+        const int64_t c = c0 + threadIdx.x;
+        t[r][threadIdx.x] = (k >= 0 && k < nz && c < nxy) ? img[(int64_t)k * nxy + c] : 0.f;
+    }
+    __syncthreads();
+    // write: warp w handles columns w, w + 8, ...; lane = k offset
+    for (int cc = threadIdx.y; cc < 32; cc += 8) {
+        const int64_t c = c0 + cc;
+        const int k = k0 + (int)threadIdx.x;
+        if (c >= nxy || k > nz || k < -1) continue;
+        const float f = t[threadIdx.x + 1][cc];
+        const float fp = t[threadIdx.x + 2][cc], fm = t[threadIdx.x][cc];
+        float2* col = fd + c * 2 * nzp + pad + k;
+        col[0] = make_float2(f, fp - f);
+        col[nzp] = make_float2(f, fm - f);
+    }
+}
+
+// One lane's pair of rays on the fd volume.
+struct FdPair {
+    float2 kpf;    // magic float: bits = kMagicBits + half * NzP + pad + k (the current cell)
+    float2 kpf0;   // kpf at the ray's entry state (crossing count = (kpf - kpf0) * dk)
+    float2 dkf;    // +1 / -1 per crossing, 0 fixed
+    float2 ntz;    // -(next crossing - sigma_c), sigma_c the current chunk's origin
+    float2 ndtz;   // -dtz (0 fixed)
+    float2 t0z;    // first crossing, sigma from the square entry (kNoCrossPos fixed)
+    float acc0a, acc0b, acc1a, acc1b;
+    float2 w;      // 1 / cos(beta)
+    bool live0, live1;
+};
+constexpr float kNoCrossPos = 1.0e30f;
+
+__device__ __forceinline__ void fd_init(FdPair& P, const RayZ& Za, const RayZ& Zb, int nzp) {
+    const float ha = Za.dk < 0 ? (float)nzp : 0.f, hb = Zb.dk < 0 ? (float)nzp : 0.f;
+    P.kpf = make_float2((float)Za.kp + ha + kMagic, (float)Zb.kp + hb + kMagic);
+    P.kpf0 = P.kpf;
+    P.dkf = make_float2((float)Za.dk, (float)Zb.dk);
+    P.ndtz = make_float2(Za.dk ? -Za.dtz : 0.f, Zb.dk ? -Zb.dtz : 0.f);
+    P.t0z = make_float2(Za.dk ? Za.t0z : kNoCrossPos, Zb.dk ? Zb.t0z : kNoCrossPos);
+    P.ntz = make_float2(-P.t0z.x, -P.t0z.y);
+    P.acc0a = P.acc0b = P.acc1a = P.acc1b = 0.f;
+    P.w = make_float2(Za.scale, Zb.scale);
+    P.live0 = Za.active;
+    P.live1 = Zb.active;
+}
+
+// crossings tau_m = t0z + m dtz with tau_m < sf taken (the ray's state at sigma_first, tiled)
+__device__ __forceinline__ void fd_skip(float& kpf, float kpf0, float dkf, float t0z, float ndtz, float sf) {
+    if (dkf == 0.f) return;
+    const float dtz = -ndtz;
+    int m0 = (int)ceilf((sf - t0z) / dtz);
+    m0 = m0 < 0 ? 0 : m0;
+    if (fmaf((float)m0, dtz, t0z) < sf) ++m0;
+    if (m0 > 0 && !(fmaf((float)(m0 - 1), dtz, t0z) < sf)) --m0;
+    kpf = fmaf((float)m0, dkf, kpf0);
+}
+
+// the next crossing relative to the chunk origin sigma_c, from the exact crossing count
+__device__ __forceinline__ void fd_anchor(FdPair& P, float sc) {
+    const float2 m = __fmul2_rn(__fadd2_rn(P.kpf, make_float2(-P.kpf0.x, -P.kpf0.y)), P.dkf);
+    const float2 tau = __ffma2_rn(m, make_float2(-P.ndtz.x, -P.ndtz.y), P.t0z);
+    P.ntz = make_float2(sc - tau.x, sc - tau.y);
+}
+
+__device__ __forceinline__ float2 ldg_f2(unsigned long long a) {
+    float2 v;
+    asm("ld.global.nc.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "l"(a));
+    return v;
+}
+
+// the chunk's segments for the lane's 2 NP rays: per segment (pointer, sigma_e - sigma_c, d_sigma)
+// and ray, z crossing cr = [tau < sigma_e], l_e = max(sigma_e - tau, 0), then the state advances;
+// software-pipelined one segment deep (the next segment's loads issue before this one's FMAs).
+template <int NP>
+__device__ __forceinline__ void fd_segments(unsigned seg, int total, FdPair (&P)[NP]) {
+    uint4 raw = lds128(seg);
+    float2 va[NP], vb[NP];
+#pragma unroll
+    for (int p = 0; p < NP; ++p) {
+        va[p] = ldg_f2(seg_ptr(raw) + 8ull * __float_as_uint(P[p].kpf.x));
+        vb[p] = ldg_f2(seg_ptr(raw) + 8ull * __float_as_uint(P[p].kpf.y));
+    }
+#pragma unroll 2
+    for (int s = 0; s < total; ++s) {
+        const float qse = __uint_as_float(raw.z), qds = __uint_as_float(raw.w);
+        const float2 se2 = make_float2(qse, qse);
+        const uint4 nraw = lds128(seg + 16u * (unsigned)min(s + 1, total - 1));   // last trip: reload
+#if XRT_FD_PREFETCH
+        const uint4 praw = lds128(seg + 16u * (unsigned)min(s + XRT_FD_PREFETCH, total - 1));
+#endif
+#pragma unroll
+        for (int p = 0; p < NP; ++p) {
+            const float2 le = __fadd2_rn(se2, P[p].ntz);                 // sigma_e - tau
+            const float2 cr = make_float2(gt0(le.x), gt0(le.y));
+            const float lma = fmaxf(le.x, 0.f), lmb = fmaxf(le.y, 0.f);  // l_e
+            P[p].kpf = __ffma2_rn(cr, P[p].dkf, P[p].kpf);
+            P[p].ntz = __ffma2_rn(cr, P[p].ndtz, P[p].ntz);
+            const float2 na = ldg_f2(seg_ptr(nraw) + 8ull * __float_as_uint(P[p].kpf.x));
+            const float2 nb = ldg_f2(seg_ptr(nraw) + 8ull * __float_as_uint(P[p].kpf.y));
+#if XRT_FD_PREFETCH
+            {   // L1 prefetch of the line two segments ahead at the current cell (a crossing moves by one cell)
+                const unsigned long long pa = seg_ptr(praw) + 8ull * __float_as_uint(P[p].kpf.x);
+                const unsigned long long pb = seg_ptr(praw) + 8ull * __float_as_uint(P[p].kpf.y);
+                asm volatile("prefetch.global.L1 [%0];" :: "l"(pa));
+                asm volatile("prefetch.global.L1 [%0];" :: "l"(pb));
+            }
+#endif
+            P[p].acc0a = fmaf(va[p].x, qds, P[p].acc0a);                  // f_s d_sigma
+            P[p].acc1a = fmaf(va[p].y, lma, P[p].acc1a);                  // (f_e - f_s) l_e
+            P[p].acc0b = fmaf(vb[p].x, qds, P[p].acc0b);
+            P[p].acc1b = fmaf(vb[p].y, lmb, P[p].acc1b);
+            va[p] = na;
+            vb[p] = nb;
+        }
+        raw = nraw;
+    }
+}
+
+// Two segments deep: the z state runs one segment ahead of the accumulation, so each segment's
+// loads issue two segments before their values are consumed (L1 misses wait on L2).  Repeating
+// the chunk's last record for the look-ahead is harmless: its crossing is already taken (cr = 0).
+template <int NP>
+__device__ __forceinline__ void fd_segments2(unsigned seg, int total, FdPair (&P)[NP]) {
+    const uint4 raw0 = lds128(seg);
+    uint4 raw1 = lds128(seg + 16u * (unsigned)min(1, total - 1));
+    float2 v0a[NP], v0b[NP], v1a[NP], v1b[NP], lm0[NP];
+    float ds0 = __uint_as_float(raw0.w);
+#pragma unroll
+    for (int p = 0; p < NP; ++p) {
+        v0a[p] = ldg_f2(seg_ptr(raw0) + 8ull * __float_as_uint(P[p].kpf.x));
+        v0b[p] = ldg_f2(seg_ptr(raw0) + 8ull * __float_as_uint(P[p].kpf.y));
+        const float se = __uint_as_float(raw0.z);
+        const float2 le = __fadd2_rn(make_float2(se, se), P[p].ntz);
+        const float2 cr = make_float2(gt0(le.x), gt0(le.y));
+        lm0[p] = make_float2(fmaxf(le.x, 0.f), fmaxf(le.y, 0.f));
+        P[p].kpf = __ffma2_rn(cr, P[p].dkf, P[p].kpf);
+        P[p].ntz = __ffma2_rn(cr, P[p].ndtz, P[p].ntz);
+        v1a[p] = ldg_f2(seg_ptr(raw1) + 8ull * __float_as_uint(P[p].kpf.x));
+        v1b[p] = ldg_f2(seg_ptr(raw1) + 8ull * __float_as_uint(P[p].kpf.y));
+    }
+#pragma unroll 2
+    for (int s = 0; s < total; ++s) {
+        const uint4 raw2 = lds128(seg + 16u * (unsigned)min(s + 2, total - 1));
+        const float se1 = __uint_as_float(raw1.z), ds1 = __uint_as_float(raw1.w);
+        const float2 se2 = make_float2(se1, se1);
+#pragma unroll
+        for (int p = 0; p < NP; ++p) {
+            const float2 le = __fadd2_rn(se2, P[p].ntz);                 // segment s + 1
+            const float2 cr = make_float2(gt0(le.x), gt0(le.y));
+            const float2 lm1 = make_float2(fmaxf(le.x, 0.f), fmaxf(le.y, 0.f));
+            P[p].kpf = __ffma2_rn(cr, P[p].dkf, P[p].kpf);
+            P[p].ntz = __ffma2_rn(cr, P[p].ndtz, P[p].ntz);
+            const float2 na = ldg_f2(seg_ptr(raw2) + 8ull * __float_as_uint(P[p].kpf.x));   // segment s + 2
+            const float2 nb = ldg_f2(seg_ptr(raw2) + 8ull * __float_as_uint(P[p].kpf.y));
+            P[p].acc0a = fmaf(v0a[p].x, ds0, P[p].acc0a);                // segment s
+            P[p].acc1a = fmaf(v0a[p].y, lm0[p].x, P[p].acc1a);
+            P[p].acc0b = fmaf(v0b[p].x, ds0, P[p].acc0b);
+            P[p].acc1b = fmaf(v0b[p].y, lm0[p].y, P[p].acc1b);
+            v0a[p] = v1a[p]; v0b[p] = v1b[p];
+            v1a[p] = na; v1b[p] = nb;
+            lm0[p] = lm1;
+        }
+        ds0 = ds1;
+        raw1 = raw2;
+    }
+}
+
+#ifndef XRT_FD_DEPTH
+#define XRT_FD_DEPTH 1
+#endif
+
+#ifndef XRT_FD_THREADS
+#define XRT_FD_THREADS 1024  // resident threads per SM targeted by the launch bounds (2 pairs per lane):
+#endif                       // cfg 4 124.0 ms vs 136.0 (768), 138.9 (512); 4 x 4 CTAs 126.6
+#ifndef XRT_FD_THREADS1
+#define XRT_FD_THREADS1 768  // ... 1 pair per lane
+#endif
+#define XRT_FD_MINB (XRT_FD_THREADS / (32 * kFdWarps) > 0 ? XRT_FD_THREADS / (32 * kFdWarps) : 1)
+#define XRT_FD_MINB1 (XRT_FD_THREADS1 / (32 * kFdWarps) > 0 ? XRT_FD_THREADS1 / (32 * kFdWarps) : 1)
+
+// CTA / warp / band layout as k_column (kOp 0): warp = one detector column, 2 NP rays per lane (rows
+// band 64 NP + 32 q + lane), band-major over (view, column group, tile) items.
+template <int NP>
+__global__ void __launch_bounds__(kFdWarps * 32, NP == 1 ? XRT_FD_MINB1 : XRT_FD_MINB)
+k_fwd_fd(const ViewRec* __restrict__ views, DetC dc, GridC g, const float2* __restrict__ fd,
+         float* __restrict__ sino_out, int view0, const ColDesc* __restrict__ desc, ColumnLaunch L) {
+    constexpr int R = 2 * NP;
+    __shared__ Seg s_seg[kFdWarps][2 * 32];
+    __shared__ float s_first[kFdWarps];
+    const int lane = threadIdx.x & 31;
+    const int warp = threadIdx.x >> 5;
+    const unsigned bid = blockIdx.x;
+    const int band = L.band0 + (int)(bid / (unsigned)L.n_items);
+    const unsigned it = bid % (unsigned)L.n_items;
+    int vv, cg, ti0 = 0, ti1 = g.n[0], tj0 = 0, tj1 = g.n[1];
+    if (L.items) {
+        const uint2 w = L.items[it];
+        vv = (int)w.x;
+        cg = (int)(w.y & 0xffffu);
+        const int t = (int)(w.y >> 16);
+        ti0 = (t % L.n_tx) * L.tile; ti1 = min(ti0 + L.tile, g.n[0]);
+        tj0 = (t / L.n_tx) * L.tile; tj1 = min(tj0 + L.tile, g.n[1]);
+    } else {
+        cg = (int)(it % (unsigned)L.n_cgroups);
+        vv = (int)(it / (unsigned)L.n_cgroups);
+    }
+    const bool tiled = L.items != nullptr;
+    const int c = cg * kFdCols + warp % kFdCols;
+    vv = vv * kFdViews + warp / kFdCols;           // items count view blocks of kFdViews views
+    if (c >= dc.cols || vv >= L.n_views) return;  // warp-uniform; no CTA barrier below
+    const int v = view0 + vv;
+    const ViewRec V = views[v];
+    ColumnPath Pth;
+    double ca = 1.0;
+    float pux = 0.f, puy = 0.f, pwx = 0.f, pwy = 0.f;
+    load_path(desc + ((int64_t)v * dc.cols + c), g.n[0], Pth, ca, pux, puy, pwx, pwy);
+    if (!Pth.hit) return;
+    int na = 0, nb = Pth.n_slices;
+    if (tiled) {
+        float lo = -INFINITY, hi = INFINITY;
+        if (pwx != 0.f) {
+            const float a0 = (ti0 - pux) / pwx, a1 = (ti1 - pux) / pwx;
+            lo = fmaxf(lo, fminf(a0, a1)); hi = fminf(hi, fmaxf(a0, a1));
+        } else if (!(pux >= ti0 - 1e-3f && pux <= ti1 + 1e-3f)) { hi = -INFINITY; }
+        if (pwy != 0.f) {
+            const float a0 = (tj0 - puy) / pwy, a1 = (tj1 - puy) / pwy;
+            lo = fmaxf(lo, fminf(a0, a1)); hi = fminf(hi, fmaxf(a0, a1));
+        } else if (!(puy >= tj0 - 1e-3f && puy <= tj1 + 1e-3f)) { hi = -INFINITY; }
+        if (!(hi >= lo)) return;
+        const float ida = 1.f / Pth.dta;
+        na = max(0, __float2int_rd((lo - Pth.t0a) * ida) - 1);
+        nb = min(Pth.n_slices, __float2int_rd((hi - Pth.t0a) * ida) + 3);
+    }
+    FdPair P[NP];
+    bool any_live = false;
+#pragma unroll
+    for (int p = 0; p < NP; ++p) {
+        RayZ Za, Zb;
+        const int ra = (band * R + 2 * p) * 32 + lane, rb = ra + 32;
+        ray_z(V, dc, g, Pth, ca, ra, L.pad, Za);
+        ray_z(V, dc, g, Pth, ca, rb, L.pad, Zb);
+        fd_init(P[p], Za, Zb, L.nzp);
+        any_live |= P[p].live0 | P[p].live1;
+    }
+    if (!__any_sync(0xffffffffu, any_live)) return;
+    Seg* seg = s_seg[warp];
+    const unsigned seg_s = (unsigned)__cvta_generic_to_shared(seg);
+    // segment pointers pre-offset by -8 kMagicBits bytes: address = ptr + 8 bits(kpf)
+    const unsigned long long base = (unsigned long long)fd - 8ull * kMagicBits;
+    const unsigned long long cstride = 16ull * (unsigned long long)L.nzp;
+    bool zinit = !tiled;  // untiled: the z state at sigma = 0 is the initial one
+    for (int n0 = na; n0 < nb; n0 += 32) {
+        // chunk origin: the start of slice n0 (the same fmaf every lane and the slices use)
+        const float sc = n0 == 0 ? 0.f : fminf(fmaf((float)(n0 - 1), Pth.dta, Pth.t0a), Pth.L);
+        const int n = n0 + lane;
+        float a0s = 0.f, a0e = 0.f, a1s = 0.f, a1e = 0.f;
+        int c0 = 0, c1 = 0, cnt = 0;
+        if (n < nb) cnt = slice_segments(Pth, n, ti0, ti1, tj0, tj1, a0s, a0e, c0, a1s, a1e, c1);
+        int incl = cnt;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int t = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += t;
+        }
+        const int b = incl - cnt;
+        if (cnt > 0) {
+            sts_seg(seg_s + 16u * (unsigned)b, base + cstride * (unsigned)c0, a0e - sc, a0e - a0s);
+            if (b == 0) s_first[warp] = a0s;
+        }
+        if (cnt > 1) sts_seg(seg_s + 16u * (unsigned)(b + 1), base + cstride * (unsigned)c1, a1e - sc, a1e - a1s);
+        const int total = __shfl_sync(0xffffffffu, incl, 31);
+        __syncwarp();
+        if (total > 0) {
+            if (!zinit) {
+                zinit = true;
+                const float sf = s_first[warp];
+#pragma unroll
+                for (int p = 0; p < NP; ++p) {
+                    fd_skip(P[p].kpf.x, P[p].kpf0.x, P[p].dkf.x, P[p].t0z.x, P[p].ndtz.x, sf);
+                    fd_skip(P[p].kpf.y, P[p].kpf0.y, P[p].dkf.y, P[p].t0z.y, P[p].ndtz.y, sf);
+                }
+            }
+#pragma unroll
+            for (int p = 0; p < NP; ++p) fd_anchor(P[p], sc);
+            if (XRT_FD_DEPTH == 2) fd_segments2<NP>(seg_s, total, P);
+            else fd_segments<NP>(seg_s, total, P);
+        }
+        __syncwarp();  // the next chunk overwrites the segments
+    }
+#pragma unroll
+    for (int q = 0; q < R; ++q) {
+        const FdPair& Q = P[q >> 1];
+        if (!((q & 1) ? Q.live1 : Q.live0)) continue;
+        const float a = (q & 1) ? (Q.acc0b + Q.acc1b) * Q.w.y : (Q.acc0a + Q.acc1a) * Q.w.x;
+        const int64_t m = ((int64_t)v * dc.rows + (band * R + q) * 32 + lane) * dc.cols + c;
+        if (tiled) { if (a != 0.f) red_sino(sino_out + m, a, l2_evict_first()); }
+        else __stcs(sino_out + m, a);
+    }
 }
 
 // ============================================================================ voxel-driven gather
@@ -1310,12 +1646,11 @@ cudaError_t launch_column_op(const xrt_plan_s* p, const float* vol, float* volw,
     if (np == 1)
         k_column<kOp, 1><<<nblk, kWarps * 32, 0, s>>>(p->d_views, p->det, p->grid, vol, volw, sino_in, sino_out, (int)v0, d, L,
                                                       sino_aux, att_mumax, att_lmax);
-    else if (np == 4 && kOp < 2)
-        k_column<kOp < 2 ? kOp : 0, 4><<<nblk, kWarps * 32, 0, s>>>(p->d_views, p->det, p->grid, vol, volw, sino_in, sino_out, (int)v0,
-                                                                    d, L, sino_aux, att_mumax, att_lmax);
-    else
+    else if (np == 2)
         k_column<kOp, 2><<<nblk, kWarps * 32, 0, s>>>(p->d_views, p->det, p->grid, vol, volw, sino_in, sino_out, (int)v0, d, L,
                                                       sino_aux, att_mumax, att_lmax);
+    else
+        return cudaErrorInvalidValue;   // only 1 or 2 ray pairs per lane are built (plan rejects others)
     return cudaGetLastError();
 }
 
@@ -1343,6 +1678,53 @@ int column_band_rows(const xrt_plan_s* p, bool adj) { return 64 * (adj ? p->col_
 int column_bands(const xrt_plan_s* p, bool adj) {
     const int rb = column_band_rows(p, adj);
     return (p->det.rows + rb - 1) / rb;
+}
+
+// ---- forward on the (f, delta f) volume (AUTO forward of the 3D column path)
+cudaError_t launch_to_fd(const xrt_plan_s* p, const float* img, float2* fd, cudaStream_t s) {
+    const int nz = p->grid.n[2];
+    dim3 grid((unsigned)((p->grid.nxy + 31) / 32), (unsigned)((nz + 2 + 31) / 32));
+    k_to_fd<<<grid, dim3(32, 8), 0, s>>>(img, fd, p->grid.nxy, nz, p->nzp, (int)p->zpad);
+    return cudaGetLastError();
+}
+
+static cudaError_t launch_fd(const xrt_plan_s* p, const float2* fd, float* sino, const ColumnLaunch& L, int nblk,
+                             cudaStream_t s) {
+    if (nblk <= 0) return cudaSuccess;
+    const ColDesc* d = (const ColDesc*)p->d_coldesc;
+    if (p->col_np == 1)
+        k_fwd_fd<1><<<nblk, kFdWarps * 32, 0, s>>>(p->d_views, p->det, p->grid, fd, sino, 0, d, L);
+    else if (p->col_np == 2)
+        k_fwd_fd<2><<<nblk, kFdWarps * 32, 0, s>>>(p->d_views, p->det, p->grid, fd, sino, 0, d, L);
+    else
+        return cudaErrorInvalidValue;
+    return cudaGetLastError();
+}
+
+// all views and bands [b0, b1) (rows b * 64 NP ...); sinogram rows of those bands pre-zeroed
+cudaError_t launch_forward_fd_bands(const xrt_plan_s* p, const float2* fd, float* sino, int b0, int b1,
+                                    cudaStream_t s) {
+    int nblk = 0;
+    ColumnLaunch L = make_launch(p, 0, p->n_views, nblk, false);
+    L.n_cgroups = (p->det.cols + kFdCols - 1) / kFdCols;
+    if (p->ct_fd.d_items) {
+        L.tile = p->ct_fd.tile;
+        L.n_tx = p->ct_fd.n_tx;
+        L.items = (const uint2*)p->ct_fd.d_items;
+        L.n_items = (int)p->ct_fd.n_items;
+    } else {
+        L.items = nullptr;
+        L.n_items = (int)((p->n_views + kFdViews - 1) / kFdViews) * L.n_cgroups;
+    }
+    const int rb = column_band_rows(p, false);
+    const int r0 = b0 * rb, r1 = std::min(p->det.rows, b1 * rb);
+    if (r1 <= r0) return cudaSuccess;
+    const size_t pitch = sizeof(float) * (size_t)p->det.per_view;
+    cudaError_t e = cudaMemset2DAsync(sino + (int64_t)r0 * p->det.cols, pitch, 0,
+                                      sizeof(float) * (size_t)(r1 - r0) * p->det.cols, (size_t)p->n_views, s);
+    if (e != cudaSuccess) return e;
+    L.band0 = b0;
+    return launch_fd(p, fd, sino, L, L.n_items * (b1 - b0), s);
 }
 
 cudaError_t launch_forward_column_bands(const xrt_plan_s* p, const float* vol_zfast, float* sino, int b0,
@@ -1443,8 +1825,8 @@ __global__ void k_att_combine(const float* __restrict__ pieces, int n_tiles, int
     const int rr = (int)(rem / dc.cols), c = (int)(rem - (int64_t)rr * dc.cols);
     const int row = band * rows_band + rr;
     if (row >= dc.rows) return;
-    float sg[16], S[16], A[16];
-    const int nt = min(n_tiles, 16);
+    float sg[kMaxAttTiles], S[kMaxAttTiles], A[kMaxAttTiles];
+    const int nt = n_tiles;   // <= kMaxAttTiles: att_tiled() routes larger tilings to the untiled path
     for (int t = 0; t < nt; ++t) {
         const float* q = pieces + 3 * (rib * n_tiles + t);
         sg[t] = q[0]; S[t] = q[1]; A[t] = q[2];
@@ -1465,7 +1847,7 @@ cudaError_t launch_forward_att_column(const xrt_plan_s* p, const float* work2, c
                                       float* pieces, cudaStream_t s) {
     int nblk = 0;
     const xrt_plan_s::ColTiling& T = p->ct[0];
-    if (!T.d_items || !pieces) {
+    if (!att_tiled(p) || !pieces) {
         // untiled: every ray's whole path in one CTA
         ColumnLaunch L = make_launch(p, 0, p->n_views, nblk, false, true);
         cudaError_t e = cudaMemsetAsync(sino, 0, sizeof(float) * (size_t)(p->n_views * p->det.per_view), s);
@@ -1494,9 +1876,17 @@ cudaError_t launch_forward_att_column(const xrt_plan_s* p, const float* work2, c
     return e;
 }
 
+// The tiled attenuated operators combine a ray's tile pieces in registers (k_att_combine /
+// k_att_suffix hold kMaxAttTiles slots), so they serve tilings of at most kMaxAttTiles tiles; a plan
+// with more tiles (large in-plane grids or small XRT_COLUMN_TILE) runs the untiled attenuated path.
+bool att_tiled(const xrt_plan_s* p) {
+    const xrt_plan_s::ColTiling& T = p->ct[0];
+    return T.d_items != nullptr && T.n_tx * T.n_ty <= kMaxAttTiles && !std::getenv("XRT_ATT_UNTILED");
+}
+
 int64_t att_piece_floats(const xrt_plan_s* p) {
     const xrt_plan_s::ColTiling& T = p->ct[0];
-    if (!T.d_items) return 0;
+    if (!att_tiled(p)) return 0;
     return 3 * p->n_views * (int64_t)column_band_rows(p, false) * p->det.cols * T.n_tx * T.n_ty;
 }
 
@@ -1506,9 +1896,9 @@ namespace {
 __global__ void k_att_suffix(float* __restrict__ pieces, int n_tiles, int64_t rays_band) {
     const int64_t rib = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (rib >= rays_band) return;
-    float sg[16], A[16];
-    int id[16];
-    const int nt = min(n_tiles, 16);
+    float sg[kMaxAttTiles], A[kMaxAttTiles];
+    int id[kMaxAttTiles];
+    const int nt = n_tiles;   // <= kMaxAttTiles (att_tiled)
     for (int t = 0; t < nt; ++t) {
         sg[t] = pieces[3 * (rib * n_tiles + t)];
         A[t] = pieces[3 * (rib * n_tiles + t) + 2];
@@ -1533,7 +1923,7 @@ __global__ void k_att_suffix(float* __restrict__ pieces, int n_tiles, int64_t ra
 cudaError_t launch_adjoint_att_tiled(const xrt_plan_s* p, const float* mu_zfast, float* pieces,
                                      const unsigned* mumax, const float* y, float* acc_zfast, cudaStream_t s) {
     const xrt_plan_s::ColTiling& T = p->ct[0];
-    if (!T.d_items) return cudaErrorNotSupported;
+    if (!att_tiled(p) || !pieces) return cudaErrorNotSupported;
     // both passes on the forward's tiles, bands and rays per lane (the pieces' layout)
     const int rbf = column_band_rows(p, false);
     int nblk = 0;
@@ -1574,9 +1964,9 @@ cudaError_t launch_adjoint_att_column(const xrt_plan_s* p, const float* mu_zfast
 // Rays per lane 2 NP, NP in {1, 2}: the fewest idle rows in the last band of 64 NP rows (ties:
 // more rays per lane, i.e. each segment descriptor shared by more rays).
 int choose_col_np(int rows) {
-    if (const char* e = std::getenv("XRT_COL_NP")) {   // experiments: 1, 2 or 4 pairs per lane
+    if (const char* e = std::getenv("XRT_COL_NP")) {   // experiments: 1 or 2 pairs per lane
         const int v = std::atoi(e);
-        if (v == 1 || v == 2 || v == 4) return v;
+        if (v == 1 || v == 2) return v;
     }
     int best = 1, best_waste = 1 << 30;
     for (int np = 1; np <= 2; ++np) {
@@ -1601,16 +1991,19 @@ cudaError_t launch_col_desc(const xrt_plan_s* p, cudaStream_t s) {
 // Host: work list of the tiled launch.  For every view and column group, the tiles crossed by
 // any of the group's in-plane lines (walked in fp64 over the tile grid); items sorted by tile.
 int build_column_items(const xrt_plan_s* p, const ViewRec* views_host, int ts, int ntx, int nty,
-                       std::vector<uint2>& items) {
+                       std::vector<uint2>& items, bool fd) {
     const GridC& g = p->grid;
     const DetC& dc = p->det;
-    const int C = kWarps;
+    const int C = fd ? kFdCols : kWarps;          // columns per CTA
+    const int VB = fd ? kFdViews : 1;             // views per CTA (item .x = view block)
     const int ncg = (dc.cols + C - 1) / C;
+    const int64_t nvb = (p->n_views + VB - 1) / VB;
     std::vector<std::vector<uint2>> per_tile((size_t)ntx * nty);
-    std::vector<int> mark((size_t)ntx * nty, -1);
-    for (int64_t v = 0; v < p->n_views; ++v) {
+    std::vector<int64_t> mark((size_t)ntx * nty, -1);
+    for (int64_t vb = 0; vb < nvb; ++vb) {
         for (int cgi = 0; cgi < ncg; ++cgi) {
-            const int stamp = (int)(v * ncg + cgi);
+            const int64_t stamp = vb * ncg + cgi;
+            for (int64_t v = vb * VB; v < std::min<int64_t>(p->n_views, (vb + 1) * VB); ++v)
             for (int c = cgi * C; c < std::min(dc.cols, (cgi + 1) * C); ++c) {
                 double qx, qy, ex, ey, ca;
                 column_line(views_host[v], dc, c, qx, qy, ex, ey, ca);
@@ -1635,7 +2028,7 @@ int build_column_items(const xrt_plan_s* p, const ViewRec* views_host, int ts, i
                         } else ok = ok && uy >= y0 && uy <= y1;
                         if (ok && hi >= lo) {
                             mark[t] = stamp;
-                            per_tile[t].push_back(make_uint2((unsigned)v, (unsigned)cgi | ((unsigned)t << 16)));
+                            per_tile[t].push_back(make_uint2((unsigned)vb, (unsigned)cgi | ((unsigned)t << 16)));
                         }
                     }
             }

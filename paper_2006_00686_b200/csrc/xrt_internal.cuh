@@ -223,13 +223,15 @@ struct xrt_plan_s {
     xrt::ViewRec* d_views = nullptr;   // device [n_views]
     float* d_work_fwd = nullptr;       // z-fastest, z-padded copy of the forward input (COLUMN)
     float* d_work_adj = nullptr;       // z-fastest, z-padded adjoint accumulator (COLUMN)
+    float2* d_work_fd = nullptr;       // forward (COLUMN): per cell 2 x NzP (f, f[k+-1] - f[k]) cells
+    bool fd_forward = true;            // AUTO forward on the (f, delta f) volume (XRT_FWD_LEGACY=1: k_column)
     int64_t zpad = 0, nzp = 0;         // z padding per side and padded column length
     // xy tiling of the column kernels (L2 residency), per operator: [0] forward, [1] adjoint
     struct ColTiling {
         int tile = 0, n_tx = 1, n_ty = 1;
         void* d_items = nullptr;       // device uint2 work list (tiled) or nullptr (one tile)
         int64_t n_items = 0;
-    } ct[2];
+    } ct[2], ct_fd;                    // ct_fd: the (f, delta f) forward's items (view blocks x column groups)
     int col_np = 2;                    // ray pairs per lane of the forward column kernel (rows per band = 64 col_np)
     int col_np_adj = 1;                // ... of the adjoint column kernel (measured: 1 pair is faster, cfg 3 / 4)
     // attenuated operators on the column path (allocated on first use)
@@ -269,6 +271,8 @@ cudaError_t launch_att_prepare(const xrt_plan_s* p, const float* img, const floa
                                unsigned* mumax, cudaStream_t s);
 cudaError_t launch_forward_att_column(const xrt_plan_s* p, const float* work2, const unsigned* mumax, float* sino,
                                       float* pieces, cudaStream_t s);
+constexpr int kMaxAttTiles = 16;   // tile pieces per ray the attenuated combine holds (att_tiled)
+bool att_tiled(const xrt_plan_s* p);
 int64_t att_piece_floats(const xrt_plan_s* p);
 cudaError_t launch_adjoint_att_tiled(const xrt_plan_s* p, const float* mu_zfast, float* pieces,
                                      const unsigned* mumax, const float* y, float* acc_zfast, cudaStream_t s);
@@ -291,7 +295,7 @@ cudaError_t launch_adjoint_column(const xrt_plan_s* p, const float* sino, float*
 #include <vector>
 namespace xrt {
 int build_column_items(const xrt_plan_s* p, const ViewRec* views_host, int ts, int ntx, int nty,
-                       std::vector<uint2>& items);
+                       std::vector<uint2>& items, bool fd = false);
 size_t column_desc_bytes();
 int choose_col_np(int rows);
 int column_cta_columns();
@@ -309,6 +313,9 @@ cudaError_t launch_slice2d(const xrt_plan_s* p, bool adjoint, const float* img, 
 int column_bands(const xrt_plan_s* p, bool adj);
 cudaError_t launch_forward_column_bands(const xrt_plan_s* p, const float* vol_zfast, float* sino, int b0,
                                         int b1, cudaStream_t s);
+cudaError_t launch_to_fd(const xrt_plan_s* p, const float* img, float2* fd, cudaStream_t s);
+cudaError_t launch_forward_fd_bands(const xrt_plan_s* p, const float2* fd, float* sino, int b0, int b1,
+                                    cudaStream_t s);
 cudaError_t launch_adjoint_column_bands(const xrt_plan_s* p, const float* sino, float* vol_zfast, int b0,
                                         int b1, cudaStream_t s);
 }  // namespace xrt

@@ -55,9 +55,12 @@ def _ray_list_struct(g: dict):
     return r, params
 
 
-def _stream_handle(stream) -> int:
+def _stream_handle(stream, device: int) -> int:
+    """The raw cudaStream_t of ``stream`` (default: the current torch stream of the plan's device)."""
     if stream is None:
-        stream = torch.cuda.current_stream()
+        stream = torch.cuda.current_stream(device)
+    elif stream.device.index != device:
+        raise ValueError(f"stream is on cuda:{stream.device.index}, plan on cuda:{device}")
     return int(stream.cuda_stream)
 
 
@@ -135,7 +138,7 @@ class Plan:
         if out is None:
             out = torch.empty(self.sino_shape, dtype=torch.float32, device=img.device)
         self._check_dev(out, self.sino_shape, "sino")
-        check(self._lib.xrt_forward(self._h, img.data_ptr(), out.data_ptr(), _stream_handle(stream)))
+        check(self._lib.xrt_forward(self._h, img.data_ptr(), out.data_ptr(), _stream_handle(stream, self.device)))
         return out
 
     def adjoint(self, sino: torch.Tensor, out: torch.Tensor | None = None, stream=None) -> torch.Tensor:
@@ -144,7 +147,7 @@ class Plan:
         if out is None:
             out = torch.empty(self.image_shape, dtype=torch.float32, device=sino.device)
         self._check_dev(out, self.image_shape, "img")
-        check(self._lib.xrt_adjoint(self._h, sino.data_ptr(), out.data_ptr(), _stream_handle(stream)))
+        check(self._lib.xrt_adjoint(self._h, sino.data_ptr(), out.data_ptr(), _stream_handle(stream, self.device)))
         return out
 
     def forward64(self, img: torch.Tensor, out: torch.Tensor | None = None, stream=None) -> torch.Tensor:
@@ -153,7 +156,7 @@ class Plan:
         if out is None:
             out = torch.empty(self.sino_shape, dtype=torch.float64, device=img.device)
         self._check_dev(out, self.sino_shape, "sino", torch.float64)
-        check(self._lib.xrt_forward_f64(self._h, img.data_ptr(), out.data_ptr(), _stream_handle(stream)))
+        check(self._lib.xrt_forward_f64(self._h, img.data_ptr(), out.data_ptr(), _stream_handle(stream, self.device)))
         return out
 
     def adjoint64(self, sino: torch.Tensor, out: torch.Tensor | None = None, stream=None) -> torch.Tensor:
@@ -162,7 +165,7 @@ class Plan:
         if out is None:
             out = torch.empty(self.image_shape, dtype=torch.float64, device=sino.device)
         self._check_dev(out, self.image_shape, "img", torch.float64)
-        check(self._lib.xrt_adjoint_f64(self._h, sino.data_ptr(), out.data_ptr(), _stream_handle(stream)))
+        check(self._lib.xrt_adjoint_f64(self._h, sino.data_ptr(), out.data_ptr(), _stream_handle(stream, self.device)))
         return out
 
     def forward_attenuated(self, img: torch.Tensor, mu: torch.Tensor, out: torch.Tensor | None = None,
@@ -175,7 +178,7 @@ class Plan:
             out = torch.empty(self.sino_shape, dtype=torch.float32, device=img.device)
         self._check_dev(out, self.sino_shape, "sino")
         check(self._lib.xrt_forward_attenuated(self._h, img.data_ptr(), mu.data_ptr(), out.data_ptr(),
-                                               _stream_handle(stream)))
+                                               _stream_handle(stream, self.device)))
         return out
 
     def adjoint_attenuated(self, sino: torch.Tensor, mu: torch.Tensor, out: torch.Tensor | None = None,
@@ -187,24 +190,33 @@ class Plan:
             out = torch.empty(self.image_shape, dtype=torch.float32, device=sino.device)
         self._check_dev(out, self.image_shape, "img")
         check(self._lib.xrt_adjoint_attenuated(self._h, sino.data_ptr(), mu.data_ptr(), out.data_ptr(),
-                                               _stream_handle(stream)))
+                                               _stream_handle(stream, self.device)))
         return out
+
+    @staticmethod
+    def _check_host(t: torch.Tensor, shape, name):
+        """The C side copies exactly prod(shape) floats through the raw pointer: check it all."""
+        if t.is_cuda or t.dtype != torch.float32 or not t.is_contiguous():
+            raise ValueError(f"{name} must be a contiguous float32 CPU tensor")
+        if t.numel() != int(np.prod(shape)):
+            raise ValueError(f"{name} has {t.numel()} elements, expected {shape}")
 
     def forward_host(self, img: torch.Tensor, out: torch.Tensor | None = None, stream=None) -> torch.Tensor:
         """xrt_forward_host: host (ideally pinned) fp32 buffers, copies inside the call."""
-        if img.is_cuda or img.dtype != torch.float32 or not img.is_contiguous():
-            raise ValueError("img must be a contiguous float32 CPU tensor")
+        self._check_host(img, self.image_shape, "img")
         if out is None:
             out = torch.empty(self.sino_shape, dtype=torch.float32, pin_memory=True)
-        check(self._lib.xrt_forward_host(self._h, img.data_ptr(), out.data_ptr(), _stream_handle(stream)))
+        self._check_host(out, self.sino_shape, "sino")
+        check(self._lib.xrt_forward_host(self._h, img.data_ptr(), out.data_ptr(), _stream_handle(stream, self.device)))
         return out
 
     def adjoint_host(self, sino: torch.Tensor, out: torch.Tensor | None = None, stream=None) -> torch.Tensor:
-        if sino.is_cuda or sino.dtype != torch.float32 or not sino.is_contiguous():
-            raise ValueError("sino must be a contiguous float32 CPU tensor")
+        """xrt_adjoint_host: host buffers, copies inside the call."""
+        self._check_host(sino, self.sino_shape, "sino")
         if out is None:
             out = torch.empty(self.image_shape, dtype=torch.float32, pin_memory=True)
-        check(self._lib.xrt_adjoint_host(self._h, sino.data_ptr(), out.data_ptr(), _stream_handle(stream)))
+        self._check_host(out, self.image_shape, "img")
+        check(self._lib.xrt_adjoint_host(self._h, sino.data_ptr(), out.data_ptr(), _stream_handle(stream, self.device)))
         return out
 
     def ray_units(self, ray_begin: int, ray_end: int, stream=None):
@@ -213,7 +225,7 @@ class Plan:
         dev = torch.device("cuda", self.device)
         row_ptr = torch.empty(max(n, 0) + 1, dtype=torch.int64, device=dev)
         nnz = ctypes.c_int64()
-        sh = _stream_handle(stream)
+        sh = _stream_handle(stream, self.device)
         check(self._lib.xrt_ray_units(self._h, int(ray_begin), int(ray_end), row_ptr.data_ptr(), None, None,
                                       0, ctypes.byref(nnz), sh))
         cols = torch.empty(max(nnz.value, 1), dtype=torch.int64, device=dev)
