@@ -33,6 +33,11 @@
  * mode 1 = separable early-out: a (k, j) pair whose z/y-interval overlap is <= tau is
  *          skipped before the i loop.  Identical output (the full overlap of such a box
  *          is <= that partial overlap <= tau, so mode 0 drops it too); tested equal.
+ * mode 2 = mode 1, and the i loop visits only the cells whose x-slab can meet the (k, j)
+ *          overlap [lo, hi]: floor(u_x(lo)) - 1 .. floor(u_x(hi)) + 1 (the slab intervals are
+ *          monotone in i; the margin of one cell absorbs rounding).  A skipped box has an
+ *          x-interval disjoint from [lo, hi], i.e. l <= 0, so mode 0 drops it too; tested equal.
+ *          (Used for the full-sinogram sweeps of the 2D fan beam, SURVEY 8(c) reading 21.)
  */
 #include <math.h>
 #include <stdint.h>
@@ -112,8 +117,24 @@ static void ray_row(const oracle_grid* g, const double* p, const double* th, dou
             if (!T->ok[1][j]) continue;
             double lo_kj = fmax(T->lo[2][k], T->lo[1][j]);
             double hi_kj = fmin(T->hi[2][k], T->hi[1][j]);
-            if (mode == 1 && !(hi_kj - lo_kj > tau)) continue;
-            for (int64_t i = 0; i < nx; ++i) {
+            if (mode >= 1 && !(hi_kj - lo_kj > tau)) continue;
+            int64_t i0 = 0, i1 = nx;
+            if (mode == 2) {
+                if (w[0] == 0.0) {
+                    i0 = (int64_t)floor(u0[0]) - 1;
+                    i1 = i0 + 3;
+                } else {
+                    /* (lo, hi) may be infinite when the y and z axes are both fixed */
+                    const double lim = (double)nx + 4.0;
+                    const double ua = fmin(fmax(u0[0] + w[0] * lo_kj, -4.0), lim);
+                    const double ub = fmin(fmax(u0[0] + w[0] * hi_kj, -4.0), lim);
+                    i0 = (int64_t)floor(fmin(ua, ub)) - 1;
+                    i1 = (int64_t)floor(fmax(ua, ub)) + 2;
+                }
+                if (i0 < 0) i0 = 0;
+                if (i1 > nx) i1 = nx;
+            }
+            for (int64_t i = i0; i < i1; ++i) {
                 if (!T->ok[0][i]) continue;
                 double c_low = fmax(lo_kj, T->lo[0][i]);
                 double c_up = fmin(hi_kj, T->hi[0][i]);

@@ -98,9 +98,10 @@ def test_modes_agree_and_sorted():
     c = grid((6, 7, 5), (1.0, 0.9, 1.1))
     p, th = random_rays(c, 200, RNG, 3)
     a = oracle.rows(c, p, th, mode=0)
-    b = oracle.rows(c, p, th, mode=1)
-    for x, y in zip(a, b):
-        assert np.array_equal(x, y)
+    for mode in (1, 2):
+        b = oracle.rows(c, p, th, mode=mode)
+        for x, y in zip(a, b):
+            assert np.array_equal(x, y), mode
     rp, cols, lens = a
     for m in range(len(p)):
         seg = cols[rp[m]:rp[m + 1]]
@@ -108,6 +109,29 @@ def test_modes_agree_and_sorted():
     assert np.all(lens > 0)
     # max length per unit = the unit diagonal
     assert np.all(lens <= math.sqrt(1.0 + 0.81 + 1.21) + 1e-12)
+
+
+@pytest.mark.parametrize("n,dim", [((9, 8, 1), 2), ((7, 6, 5), 3)])
+def test_mode2_agrees_on_edge_rays(n, dim):
+    """Mode 2 (x-range restricted) = mode 0 also for rays on grid lines / planes and through
+    corners (axis-parallel and diagonal rays at integer offsets: the tie cases of reading 2)."""
+    c = grid(n, (1.0, 1.0, 1.0))
+    pts, dirs = [], []
+    for s in np.arange(-5, 5.5, 0.5):
+        for th in ((1, 0, 0), (0, 1, 0), (1, 1, 0), (1, -1, 0), (0, 0, 1), (1, 0, 1), (1, 1, 1)):
+            if dim == 2 and th[2] != 0:
+                continue
+            t = np.array(th, dtype=float) / np.linalg.norm(th)
+            off = np.array([s, -s, 0.0 if dim == 2 else s * 0.5])
+            pts.append(off)
+            dirs.append(t)
+    p, th = np.array(pts), np.array(dirs)
+    a = oracle.rows(c, p, th, mode=0)
+    b = oracle.rows(c, p, th, mode=2)
+    for x, y in zip(a, b):
+        assert np.array_equal(x, y)
+    img = RNG.uniform(0, 1, size=int(np.prod(n))).astype(np.float32)
+    assert np.array_equal(oracle.forward(c, img, p, th, mode=0), oracle.forward(c, img, p, th, mode=2))
 
 
 def test_adjoint_identity():
