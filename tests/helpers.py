@@ -34,19 +34,32 @@ def ray_ids_all(c):
     return np.arange(workloads.configs.n_rays(c), dtype=np.int64)
 
 
-def oracle_csr(c, ids):
+def oracle_csr(c, ids, mode=2):
     p, th = G.rays(c, ids)
-    return oracle.rows(c, p, th, mode=1)
+    return oracle.rows(c, p, th, mode=mode)
 
 
-def oracle_forward(c, img_cpu, ids):
+def oracle_forward(c, img_cpu, ids, mode=2):
     p, th = G.rays(c, ids)
-    return oracle.forward(c, img_cpu.numpy().reshape(-1), p, th, mode=1)
+    return oracle.forward(c, img_cpu.numpy().reshape(-1), p, th, mode=mode)
 
 
-def oracle_adjoint(c, y, ids):
+def stratified_ranges(c, n_ranges: int, width: int, seed: int):
+    """Reading 21: n_ranges ranges of `width` consecutive ray ids, one per stratum of the ray-id
+    space (uniform over (view, row, column)); returns the list of (begin, end)."""
+    M = workloads.configs.n_rays(c)
+    rng = np.random.Generator(np.random.PCG64(seed))
+    edges = np.linspace(0, M - width, n_ranges + 1).astype(np.int64)
+    out = []
+    for a, b in zip(edges[:-1], edges[1:]):
+        s = int(rng.integers(a, max(a + 1, b)))
+        out.append((s, s + width))
+    return out
+
+
+def oracle_adjoint(c, y, ids, mode=2):
     p, th = G.rays(c, ids)
-    return oracle.adjoint(c, y, p, th, mode=1)
+    return oracle.adjoint(c, y, p, th, mode=mode)
 
 
 def compare_csr(gpu, ref, ids_desc=""):

@@ -60,17 +60,19 @@ def test_csr_small_every_ray(cuda_ok, idx):
 
 
 @pytest.mark.parametrize("idx", [1, 2, 3, 4, 5])
-def test_csr_full_size_sampled(cuda_ok, idx):
+def test_csr_full_size(cuda_ok, idx):
+    """Reading 21: every ray of the full cfg 1 and cfg 2 sinograms; 4096 rays of cfg
+    3 / 4 / 5 in 256 stratified ranges of 16 consecutive ids (uniform over view, row, column)."""
     c = workloads.config(idx)
     p = _plan(c)
-    rng = np.random.Generator(np.random.PCG64(100 + idx))
     M = p.n_rays
-    n_ranges, width = (4, 64) if idx in (1, 2) else (4, 24)
-    for _ in range(n_ranges):
-        a = int(rng.integers(0, M - width))
-        gpu = p.ray_units(a, a + width)
-        ref = H.oracle_csr(c, np.arange(a, a + width))
-        H.compare_csr(gpu, ref, f"cfg{idx} rays [{a},{a + width})")
+    if idx in (1, 2):
+        step = 36 * c["det_rows"] * c["det_cols"]           # 36 views per call
+        ranges = [(a, min(M, a + step)) for a in range(0, M, step)]
+    else:
+        ranges = H.stratified_ranges(c, 256, 16, seed=100 + idx)
+    for a, b in ranges:
+        H.compare_csr(p.ray_units(a, b), H.oracle_csr(c, np.arange(a, b)), f"cfg{idx} rays [{a},{b})")
 
 
 def test_csr_constructed_rays(cuda_ok):
@@ -127,20 +129,23 @@ def test_forward_small_every_ray(cuda_ok, idx, algo):
 
 @pytest.mark.parametrize("algo", ALGOS)
 @pytest.mark.parametrize("idx", [1, 2, 3, 4, 5])
-def test_forward_full_size_sampled(cuda_ok, idx, algo):
-    """Full BASELINE size in the launch configuration bench.py times; sampled rays vs oracle."""
+def test_forward_full_size(cuda_ok, idx, algo):
+    """Full BASELINE size in the launch configuration bench.py times: every ray of cfg 1 / 2, 4096
+    stratified rays of cfg 3 / 4 / 5 (reading 21).  The tolerance scale is the ORACLE's max over
+    the rays checked (never the GPU output; for a sample it is <= max|sino|, so the bar is
+    stricter than north_star's)."""
     c = workloads.config(idx)
     p = _plan(c, algo)
     img = _image(c)
     sino = p.forward(img)
     torch.cuda.synchronize()
-    n = {1: 8640, 2: 1500, 3: 600, 4: 300, 5: 400}[idx]
-    ids = workloads.sample_rays(c, n, seed=200 + idx)
+    if idx in (1, 2):
+        ids = H.ray_ids_all(c)
+    else:
+        ids = np.concatenate([np.arange(a, b) for a, b in H.stratified_ranges(c, 256, 16, seed=200 + idx)])
     ref = H.oracle_forward(c, img.cpu(), ids)
     got = sino.reshape(-1)[torch.from_numpy(ids).cuda()].cpu().numpy()
-    # normalise by the max of the full GPU sinogram (the oracle only sees a sample)
-    scale = float(sino.abs().max())
-    err = H.fwd_err(got, ref, scale=scale)
+    err = H.fwd_err(got, ref)
     assert err <= H.FWD_TOL, err
 
 
@@ -190,11 +195,11 @@ def test_adjoint_small_sparse_parity(cuda_ok, idx, algo):
 
 
 @pytest.mark.parametrize("algo", ADJ_ALGOS)
-@pytest.mark.parametrize("idx", [2, 4, 5])
+@pytest.mark.parametrize("idx", [2, 3, 4, 5])
 def test_adjoint_full_size_sparse_parity(cuda_ok, idx, algo):
     c = workloads.config(idx)
     p = _plan(c, algo)
-    ids = workloads.sample_rays(c, {2: 800, 4: 120, 5: 200}[idx], seed=500 + idx)
+    ids = workloads.sample_rays(c, {2: 4000, 3: 4096, 4: 1024, 5: 2048}[idx], seed=500 + idx)
     y = torch.zeros(p.n_rays, dtype=torch.float32, device="cuda")
     rng = np.random.Generator(np.random.PCG64(600 + idx))
     yv = rng.uniform(-1, 1, size=ids.size).astype(np.float32)
@@ -207,8 +212,16 @@ def test_adjoint_full_size_sparse_parity(cuda_ok, idx, algo):
 
 @pytest.mark.parametrize("algo", ADJ_ALGOS)
 @pytest.mark.parametrize("idx", [1, 2, 3, 4, 5])
-def test_dot_product(cuda_ok, idx, algo):
-    c = H.small_config(idx) if idx in (3, 4, 5) else workloads.config(idx)
+@pytest.mark.parametrize("size", ["small", "full"])
+def test_dot_product(cuda_ok, idx, algo, size):
+    """<A x, y> = <x, A^T y> with fp64 sums of the fp32 GPU outputs, to 1e-5 of
+    ||Ax|| ||y|| + ||x|| ||A^T y||: oracle-sized and FULL size (cfg 4: ~1630 fp32 atomic
+    contributions per voxel in the scatter adjoint).  The gather adjoint at full cfg 3 / 4 / 5 takes
+    seconds per call (it is not AUTO); its full-size case runs on cfg 1 / 2 only."""
+    if size == "full" and algo == "gather" and idx in (3, 4, 5):
+        pytest.skip("full-size gather: covered on cfg 1 / 2 (seconds per call on the 3D configs)")
+    c = (H.small_config(idx) if idx in (3, 4, 5) else workloads.config(idx)) if size == "small" \
+        else workloads.config(idx)
     p = _plan(c, algo)
     x = _image(c)
     y = workloads.make_sino_input(c, device="cuda")
@@ -218,6 +231,19 @@ def test_dot_product(cuda_ok, idx, algo):
     rhs = float((x.double() * Aty.double()).sum())
     scale = float(Ax.double().norm() * y.double().norm() + x.double().norm() * Aty.double().norm())
     assert abs(lhs - rhs) <= H.DOT_TOL * scale, (lhs, rhs)
+
+
+def test_tiled_forward_reproducible(cuda_ok):
+    """The xy-tiled forward adds a ray's per-tile partial sums with red.global.add (order not fixed):
+    repeated full-size cfg 4 forwards agree to fp32 reassociation of <= 9 partial sums (DESIGN.md
+    section 6), far inside the 1e-5 bar."""
+    c = workloads.config(4)
+    p = _plan(c)
+    x = _image(c)
+    a = p.forward(x).clone()
+    b = p.forward(x)
+    scale = float(a.abs().max())
+    assert float((a - b).abs().max()) <= 4e-7 * scale
 
 
 # ------------------------------------------------------------------- host-buffer path
