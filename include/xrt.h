@@ -164,6 +164,20 @@ xrt_status xrt_forward(xrt_plan p, const float* img, float* sino, void* cuda_str
  * overwritten with A^T sino. */
 xrt_status xrt_adjoint(xrt_plan p, const float* sino, float* img, void* cuda_stream);
 
+/* Staged adjoint, for overlapping a multi-GPU reduction of the image with the backprojection
+ * (rays are independent).  The COLUMN adjoint runs band-major over blocks of
+ * detector rows, each a z slab of the image (bands in row order: monotone in z).  xrt_adjoint_stages
+ * reports S stages and, per stage s, the image rows [k_begin[s], k_end[s]) of [N_z][N_y][N_x] that
+ * are FINAL after stage s (no later band reaches them; conservative, 2-cell margin); the ranges are
+ * disjoint and cover [0, N_z) (an empty range: begin == end).  k_begin / k_end: host arrays of
+ * capacity >= S, or both NULL to query S only.  xrt_adjoint_stage(p, sino, img, s, stream), called
+ * for s = 0 .. S-1 in order on one stream, adds stage s's rows and writes img[k_begin[s]:k_end[s]]
+ * (fully overwritten); after stage S-1 img = A^T sino, identical to xrt_adjoint.  A caller can
+ * reduce img[k_begin[s]:k_end[s]] across ranks while stage s+1 computes.  Algorithms other than the
+ * 3D COLUMN adjoint: S = 1 (the whole image).  Errors: XRT_ERR_INVALID_ARG (NULL, stage out of range). */
+xrt_status xrt_adjoint_stages(xrt_plan p, int32_t* n_stages, int64_t* k_begin, int64_t* k_end);
+xrt_status xrt_adjoint_stage(xrt_plan p, const float* sino, float* img, int32_t stage, void* cuda_stream);
+
 /* fp64 variants (the paper's "switching float ... into double"): the same
  * operator with the fp64 unit enumeration of xrt_ray_units (units with l <= tau dropped) and fp64
  * sums.  img: device fp64 [N_z][N_y][N_x]; sino: device fp64 [n_views][det_rows][det_cols]; the

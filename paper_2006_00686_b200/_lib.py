@@ -26,7 +26,8 @@ ALGOS = {"auto": 0, "ray": 1, "column": 2, "gather": 3}
 EXPORTS = ("xrt_plan_create", "xrt_plan_create_rays", "xrt_plan_destroy", "xrt_plan_query", "xrt_plan_set_algorithm",
            "xrt_plan_launch_count", "xrt_forward", "xrt_adjoint", "xrt_forward_host",
            "xrt_adjoint_host", "xrt_forward_f64", "xrt_adjoint_f64",
-           "xrt_forward_attenuated", "xrt_adjoint_attenuated", "xrt_ray_units", "xrt_last_error", "xrt_version")
+           "xrt_forward_attenuated", "xrt_adjoint_attenuated", "xrt_ray_units", "xrt_last_error", "xrt_version",
+           "xrt_adjoint_stages", "xrt_adjoint_stage")
 
 
 class XrtGeometry(ctypes.Structure):
@@ -91,6 +92,8 @@ def load(path: str | None = None) -> ctypes.CDLL:
             "xrt_ray_units": (i32, [vp, i64, i64, vp, vp, vp, i64, ip, vp]),
             "xrt_last_error": (ctypes.c_char_p, []),
             "xrt_version": (i32, []),
+            "xrt_adjoint_stages": (i32, [vp, ctypes.POINTER(i32), ip, ip]),
+            "xrt_adjoint_stage": (i32, [vp, vp, vp, i32, vp]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(lib, name)

@@ -149,6 +149,38 @@ int64_t column_zpad(const xrt_geometry* g, const xrt::GridC& G) {
     return pad + 4;
 }
 
+// Physical z range [zlo, zhi] that the rays of detector rows [r0, r1] can reach (all views): z of a
+// ray at in-plane distance rho from the source (divergent) or in-plane arc sigma (parallel) is affine
+// in the row coordinate v, so the extreme rows and extreme rho bound it (+ the helical H range).
+static void band_z_range(const xrt_geometry* g, const xrt::GridC& G, int64_t r0, int64_t r1, double& zlo,
+                         double& zhi) {
+    const double hx = G.n[0] * G.d[0] / 2 + std::fabs(g->center[0]);
+    const double hy = G.n[1] * G.d[1] / 2 + std::fabs(g->center[1]);
+    const double R = std::sqrt(hx * hx + hy * hy);
+    const double v0 = (r0 - (g->det_rows - 1) / 2.0) * g->det_spacing[1] + g->det_offset[1];
+    const double v1 = (r1 - (g->det_rows - 1) / 2.0) * g->det_spacing[1] + g->det_offset[1];
+    if (g->beam == XRT_PAR3D) {
+        const double c2 = std::cos(g->tilt), t2 = std::fabs(std::tan(g->tilt));
+        zlo = std::min(v0, v1) / c2 - R * t2;
+        zhi = std::max(v0, v1) / c2 + R * t2;
+        return;
+    }
+    const double rmin = std::max(0.0, g->sod - R), rmax = g->sod + R;
+    const double a[4] = {v0 * rmin / g->sdd, v0 * rmax / g->sdd, v1 * rmin / g->sdd, v1 * rmax / g->sdd};
+    zlo = std::min(std::min(a[0], a[1]), std::min(a[2], a[3]));
+    zhi = std::max(std::max(a[0], a[1]), std::max(a[2], a[3]));
+    if (g->beam == XRT_HELICAL) {
+        double hmin = INFINITY, hmax = -INFINITY;
+        for (int64_t v = 0; v < g->n_views; ++v) {
+            const double H = g->z0 + g->pitch * g->angles[v] / (2.0 * M_PI);
+            hmin = std::min(hmin, H);
+            hmax = std::max(hmax, H);
+        }
+        zlo += hmin;
+        zhi += hmax;
+    }
+}
+
 // Largest number of z cells that the rays of one band of `band_rows` detector rows can reach inside
 // the image (over all views).  z of a ray at in-plane distance rho from the source (divergent) or at
 // in-plane arc sigma (parallel) is affine in the row coordinate v, so the extreme rows and extreme
@@ -521,6 +553,54 @@ xrt_status plan_create_impl(const xrt_geometry* g, int cuda_device, xrt_plan* ou
             xrt_plan_destroy(p);
             return cuda_fail(e, "plan workspace");
         }
+        // staged adjoint (xrt_adjoint_stages): band b of the adjoint touches image rows
+        // [klo_b, khi_b] (conservative, 2-cell margin); rows no later band touches are final after b.
+        // Bands run in row order, i.e. monotone in z; a non-monotone tail folds into the last stage.
+        const int nb = xrt::column_bands(p, true), rb = xrt::column_band_rows(p, true);
+        std::vector<int64_t> klo(nb), khi(nb);
+        for (int b = 0; b < nb; ++b) {
+            double zlo, zhi;
+            band_z_range(g, G, (int64_t)b * rb, std::min<int64_t>(g->det_rows, (int64_t)(b + 1) * rb) - 1, zlo, zhi);
+            klo[b] = std::max<int64_t>(0, (int64_t)std::floor((G.z_hi - zhi) / G.d[2]) - 2);
+            khi[b] = std::min<int64_t>(G.n[2] - 1, (int64_t)std::floor((G.z_hi - zlo) / G.d[2]) + 2);
+        }
+        std::vector<char> done((size_t)G.n[2], 0);
+        p->adj_stage_k.assign(2 * (size_t)nb, 0);
+        for (int b = 0; b < nb; ++b) {
+            std::vector<char> later((size_t)G.n[2], 0);
+            for (int b2 = b + 1; b2 < nb; ++b2)
+                for (int64_t k = klo[b2]; k <= khi[b2]; ++k) later[(size_t)k] = 1;
+            int64_t k0 = -1, k1 = -1;
+            bool ok = true;
+            for (int64_t k = 0; k < G.n[2]; ++k) {
+                if (done[(size_t)k] || later[(size_t)k]) continue;
+                if (k0 < 0) k0 = k;
+                else if (k != k1) ok = false;       // not one contiguous range: defer
+                k1 = k + 1;
+            }
+            if (!ok || k0 < 0) { p->adj_stage_k[2 * b] = p->adj_stage_k[2 * b + 1] = 0; continue; }
+            for (int64_t k = k0; k < k1; ++k) done[(size_t)k] = 1;
+            p->adj_stage_k[2 * b] = k0;
+            p->adj_stage_k[2 * b + 1] = k1;
+        }
+        // the last stage finishes everything left (deferred ranges included): check contiguity
+        int64_t k0 = -1, k1 = -1;
+        bool ok = true;
+        for (int64_t k = 0; k < G.n[2]; ++k) {
+            if (done[(size_t)k]) continue;
+            if (k0 < 0) k0 = k;
+            else if (k != k1) ok = false;
+            k1 = k + 1;
+        }
+        if (!ok) {   // fall back to one stage
+            p->adj_stage_k.assign(2 * (size_t)nb, 0);
+            p->adj_stage_k[2 * (nb - 1)] = 0;
+            p->adj_stage_k[2 * (nb - 1) + 1] = G.n[2];
+        } else if (k0 >= 0) {
+            const int64_t a = p->adj_stage_k[2 * (nb - 1)], bnd = p->adj_stage_k[2 * (nb - 1) + 1];
+            p->adj_stage_k[2 * (nb - 1)] = bnd > a ? std::min(a, k0) : k0;
+            p->adj_stage_k[2 * (nb - 1) + 1] = bnd > a ? std::max(bnd, k1) : k1;
+        }
     }
     *out = p;
     return XRT_OK;
@@ -729,6 +809,43 @@ xrt_status xrt_adjoint_attenuated(xrt_plan p, const float* sino, const float* mu
         p->launches += 1;
     }
     if (e != cudaSuccess) return cuda_fail(e, "adjoint_attenuated launch");
+    return XRT_OK;
+}
+
+xrt_status xrt_adjoint_stages(xrt_plan p, int32_t* n_stages, int64_t* k_begin, int64_t* k_end) {
+    if (!p || !n_stages) return fail(XRT_ERR_INVALID_ARG, "NULL argument");
+    const bool staged = resolve(p, XRT_OP_ADJOINT) == XRT_ALGO_COLUMN && p->dim == 3 && !p->adj_stage_k.empty();
+    const int32_t S = staged ? (int32_t)(p->adj_stage_k.size() / 2) : 1;
+    *n_stages = S;
+    if (k_begin && k_end) {
+        for (int32_t s = 0; s < S; ++s) {
+            k_begin[s] = staged ? p->adj_stage_k[2 * s] : 0;
+            k_end[s] = staged ? p->adj_stage_k[2 * s + 1] : p->grid.n[2];
+        }
+    }
+    return XRT_OK;
+}
+
+xrt_status xrt_adjoint_stage(xrt_plan p, const float* sino, float* img, int32_t stage, void* cuda_stream) {
+    if (!p || !img || !sino) return fail(XRT_ERR_INVALID_ARG, "NULL argument");
+    DevGuard guard(p->device);
+    cudaStream_t s = (cudaStream_t)cuda_stream;
+    const bool staged = resolve(p, XRT_OP_ADJOINT) == XRT_ALGO_COLUMN && p->dim == 3 && !p->adj_stage_k.empty();
+    const int32_t S = staged ? (int32_t)(p->adj_stage_k.size() / 2) : 1;
+    if (stage < 0 || stage >= S) return fail(XRT_ERR_INVALID_ARG, "stage %d outside [0, %d)", stage, S);
+    if (!staged) return xrt_adjoint(p, sino, img, cuda_stream);
+    xrt_status st = XRT_OK;
+    if (stage == 0) st = adj_begin(p, img, s);
+    if (st != XRT_OK) return st;
+    cudaError_t e = xrt::launch_adjoint_column_bands(p, sino, p->d_work_adj, stage, stage + 1, s);
+    p->launches += 1;
+    if (e != cudaSuccess) return cuda_fail(e, "adjoint stage launch");
+    const int64_t k0 = p->adj_stage_k[2 * stage], k1 = p->adj_stage_k[2 * stage + 1];
+    if (k1 > k0) {
+        e = xrt::launch_from_zfast_rows(p, p->d_work_adj, img, k0, k1, s);
+        p->launches += 1;
+        if (e != cudaSuccess) return cuda_fail(e, "transpose launch");
+    }
     return XRT_OK;
 }
 

@@ -1600,6 +1600,12 @@ namespace {
 
 }  // namespace
 
+// padded z-fastest work [N_xy][NzP] -> image rows [k0, k1) of [N_z][N_xy] (staged adjoint)
+cudaError_t launch_from_zfast_rows(const xrt_plan_s* p, const float* work, float* img, int64_t k0, int64_t k1,
+                                   cudaStream_t s) {
+    return transpose(work, img + k0 * p->grid.nxy, p->grid.nxy, k1 - k0, p->nzp, p->zpad + k0, p->grid.nxy, 0, s);
+}
+
 // image [N_z][N_xy] -> padded z-fastest work [N_xy][NzP] (interior rows pad .. pad + N_z)
 cudaError_t launch_to_zfast(const xrt_plan_s* p, const float* img, float* work, cudaStream_t s) {
     return transpose(img, work, p->grid.n[2], p->grid.nxy, p->grid.nxy, 0, p->nzp, p->zpad, s);

@@ -211,6 +211,7 @@ __device__ __forceinline__ bool setup_ray(const ViewRec& V, const DetC& dc, cons
 }  // namespace xrt
 
 // ---------------------------------------------------------------------------------- host side
+#include <vector>
 struct xrt_plan_s {
     int device = 0;
     int beam = 0;
@@ -252,6 +253,7 @@ struct xrt_plan_s {
     int algo_fwd = XRT_ALGO_AUTO;
     int algo_adj = XRT_ALGO_AUTO;
     bool column_ok = false;            // geometry admits the column-shared kernels
+    std::vector<int64_t> adj_stage_k;  // staged adjoint: per band b, image rows [k0, k1) final after b
     int64_t launches = 0;
 };
 
@@ -287,6 +289,8 @@ cudaError_t launch_units_fill(const xrt_plan_s* p, int64_t ray0, int64_t ray1,
 // kernels (kern_column.cu)
 cudaError_t launch_to_zfast(const xrt_plan_s* p, const float* img, float* work, cudaStream_t s);
 cudaError_t launch_from_zfast(const xrt_plan_s* p, const float* work, float* img, cudaStream_t s);
+cudaError_t launch_from_zfast_rows(const xrt_plan_s* p, const float* work, float* img, int64_t k0, int64_t k1,
+                                   cudaStream_t s);
 cudaError_t launch_forward_column(const xrt_plan_s* p, const float* vol_zfast, float* sino,
                                   int64_t v0, int64_t v1, cudaStream_t s);
 cudaError_t launch_adjoint_column(const xrt_plan_s* p, const float* sino, float* vol_zfast,

@@ -7,7 +7,12 @@ One process per GPU.  Rank r of G owns the contiguous view block
 * forward: every rank projects its block into its own sinogram slab -- no exchange when x
   is already replicated; ``forward`` can broadcast x from ``src`` first (NCCL).
 * adjoint: every rank backprojects its slab into a partial image; the partials are summed
-  with one NCCL all_reduce (the path's only real exchange step).
+  with NCCL all_reduce (the path's only real exchange step).  With the staged adjoint
+  (xrt_adjoint_stages / xrt_adjoint_stage) each z slab of the image is reduced as soon as no later
+  band of detector rows can reach it, overlapping the reduction with the remaining bands.
+* helical (cfg 5): a contiguous view block sees only a z window of the image (the source rises
+  with the angle), so ``adjoint_windowed`` exchanges only the overlaps of neighbouring windows
+  (P2P) and ``forward`` needs x only on the window -- traffic ~ overlap, not image size.
 
 The process group is torch.distributed's (backend "nccl" on GPUs; "gloo" for the CPU tests
 of the sharding logic).
@@ -49,6 +54,7 @@ class ShardedPlan:
         if world is None:
             world = dist.get_world_size(group) if dist.is_initialized() else 1
         self.rank, self.world, self.group = rank, world, group
+        self.full_geometry = geometry
         self.geometry = shard_geometry(geometry, rank, world)
         self.view_block = self.geometry["view_block"]
         if plan_factory is None:
@@ -62,12 +68,80 @@ class ShardedPlan:
             dist.broadcast(img, src=broadcast_src, group=self.group)
         return self.plan.forward(img, out=out)
 
-    def adjoint(self, sino_slab: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
-        """A^T y of the FULL sinogram (replicated on every rank): local partial + all_reduce(sum)."""
+    def adjoint(self, sino_slab: torch.Tensor, out: torch.Tensor | None = None, overlap: bool = True) -> torch.Tensor:
+        """A^T y of the FULL sinogram (replicated on every rank): local partial + all_reduce(sum).
+        overlap: run the staged adjoint and all-reduce each final z slab asynchronously while the
+        next band computes (same result up to fp32 reassociation of the reduction)."""
+        if self.world == 1 or not overlap or not hasattr(self.plan, "adjoint_stages"):
+            part = self.plan.adjoint(sino_slab, out=out)
+            if self.world > 1:
+                dist.all_reduce(part, op=dist.ReduceOp.SUM, group=self.group)
+            return part
+        if out is None:
+            out = torch.empty(self.plan.image_shape, dtype=sino_slab.dtype, device=sino_slab.device)
+        works = []
+        for s, (k0, k1) in enumerate(self.plan.adjoint_stages()):
+            self.plan.adjoint_stage(sino_slab, out, s)
+            if k1 > k0:
+                works.append(dist.all_reduce(out[k0:k1], op=dist.ReduceOp.SUM, group=self.group, async_op=True))
+        for w in works:
+            w.wait()
+        return out
+
+    # ---------------------------------------------------------------- helical z windows
+    def window(self, rank: int | None = None) -> tuple[int, int]:
+        """Image rows [k0, k1) that the rays of ``rank``'s view block can reach (conservative)."""
+        r = self.rank if rank is None else rank
+        return zwindow(shard_geometry(self.full_geometry, r, self.world))
+
+    def adjoint_windowed(self, sino_slab: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
+        """A^T y restricted to this rank's z window: the local partial plus the overlapping rows of
+        the other ranks' partials (P2P, only the overlaps travel).  Rows outside the window hold this
+        rank's partial (zero: no ray of the block reaches them)."""
         part = self.plan.adjoint(sino_slab, out=out)
-        if self.world > 1:
-            dist.all_reduce(part, op=dist.ReduceOp.SUM, group=self.group)
+        if self.world == 1:
+            return part
+        k0, k1 = self.window()
+        ops, bufs = [], []
+        for q in range(self.world):
+            if q == self.rank:
+                continue
+            a0, a1 = self.window(q)
+            lo, hi = max(k0, a0), min(k1, a1)
+            if hi <= lo:
+                continue
+            buf = torch.empty_like(part[lo:hi])
+            ops.append(dist.P2POp(dist.isend, part[lo:hi].contiguous(), q, group=self.group))
+            ops.append(dist.P2POp(dist.irecv, buf, q, group=self.group))
+            bufs.append((lo, hi, buf))
+        if ops:
+            for w in dist.batch_isend_irecv(ops):
+                w.wait()
+        for lo, hi, buf in bufs:
+            part[lo:hi] += buf
         return part
+
+    def scatter_windows(self, img: torch.Tensor, src: int = 0) -> torch.Tensor:
+        """Send every rank the rows of ``img`` (valid on ``src``) in its z window (P2P): the
+        windowed counterpart of broadcasting x before the forward."""
+        if self.world == 1:
+            return img
+        ops = []
+        if self.rank == src:
+            for q in range(self.world):
+                if q != src:
+                    a0, a1 = self.window(q)
+                    ops.append(dist.P2POp(dist.isend, img[a0:a1].contiguous(), q, group=self.group))
+        else:
+            k0, k1 = self.window()
+            buf = torch.empty_like(img[k0:k1])
+            ops.append(dist.P2POp(dist.irecv, buf, src, group=self.group))
+        if ops:
+            for w in dist.batch_isend_irecv(ops):
+                w.wait()
+        if self.rank != src:
+            img[k0:k1] = buf
+        return img
 
     def forward_attenuated(self, img: torch.Tensor, mu: torch.Tensor, out: torch.Tensor | None = None,
                            broadcast_src: int | None = None):
@@ -85,6 +159,40 @@ class ShardedPlan:
         if self.world > 1:
             dist.all_reduce(part, op=dist.ReduceOp.SUM, group=self.group)
         return part
+
+
+def zwindow(g: dict) -> tuple[int, int]:
+    """Image rows [k0, k1) (of [N_z][N_y][N_x]) that any ray of geometry ``g`` can reach: z of a ray
+    at in-plane distance rho from the source is affine in the row coordinate v (cone / helical:
+    z = H + v rho / sdd, P:631-661 with reading 8), so the extreme rows, the extreme rho over the image
+    square and the extreme source heights of the views bound it; parallel beams: v / cos(tilt) +-
+    R tan(tilt).  Two-cell margin (conservative; rows outside receive nothing)."""
+    nx, ny, nz = (int(v) for v in g["n"])
+    dx, dy, dz = (float(v) for v in g["spacing"])
+    cx, cy, cz = g.get("center", (0.0, 0.0, 0.0))
+    if g["beam"] in ("par2d", "fan2d"):
+        return 0, 1
+    R = float(np.hypot(nx * dx / 2 + abs(cx), ny * dy / 2 + abs(cy)))
+    rows = int(g["det_rows"])
+    dv = float(g["det_spacing"][1])
+    off = float(g.get("det_offset", (0.0, 0.0))[1])
+    v = np.array([-(rows - 1) / 2.0, (rows - 1) / 2.0]) * dv + off
+    ang = np.asarray(g["angles"], dtype=np.float64)
+    if g["beam"] == "par3d":
+        t = float(g.get("tilt", 0.0))
+        z = np.concatenate([v / np.cos(t) - R * abs(np.tan(t)), v / np.cos(t) + R * abs(np.tan(t))])
+    else:
+        sod, sdd = float(g["sod"]), float(g["sdd"])
+        rho = np.array([max(0.0, sod - R), sod + R])
+        H = np.zeros(1)
+        if g["beam"] == "helical":
+            H = float(g["z0"]) + float(g["pitch"]) * ang / (2 * np.pi)
+        zz = np.outer(v, rho).ravel() / sdd
+        z = np.concatenate([zz + H.min(), zz + H.max()])
+    z_hi = float(cz) + nz * dz / 2.0
+    k0 = int(np.floor((z_hi - z.max()) / dz)) - 2
+    k1 = int(np.floor((z_hi - z.min()) / dz)) + 3
+    return max(0, k0), min(nz, max(k1, 0))
 
 
 def gather_sinogram(slab: torch.Tensor, n_views_total: int, rank: int, world: int, group=None) -> torch.Tensor:
@@ -163,12 +271,39 @@ class ZSlabShardedPlan:
         self.rank, self.world, self.group = rank, world, group
         self.parts = zslab_partition(geometry, world)
         k0, k1, r0, r1 = self.parts[rank]
+        self.full_rows = int(geometry["det_rows"])
+        self.full_off_v = float(geometry.get("det_offset", (0.0, 0.0))[1])
+        self.full_z_hi = float(geometry.get("center", (0, 0, 0))[2]) + int(geometry["n"][2]) * float(geometry["spacing"][2]) / 2.0
         self.slab, self.rows = (k0, k1), (r0, r1)
         self.geometry = zslab_geometry(geometry, k0, k1, r0, r1)
         if plan_factory is None:
             from .plan import Plan
             plan_factory = Plan
         self.plan = plan_factory(self.geometry, device=device)
+        if hasattr(self.plan, "ray_units"):
+            self.check_row_cells()
+
+    def check_row_cells(self) -> None:
+        """Assert that the kernel's fixed z cell of every row of this slab (its fp64 floor decision,
+        read back through xrt_ray_units on the central column of view 0) is the cell
+        zslab_partition assigned from numpy -- a disagreement at a tie would silently drop a row."""
+        g = self.geometry
+        k0, k1 = self.slab
+        nxy = int(g["n"][0]) * int(g["n"][1])
+        cols = int(g["det_cols"])
+        c_mid = (cols - 1) // 2
+        v_full = (np.arange(self.rows[0], self.rows[1]) - (int(self.full_rows) - 1) / 2.0) * float(g["det_spacing"][1]) \
+            + float(self.full_off_v)
+        z_hi = float(self.full_z_hi)
+        dz = float(g["spacing"][2])
+        want = np.floor((z_hi - v_full) / dz).astype(np.int64)
+        for i in range(self.rows[1] - self.rows[0]):
+            if not (k0 <= want[i] < k1):
+                continue                     # rows outside the image: no unit either way
+            rp, colsI, _ = self.plan.ray_units(i * cols + c_mid, i * cols + c_mid + 1)
+            ks = np.unique(colsI.cpu().numpy() // nxy) + k0
+            if ks.size and not (ks.size == 1 and ks[0] == want[i]):
+                raise AssertionError(f"z-slab row {self.rows[0] + i}: kernel cells {ks}, partition cell {want[i]}")
 
     def forward(self, img_slab: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
         """Sinogram rows [views][r0:r1][cols] of A x from this rank's slab x[k0:k1] alone."""

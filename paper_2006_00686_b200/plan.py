@@ -150,6 +150,23 @@ class Plan:
         check(self._lib.xrt_adjoint(self._h, sino.data_ptr(), out.data_ptr(), _stream_handle(stream, self.device)))
         return out
 
+    def adjoint_stages(self) -> list[tuple[int, int]]:
+        """xrt_adjoint_stages: per stage s, the image rows [k0, k1) final after stage s."""
+        n = ctypes.c_int32()
+        check(self._lib.xrt_adjoint_stages(self._h, ctypes.byref(n), None, None))
+        kb = (ctypes.c_int64 * n.value)()
+        ke = (ctypes.c_int64 * n.value)()
+        check(self._lib.xrt_adjoint_stages(self._h, ctypes.byref(n), kb, ke))
+        return [(int(kb[i]), int(ke[i])) for i in range(n.value)]
+
+    def adjoint_stage(self, sino: torch.Tensor, out: torch.Tensor, stage: int, stream=None) -> torch.Tensor:
+        """xrt_adjoint_stage: stage `stage` of the staged adjoint (writes out's final rows of that stage)."""
+        self._check_dev(sino, self.sino_shape, "sino")
+        self._check_dev(out, self.image_shape, "img")
+        check(self._lib.xrt_adjoint_stage(self._h, sino.data_ptr(), out.data_ptr(), int(stage),
+                                          _stream_handle(stream, self.device)))
+        return out
+
     def forward64(self, img: torch.Tensor, out: torch.Tensor | None = None, stream=None) -> torch.Tensor:
         """xrt_forward_f64: the same operator in fp64 (P:725's double option)."""
         self._check_dev(img, self.image_shape, "img", torch.float64)

@@ -239,3 +239,80 @@ def test_sharded_attenuated_gloo():
         p.join(timeout=60)
     for rank, ef, eb, ez in res:
         assert ef == 0.0 and eb <= 1e-6 and ez <= 1e-6, (rank, ef, eb, ez)
+
+
+class StagedOraclePlan(OraclePlan):
+    """OraclePlan with the staged-adjoint interface of Plan (xrt_adjoint_stages / _stage): the image
+    rows are split into `n` slabs; stage s writes slab s of the oracle's partial (computed once)."""
+
+    n_stages = 3
+
+    def adjoint_stages(self):
+        nz = self.image_shape[0]
+        cuts = np.linspace(0, nz, self.n_stages + 1).astype(int)
+        return [(int(a), int(b)) for a, b in zip(cuts[:-1], cuts[1:])]
+
+    def adjoint_stage(self, sino, out, stage):
+        if stage == 0:
+            self._part = OraclePlan.adjoint(self, sino)
+        k0, k1 = self.adjoint_stages()[stage]
+        out[k0:k1] = self._part[k0:k1]
+        return out
+
+
+def _staged_worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import workloads
+        from paper_2006_00686_b200.dist import zwindow
+        # staged (chunked, asynchronous) all-reduce == one all-reduce
+        c = workloads.scaled(4, n=(10, 10, 9), n_views=6, det_cols=11, det_rows=9)
+        sp = ShardedPlan(c, rank=rank, world=world, plan_factory=StagedOraclePlan)
+        y = workloads.make_sino_input(c)
+        v0, v1 = sp.view_block
+        staged = sp.adjoint(y[v0:v1].contiguous(), overlap=True).clone()
+        single = sp.adjoint(y[v0:v1].contiguous(), overlap=False)
+        e_stage = float((staged - single).abs().max())
+        # helical windows: A^T y on this rank's window from P2P overlaps == the full reduction there
+        ch = workloads.scaled(5, n=(12, 12, 24), n_views=16, det_cols=13, det_rows=5)
+        hp = ShardedPlan(ch, rank=rank, world=world, plan_factory=OraclePlan)
+        yh = workloads.make_sino_input(ch)
+        a0, a1 = hp.view_block
+        win = hp.adjoint_windowed(yh[a0:a1].contiguous())
+        full = OraclePlan(ch).adjoint(yh)
+        k0, k1 = hp.window()
+        e_win = float((win[k0:k1] - full[k0:k1]).abs().max() / full.abs().max())
+        # the partial of this rank is zero outside its window (the window is conservative)
+        part = OraclePlan(shard_geometry(ch, rank, world)).adjoint(yh[a0:a1].contiguous())
+        outside = float(torch.cat([part[:k0].reshape(-1), part[k1:].reshape(-1)]).abs().max()) if (k0 > 0 or k1 < 24) else 0.0
+        # scatter_windows delivers the window rows of x
+        x = workloads.make_image(ch) if rank == 0 else torch.zeros(hp.plan.image_shape)
+        hp.scatter_windows(x, src=0)
+        e_sc = float((x[k0:k1] - workloads.make_image(ch)[k0:k1]).abs().max())
+        # and the forward of the block needs x only on the window: zeros elsewhere change nothing
+        xw = torch.zeros_like(x)
+        xw[k0:k1] = x[k0:k1]
+        e_fw = float((hp.forward(xw) - hp.forward(workloads.make_image(ch))).abs().max())
+        q.put((rank, e_stage, e_win, outside, e_sc, e_fw, (k0, k1), zwindow(ch)))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_staged_and_windowed_collectives_gloo():
+    """World size 2 (gloo): the staged adjoint's per-slab asynchronous all-reduces equal one
+    all-reduce; the helical windowed exchange (P2P overlaps) gives A^T y exactly on each rank's z
+    window; windows are conservative (partials vanish outside) and suffice for the forward."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_staged_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=300) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+    for rank, e_stage, e_win, outside, e_sc, e_fw, win, full_win in res:
+        assert e_stage == 0.0, (rank, e_stage)
+        assert e_win <= 1e-6 and outside == 0.0 and e_sc == 0.0 and e_fw == 0.0, (rank, e_win, outside, e_sc, e_fw)
+        assert win[1] - win[0] < full_win[1] - full_win[0]     # a block sees less than the whole helix

@@ -662,3 +662,30 @@ def test_user_streams(cuda_ok, idx):
         assert H.rel_l2(a.cpu().numpy(), r.cpu().numpy()) <= 1e-6
         assert H.rel_l2(b.cpu().numpy(), r.cpu().numpy()) <= 1e-6
     assert torch.equal(r1[0], ref[0]) and torch.equal(r2[0], ref[0])
+
+
+@pytest.mark.parametrize("size", ["small", "full"])
+@pytest.mark.parametrize("idx", [3, 4, 5])
+def test_staged_adjoint(cuda_ok, idx, size):
+    """xrt_adjoint_stages / xrt_adjoint_stage (the overlapped multi-GPU reduction's building block):
+    the stage ranges partition [0, N_z); after the last stage the image equals xrt_adjoint (fp32
+    reassociation of the per-band atomics only), and each stage's rows are final when written."""
+    c = H.small_config(idx) if size == "small" else workloads.config(idx)
+    p = _plan(c)
+    stages = p.adjoint_stages()
+    nz = p.image_shape[0]
+    covered = np.zeros(nz, dtype=int)
+    for k0, k1 in stages:
+        covered[k0:k1] += 1
+    assert np.all(covered == 1), stages
+    y = workloads.make_sino_input(c, device="cuda")
+    ref = p.adjoint(y).clone()
+    out = torch.full_like(ref, float("nan"))
+    for s, (k0, k1) in enumerate(stages):
+        p.adjoint_stage(y, out, s)
+        torch.cuda.synchronize()
+        if k1 > k0:   # final rows: already equal to the full adjoint's
+            assert H.rel_l2(out[k0:k1].cpu().numpy(), ref[k0:k1].cpu().numpy()) < 1e-6, (s, k0, k1)
+    assert H.rel_l2(out.cpu().numpy(), ref.cpu().numpy()) < 1e-6
+    if size == "full" and idx == 4:
+        assert len(stages) > 1 and stages[0][1] > stages[0][0]   # cfg 4: the first band already finalises rows
