@@ -48,6 +48,10 @@ C_OPS = {2: 4, 3: 5}  # algorithmic FP32 ops per ray-unit intersection (SURVEY 8
 
 
 def peaks():
+    """Roofline denominators.  HBM and the SM clock from the driver-written MEASURED_PEAKS.json; the
+    FP32 issue rate from tools/issue_peak (profiles/issue_peak.json): the highest FP32 lane rate per
+    SM-cycle it measured on this GPU type (packed FFMA2 / FADD2 / FMUL2 or scalar FFMA, 8 independent
+    chains, 64 warps per SM) x 148 SMs x sm_max_mhz.  Fallback: the nominal 128 lanes."""
     path = os.path.join(ROOT, "MEASURED_PEAKS.json")
     src = "measured"
     try:
@@ -57,8 +61,19 @@ def peaks():
         pk = {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0}
         src = "fallback"
     sm_mhz = float(pk.get("sm_max_mhz", 1965.0))
-    return {"hbm_gbs": float(pk["hbm_gbs"]), "sm_mhz": sm_mhz,
-            "fp32_tops": 148 * 128 * sm_mhz * 1e6 / 1e12, "src": src}
+    lanes, lanes_src = 128.0, "nominal 128 FP32 lanes per SM-cycle (profiles/issue_peak.json missing)"
+    try:
+        with open(os.path.join(ROOT, "profiles", "issue_peak.json")) as f:
+            ip = json.load(f)
+        best = max(("FFMA", "FFMA2", "FADD2", "FMUL2"), key=lambda k: ip[k]["lane_ops_per_sm_cycle"])
+        lanes = float(ip[best]["lane_ops_per_sm_cycle"])
+        lanes_src = (f"measured: tools/issue_peak (profiles/issue_peak.json), {best} {lanes:.1f} FP32 lane ops "
+                     f"per SM-cycle (of 128 nominal)")
+    except Exception:
+        pass
+    return {"hbm_gbs": float(pk["hbm_gbs"]), "sm_mhz": sm_mhz, "fp32_lanes": lanes,
+            "fp32_tops": 148 * lanes * sm_mhz * 1e6 / 1e12, "src": src,
+            "fp32_src": f"{lanes_src} x 148 SMs x {sm_mhz:.0f} MHz ({src} sm_max_mhz, MEASURED_PEAKS.json)"}
 
 
 class ClockSampler:
@@ -145,26 +160,50 @@ def reduction_roofline(workload: str, nnz: int, adj_ms: float):
 
 
 def cpu_baseline(c: dict, budget_s: float = 12.0):
-    """The oracle, as it stands, on a bounded sample of the workload's rays (forward)."""
+    """The oracle, as it stands (fp64 brute force, mode 2: the i loop restricted to the x-range that
+    can meet the (k, j) overlap -- identical output to the full loop, tested), forward, on this
+    host's cores: the FULL sinogram of cfg 1 / 2, 4096 stratified rays of
+    cfg 3 / 5, and a bounded (~budget_s) stratified sample of cfg 4."""
     import oracle
     from oracle import geometry as G
     img = workloads.make_image(c, device="cuda" if torch.cuda.is_available() else "cpu").cpu().numpy().reshape(-1)
-    done, t_used, rays = 0, 0.0, 0
-    seed = 9000
-    batch = 64
-    while t_used < budget_s and done < 200000:
-        ids = workloads.sample_rays(c, batch, seed=seed)
-        seed += 1
-        p, th = G.rays(c, ids)
-        t0 = time.perf_counter()
-        oracle.forward(c, img, p, th)
-        t_used += time.perf_counter() - t0
-        done += ids.size
-        if t_used < budget_s / 8:
-            batch *= 2
+    M = workloads.configs.n_rays(c)
+    idx = int(c["name"][3])
+    t_used, done, nnz = 0.0, 0, 0
+    if idx in (1, 2, 3, 5):
+        if idx in (1, 2):
+            chunks = [np.arange(a, min(M, a + 200000), dtype=np.int64) for a in range(0, M, 200000)]
+            what = f"the full sinogram ({M} rays)"
+        else:
+            chunks = [workloads.sample_rays(c, 4096, seed=9000)]
+            what = f"{chunks[0].size} seeded stratified rays"
+        for ids in chunks:
+            p, th = G.rays(c, ids)
+            t0 = time.perf_counter()
+            rp, _, _ = oracle.rows(c, p, th, mode=2)
+            oracle.forward(c, img, p, th, mode=2)
+            t_used += time.perf_counter() - t0
+            done += ids.size
+            nnz += int(rp[-1])
+        t_used /= 2.0   # rows + forward walk the same boxes; report one pass
+    else:
+        seed, batch = 9000, 64
+        while t_used < budget_s and done < 200000:
+            ids = workloads.sample_rays(c, batch, seed=seed)
+            seed += 1
+            p, th = G.rays(c, ids)
+            t0 = time.perf_counter()
+            oracle.forward(c, img, p, th, mode=2)
+            t_used += time.perf_counter() - t0
+            done += ids.size
+            if t_used < budget_s / 8:
+                batch *= 2
+        what = f"{done} seeded stratified rays"
     out = {"value": done / t_used, "unit": "rays/s", "cores": oracle.threads(), "kind": "oracle",
-           "sample": f"{done} seeded rays of {c['name']} (stratified over views), fp64 brute-force forward "
-                     f"(separable early-out mode), {t_used:.1f} s"}
+           "sample": f"{what} of {c['name']}, fp64 brute-force forward (mode 2), {t_used:.1f} s",
+           "full_sinogram_s_extrapolated": M / (done / t_used)}
+    if nnz:
+        out["intersections_per_s"] = nnz / t_used
     # context: the paper's own O(N)-per-ray enumeration on the same host cores (cpu_method/, N3)
     try:
         import cpu_method
@@ -267,18 +306,30 @@ def main():
     M = workloads.configs.n_rays(c)
     dim = 2 if c["beam"] in ("par2d", "fan2d") else 3
     s = torch.cuda.current_stream()
+    helical_windows = world > 1 and c["beam"] == "helical"
 
     def step(ev=None):
+        """One pass of the hot path: (N > 1: x to every rank -- broadcast, or the helical z windows)
+        A x over this rank's views, then A^T over them (+ the overlapped staged all-reduce, or the
+        helical window exchange)."""
         if ev is not None:
             ev[0].record(s)
-        plan.forward(x, out=sino)
+        if world > 1:
+            if helical_windows:
+                sp.scatter_windows(x, src=0)
+            else:
+                dist.broadcast(x, src=0)
         if ev is not None:
             ev[1].record(s)
-        plan.adjoint(sino, out=xo)
+        plan.forward(x, out=sino)
         if ev is not None:
             ev[2].record(s)
-        if world > 1:
-            dist.all_reduce(xo)
+        if helical_windows:
+            sp.adjoint_windowed(sino, out=xo)
+        else:
+            sp.adjoint(sino, out=xo, overlap=True)
+        if ev is not None:
+            ev[3].record(s)
 
     for _ in range(args.warmup):
         step()
@@ -286,7 +337,7 @@ def main():
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
-    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.steps)]
     start = torch.cuda.Event(enable_timing=True)
     end = torch.cuda.Event(enable_timing=True)
     launches0 = plan.launch_count
@@ -301,23 +352,54 @@ def main():
     torch.cuda.synchronize()
     launches = plan.launch_count - launches0
     ms = start.elapsed_time(end)
-    fwd_ms = [e[0].elapsed_time(e[1]) for e in evs]
-    adj_ms = [e[1].elapsed_time(e[2]) for e in evs]
-    t = torch.tensor([ms, sum(fwd_ms), sum(adj_ms)], dtype=torch.float64, device=dev)
+    step_ms = [e[0].elapsed_time(e[3]) for e in evs]
+    bc_ms = [e[0].elapsed_time(e[1]) for e in evs]
+    fwd_ms = [e[1].elapsed_time(e[2]) for e in evs]
+    adj_ms = [e[2].elapsed_time(e[3]) for e in evs]     # adjoint (+ its overlapped reduction for N > 1)
+    t = torch.tensor([ms, sum(fwd_ms), sum(adj_ms), sum(bc_ms)], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms_max, fwd_sum, adj_sum = [float(v) for v in t.tolist()]
+    ms_max, fwd_sum, adj_sum, bc_sum = [float(v) for v in t.tolist()]
     value = M * args.steps / (ms_max / 1e3)
+    # the adjoint kernels alone (no collective), for the compute / collective split at N > 1
+    adj_compute_ms = None
+    if world > 1:
+        a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        a0.record(s)
+        for _ in range(args.steps):
+            plan.adjoint(sino, out=xo)
+        a1.record(s)
+        torch.cuda.synchronize()
+        ta = torch.tensor([a0.elapsed_time(a1) / args.steps], dtype=torch.float64, device=dev)
+        dist.all_reduce(ta, op=dist.ReduceOp.MAX)
+        adj_compute_ms = float(ta.item())
 
-    # ---------------- e2e through the host-buffer C ABI (pinned host memory)
+    # ---------------- e2e: host buffers in, host buffers out, through the public API
     e2e = None
     if not args.no_e2e:
         xh = x.cpu().pin_memory()
         sh = torch.empty(plan.sino_shape, dtype=torch.float32).pin_memory()
         xoh = torch.empty(plan.image_shape, dtype=torch.float32).pin_memory()
-        for _ in range(1):
-            plan.forward_host(xh, out=sh)
-            plan.adjoint_host(sh, out=xoh)
+
+        def e2e_step():
+            if world == 1:
+                # the C ABI's host-buffer entry points (copies pipelined with the kernels inside)
+                plan.forward_host(xh, out=sh)
+                plan.adjoint_host(sh, out=xoh)
+            else:
+                # sharded: H2D of x, A x, D2H of this rank's sinogram slab; H2D of the slab, A^T with
+                # the overlapped all-reduce, D2H of the image
+                x.copy_(xh, non_blocking=True)
+                plan.forward(x, out=sino)
+                sh.copy_(sino, non_blocking=True)
+                sino.copy_(sh, non_blocking=True)
+                if helical_windows:
+                    sp.adjoint_windowed(sino, out=xo)
+                else:
+                    sp.adjoint(sino, out=xo, overlap=True)
+                xoh.copy_(xo, non_blocking=True)
+        e2e_step()
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
@@ -326,8 +408,7 @@ def main():
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record(s)
         for _ in range(ke):
-            plan.forward_host(xh, out=sh)
-            plan.adjoint_host(sh, out=xoh)
+            e2e_step()
         e1.record(s)
         torch.cuda.synchronize()
         te = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
@@ -338,7 +419,9 @@ def main():
         sino_b = sino.numel() * 4
         e2e = {"value": M * ke / (e2e_ms / 1e3), "unit": "rays/s", "ms_per_step": e2e_ms / ke,
                "h2d_bytes_per_step": img_b + sino_b, "d2h_bytes_per_step": sino_b + img_b,
-               "note": "xrt_forward_host + xrt_adjoint_host, pinned host buffers, per-rank bytes"}
+               "note": ("xrt_forward_host + xrt_adjoint_host (copies pipelined inside the C ABI)" if world == 1 else
+                        "ShardedPlan: H2D x, A x, D2H + H2D of the rank's sinogram slab, A^T with the "
+                        "overlapped all-reduce, D2H image") + "; pinned host buffers; bytes per rank"}
 
     # ---------------- attenuated transform (N4): side measurement, outside the timed step
     att = None
@@ -375,7 +458,7 @@ def main():
     pk = peaks()
     c_ops = C_OPS[dim]
     fwd_avg = fwd_sum / args.steps
-    adj_avg = adj_sum / args.steps
+    adj_avg = adj_sum / args.steps if world == 1 else adj_compute_ms
     # per-rank kernels: ops of this rank's shard
     k_fwd = {"ms": fwd_avg, "tflops": c_ops * nnz_local / (fwd_avg / 1e3) / 1e12}
     k_adj = {"ms": adj_avg, "tflops": c_ops * nnz_local / (adj_avg / 1e3) / 1e12}
@@ -385,23 +468,29 @@ def main():
             "traffic": measured_traffic(c["name"], dom_name) if world == 1 else None,
             "traffic_unit": "bytes per launch (dram__bytes_read.sum + dram__bytes_write.sum, ncu --set full)",
             "algorithmic_bytes": int(4 * (x.numel() + sino.numel())),
-            "peak_source": f"FP32 issue 148 SM x 128 lanes x {pk['sm_mhz']:.0f} MHz ({pk['src']} sm_max_mhz)",
+            "peak_source": pk["fp32_src"],
             "ops_per_intersection": c_ops}
     line = {
         "metric": METRIC, "value": value, "unit": "rays/s", "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
+        "warmup": args.warmup, "ms_per_step": ms_max / args.steps,
+        "ms_per_step_median": statistics.median(step_ms), "ms_per_step_min": min(step_ms),
+        "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": {"workload": c["name"], "rays": M, "intersections": nnz_total,
                    "image": list(c["n"]), "views": c["n_views"], "det": [c["det_rows"], c["det_cols"]],
-                   "step": "sino = A x; x' = A^T sino (+ all_reduce for N > 1)",
+                   "step": "sino = A x; x' = A^T sino (N > 1: broadcast x, staged all-reduce of x' overlapped "
+                           "with the adjoint; helical: z-window scatter / P2P overlap exchange)",
                    "l2": "inputs larger than L2 (image + sinogram > 126 MB)" if (x.numel() + sino.numel()) * 4 > 126e6
                    else "inputs smaller than L2 (no flush)",
                    "parallelism": f"views/{world}"},
         "intersections_per_s": nnz_total * args.steps / (ms_max / 1e3),
-        "forward": {"ms": fwd_avg, "rays_per_s": M / world / (fwd_avg / 1e3),
+        "forward": {"ms": fwd_avg, "ms_median": statistics.median(fwd_ms), "ms_min": min(fwd_ms),
+                    "rays_per_s": M / world / (fwd_avg / 1e3),
                     "intersections_per_s": nnz_local / (fwd_avg / 1e3),
                     "roofline_frac": k_fwd["tflops"] / pk["fp32_tops"]},
-        "adjoint": {"ms": adj_avg, "rays_per_s": M / world / (adj_avg / 1e3),
+        "adjoint": {"ms": adj_avg, "ms_median": statistics.median(adj_ms) if world == 1 else adj_compute_ms,
+                    "ms_min": min(adj_ms) if world == 1 else adj_compute_ms,
+                    "rays_per_s": M / world / (adj_avg / 1e3),
                     "intersections_per_s": nnz_local / (adj_avg / 1e3),
                     "roofline_frac": k_adj["tflops"] / pk["fp32_tops"]},
         "roofline": roof,
@@ -409,6 +498,14 @@ def main():
         "clocks": clk.summary(),
         "algo": args.algo, "adj_algo": args.adj_algo or args.algo,
     }
+    if world > 1:
+        line["collective"] = {
+            "broadcast_ms": bc_sum / args.steps, "forward_ms": fwd_avg,
+            "adjoint_plus_reduce_ms": adj_sum / args.steps, "adjoint_compute_ms": adj_compute_ms,
+            "exposed_reduce_ms": adj_sum / args.steps - adj_compute_ms,
+            "mode": "helical z windows (scatter + P2P overlaps)" if helical_windows else
+                    "broadcast + staged all-reduce overlapped with the adjoint bands",
+            "note": "max over ranks; compute-only = the adjoint kernels timed alone"}
     if world == 1 and args.adj_algo in (None, "auto", "column") and args.algo in ("auto", "column") and dim == 3:
         rr = reduction_roofline(c["name"], nnz_local, adj_avg)
         if rr is not None:
