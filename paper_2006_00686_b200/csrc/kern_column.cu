@@ -66,9 +66,6 @@ constexpr int kWarps = XRT_COL_WARPS;  // warps per CTA = adjacent detector colu
 #ifndef XRT_FD_VIEWS
 #define XRT_FD_VIEWS 2
 #endif
-#ifndef XRT_FD_PREFETCH
-#define XRT_FD_PREFETCH 0   // > 0: L1 prefetch that many segments ahead (experiment)
-#endif
 constexpr int kFdCols = XRT_FD_COLS, kFdViews = XRT_FD_VIEWS, kFdWarps = kFdCols * kFdViews;
 #ifndef XRT_KPASSES
 #define XRT_KPASSES 4
@@ -1120,9 +1117,6 @@ __device__ __forceinline__ void fd_segments(unsigned seg, int total, FdPair (&P)
         const float qse = __uint_as_float(raw.z), qds = __uint_as_float(raw.w);
         const float2 se2 = make_float2(qse, qse);
         const uint4 nraw = lds128(seg + 16u * (unsigned)min(s + 1, total - 1));   // last trip: reload
-#if XRT_FD_PREFETCH
-        const uint4 praw = lds128(seg + 16u * (unsigned)min(s + XRT_FD_PREFETCH, total - 1));
-#endif
 #pragma unroll
         for (int p = 0; p < NP; ++p) {
             const float2 le = __fadd2_rn(se2, P[p].ntz);                 // sigma_e - tau
@@ -1132,14 +1126,6 @@ __device__ __forceinline__ void fd_segments(unsigned seg, int total, FdPair (&P)
             P[p].ntz = __ffma2_rn(cr, P[p].ndtz, P[p].ntz);
             const float2 na = ldg_f2(seg_ptr(nraw) + 8ull * __float_as_uint(P[p].kpf.x));
             const float2 nb = ldg_f2(seg_ptr(nraw) + 8ull * __float_as_uint(P[p].kpf.y));
-#if XRT_FD_PREFETCH
-            {   // L1 prefetch of the line two segments ahead at the current cell (a crossing moves by one cell)
-                const unsigned long long pa = seg_ptr(praw) + 8ull * __float_as_uint(P[p].kpf.x);
-                const unsigned long long pb = seg_ptr(praw) + 8ull * __float_as_uint(P[p].kpf.y);
-                asm volatile("prefetch.global.L1 [%0];" :: "l"(pa));
-                asm volatile("prefetch.global.L1 [%0];" :: "l"(pb));
-            }
-#endif
             P[p].acc0a = fmaf(va[p].x, qds, P[p].acc0a);                  // f_s d_sigma
             P[p].acc1a = fmaf(va[p].y, lma, P[p].acc1a);                  // (f_e - f_s) l_e
             P[p].acc0b = fmaf(vb[p].x, qds, P[p].acc0b);
@@ -1151,58 +1137,6 @@ __device__ __forceinline__ void fd_segments(unsigned seg, int total, FdPair (&P)
     }
 }
 
-// Two segments deep: the z state runs one segment ahead of the accumulation, so each segment's
-// loads issue two segments before their values are consumed (L1 misses wait on L2).  Repeating
-// the chunk's last record for the look-ahead is harmless: its crossing is already taken (cr = 0).
-template <int NP>
-__device__ __forceinline__ void fd_segments2(unsigned seg, int total, FdPair (&P)[NP]) {
-    const uint4 raw0 = lds128(seg);
-    uint4 raw1 = lds128(seg + 16u * (unsigned)min(1, total - 1));
-    float2 v0a[NP], v0b[NP], v1a[NP], v1b[NP], lm0[NP];
-    float ds0 = __uint_as_float(raw0.w);
-#pragma unroll
-    for (int p = 0; p < NP; ++p) {
-        v0a[p] = ldg_f2(seg_ptr(raw0) + 8ull * __float_as_uint(P[p].kpf.x));
-        v0b[p] = ldg_f2(seg_ptr(raw0) + 8ull * __float_as_uint(P[p].kpf.y));
-        const float se = __uint_as_float(raw0.z);
-        const float2 le = __fadd2_rn(make_float2(se, se), P[p].ntz);
-        const float2 cr = make_float2(gt0(le.x), gt0(le.y));
-        lm0[p] = make_float2(fmaxf(le.x, 0.f), fmaxf(le.y, 0.f));
-        P[p].kpf = __ffma2_rn(cr, P[p].dkf, P[p].kpf);
-        P[p].ntz = __ffma2_rn(cr, P[p].ndtz, P[p].ntz);
-        v1a[p] = ldg_f2(seg_ptr(raw1) + 8ull * __float_as_uint(P[p].kpf.x));
-        v1b[p] = ldg_f2(seg_ptr(raw1) + 8ull * __float_as_uint(P[p].kpf.y));
-    }
-#pragma unroll 2
-    for (int s = 0; s < total; ++s) {
-        const uint4 raw2 = lds128(seg + 16u * (unsigned)min(s + 2, total - 1));
-        const float se1 = __uint_as_float(raw1.z), ds1 = __uint_as_float(raw1.w);
-        const float2 se2 = make_float2(se1, se1);
-#pragma unroll
-        for (int p = 0; p < NP; ++p) {
-            const float2 le = __fadd2_rn(se2, P[p].ntz);                 // segment s + 1
-            const float2 cr = make_float2(gt0(le.x), gt0(le.y));
-            const float2 lm1 = make_float2(fmaxf(le.x, 0.f), fmaxf(le.y, 0.f));
-            P[p].kpf = __ffma2_rn(cr, P[p].dkf, P[p].kpf);
-            P[p].ntz = __ffma2_rn(cr, P[p].ndtz, P[p].ntz);
-            const float2 na = ldg_f2(seg_ptr(raw2) + 8ull * __float_as_uint(P[p].kpf.x));   // segment s + 2
-            const float2 nb = ldg_f2(seg_ptr(raw2) + 8ull * __float_as_uint(P[p].kpf.y));
-            P[p].acc0a = fmaf(v0a[p].x, ds0, P[p].acc0a);                // segment s
-            P[p].acc1a = fmaf(v0a[p].y, lm0[p].x, P[p].acc1a);
-            P[p].acc0b = fmaf(v0b[p].x, ds0, P[p].acc0b);
-            P[p].acc1b = fmaf(v0b[p].y, lm0[p].y, P[p].acc1b);
-            v0a[p] = v1a[p]; v0b[p] = v1b[p];
-            v1a[p] = na; v1b[p] = nb;
-            lm0[p] = lm1;
-        }
-        ds0 = ds1;
-        raw1 = raw2;
-    }
-}
-
-#ifndef XRT_FD_DEPTH
-#define XRT_FD_DEPTH 1
-#endif
 
 #ifndef XRT_FD_THREADS
 #define XRT_FD_THREADS 1024  // resident threads per SM targeted by the launch bounds (2 pairs per lane):
@@ -1211,6 +1145,7 @@ __device__ __forceinline__ void fd_segments2(unsigned seg, int total, FdPair (&P
 #define XRT_FD_THREADS1 768  // ... 1 pair per lane
 #endif
 #define XRT_FD_MINB (XRT_FD_THREADS / (32 * kFdWarps) > 0 ? XRT_FD_THREADS / (32 * kFdWarps) : 1)
+
 #define XRT_FD_MINB1 (XRT_FD_THREADS1 / (32 * kFdWarps) > 0 ? XRT_FD_THREADS1 / (32 * kFdWarps) : 1)
 
 // CTA / warp / band layout as k_column (kOp 0): warp = one detector column, 2 NP rays per lane (rows
@@ -1317,8 +1252,7 @@ k_fwd_fd(const ViewRec* __restrict__ views, DetC dc, GridC g, const float2* __re
             }
 #pragma unroll
             for (int p = 0; p < NP; ++p) fd_anchor(P[p], sc);
-            if (XRT_FD_DEPTH == 2) fd_segments2<NP>(seg_s, total, P);
-            else fd_segments<NP>(seg_s, total, P);
+            fd_segments<NP>(seg_s, total, P);
         }
         __syncwarp();  // the next chunk overwrites the segments
     }
