@@ -19,7 +19,16 @@
 
 #include "xrt_internal.cuh"
 
+// NVTX ranges around the entry points (header-only nvtx3: no library dependency; visible in nsys /
+// ncu --nvtx when a tool is attached, no cost otherwise)
+#include <nvtx3/nvToolsExt.h>
+
 namespace {
+
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+};
 
 thread_local std::string g_err;
 
@@ -325,6 +334,8 @@ xrt_status adjoint_range(xrt_plan p, const float* sino, float* img, int64_t v0, 
         if (p->dim == 2) {
             e = xrt::launch_adjoint_gather2d(p, sino, img, s);
         } else {
+            if (!p->d_gather_y)
+                XRT_CUDA(cudaMalloc(&p->d_gather_y, sizeof(float) * (size_t)(p->gather_views * p->det.per_view)));
             e = xrt::launch_adjoint_gather(p, sino, p->d_work_adj, s);
             p->launches += xrt::gather_launches(p) - 1;
         }
@@ -500,8 +511,7 @@ xrt_status plan_create_impl(const xrt_geometry* g, int cuda_device, xrt_plan* ou
         // gather workspace: one block of views of the rescaled, transposed sinogram (~40 MB, so the
         // block stays L2-resident while every voxel reads it)
         p->gather_views = std::max<int64_t>(1, std::min<int64_t>(g->n_views, (40ll << 20) / (4 * D.per_view)));
-        if (e == cudaSuccess)
-            e = cudaMalloc(&p->d_gather_y, sizeof(float) * (size_t)(p->gather_views * D.per_view));
+        // (the gather's workspace, ~40 MB, is allocated on first use: AUTO never runs the gather)
         if (e == cudaSuccess) e = cudaDeviceSynchronize();
         // xy tiling, per operator: the largest power-of-two tile whose z-fastest columns, restricted
         // to the z slab one band of detector rows can reach (the kernels run band-major), fit the
@@ -610,6 +620,7 @@ xrt_status plan_create_impl(const xrt_geometry* g, int cuda_device, xrt_plan* ou
 extern "C" {
 
 xrt_status xrt_plan_create(const xrt_geometry* g, int cuda_device, xrt_plan* out) {
+    NvtxRange nvtx_("xrt_plan_create");
     if (!out) return fail(XRT_ERR_INVALID_ARG, "out is NULL");
     *out = nullptr;
     xrt_status st = validate(g);
@@ -618,6 +629,7 @@ xrt_status xrt_plan_create(const xrt_geometry* g, int cuda_device, xrt_plan* out
 }
 
 xrt_status xrt_plan_create_rays(const xrt_ray_list* r, int cuda_device, xrt_plan* out) {
+    NvtxRange nvtx_("xrt_plan_create_rays");
     if (!out) return fail(XRT_ERR_INVALID_ARG, "out is NULL");
     *out = nullptr;
     if (!r) return fail(XRT_ERR_INVALID_ARG, "ray list is NULL");
@@ -704,6 +716,7 @@ xrt_status xrt_plan_set_algorithm(xrt_plan p, int32_t op, int32_t algo) {
 int64_t xrt_plan_launch_count(xrt_plan p) { return p ? p->launches : -1; }
 
 xrt_status xrt_forward(xrt_plan p, const float* img, float* sino, void* cuda_stream) {
+    NvtxRange nvtx_("xrt_forward");
     if (!p || !img || !sino) return fail(XRT_ERR_INVALID_ARG, "NULL argument");
     DevGuard guard(p->device);
     cudaStream_t s = (cudaStream_t)cuda_stream;
@@ -713,6 +726,7 @@ xrt_status xrt_forward(xrt_plan p, const float* img, float* sino, void* cuda_str
 }
 
 xrt_status xrt_adjoint(xrt_plan p, const float* sino, float* img, void* cuda_stream) {
+    NvtxRange nvtx_("xrt_adjoint");
     if (!p || !img || !sino) return fail(XRT_ERR_INVALID_ARG, "NULL argument");
     DevGuard guard(p->device);
     cudaStream_t s = (cudaStream_t)cuda_stream;
@@ -723,6 +737,7 @@ xrt_status xrt_adjoint(xrt_plan p, const float* sino, float* img, void* cuda_str
 }
 
 xrt_status xrt_forward_f64(xrt_plan p, const double* img, double* sino, void* cuda_stream) {
+    NvtxRange nvtx_("xrt_forward_f64");
     if (!p || !img || !sino) return fail(XRT_ERR_INVALID_ARG, "NULL argument");
     DevGuard guard(p->device);
     cudaError_t e = xrt::launch_forward64(p, img, sino, 0, p->n_rays, (cudaStream_t)cuda_stream);
@@ -732,6 +747,7 @@ xrt_status xrt_forward_f64(xrt_plan p, const double* img, double* sino, void* cu
 }
 
 xrt_status xrt_adjoint_f64(xrt_plan p, const double* sino, double* img, void* cuda_stream) {
+    NvtxRange nvtx_("xrt_adjoint_f64");
     if (!p || !img || !sino) return fail(XRT_ERR_INVALID_ARG, "NULL argument");
     DevGuard guard(p->device);
     cudaStream_t s = (cudaStream_t)cuda_stream;
@@ -763,6 +779,7 @@ static cudaError_t att_alloc(xrt_plan p, bool adjoint) {
 }
 
 xrt_status xrt_forward_attenuated(xrt_plan p, const float* img, const float* mu, float* sino, void* cuda_stream) {
+    NvtxRange nvtx_("xrt_forward_attenuated");
     if (!p || !img || !mu || !sino) return fail(XRT_ERR_INVALID_ARG, "NULL argument");
     DevGuard guard(p->device);
     cudaStream_t s = (cudaStream_t)cuda_stream;
@@ -781,6 +798,7 @@ xrt_status xrt_forward_attenuated(xrt_plan p, const float* img, const float* mu,
 }
 
 xrt_status xrt_adjoint_attenuated(xrt_plan p, const float* sino, const float* mu, float* img, void* cuda_stream) {
+    NvtxRange nvtx_("xrt_adjoint_attenuated");
     if (!p || !img || !mu || !sino) return fail(XRT_ERR_INVALID_ARG, "NULL argument");
     DevGuard guard(p->device);
     cudaStream_t s = (cudaStream_t)cuda_stream;
@@ -827,6 +845,7 @@ xrt_status xrt_adjoint_stages(xrt_plan p, int32_t* n_stages, int64_t* k_begin, i
 }
 
 xrt_status xrt_adjoint_stage(xrt_plan p, const float* sino, float* img, int32_t stage, void* cuda_stream) {
+    NvtxRange nvtx_("xrt_adjoint_stage");
     if (!p || !img || !sino) return fail(XRT_ERR_INVALID_ARG, "NULL argument");
     DevGuard guard(p->device);
     cudaStream_t s = (cudaStream_t)cuda_stream;
@@ -852,6 +871,7 @@ xrt_status xrt_adjoint_stage(xrt_plan p, const float* sino, float* img, int32_t 
 // Host-buffer forward: H2D(image) -> per view chunk: kernel, then D2H of that chunk on the aux
 // stream, so the sinogram download overlaps the next chunk's kernel.
 xrt_status xrt_forward_host(xrt_plan p, const float* img_host, float* sino_host, void* cuda_stream) {
+    NvtxRange nvtx_("xrt_forward_host");
     if (!p || !img_host || !sino_host) return fail(XRT_ERR_INVALID_ARG, "NULL argument");
     DevGuard guard(p->device);
     xrt_status st = alloc_stage(p);
@@ -918,6 +938,7 @@ xrt_status xrt_forward_host(xrt_plan p, const float* img_host, float* sino_host,
 // Host-buffer adjoint: per view chunk H2D(sino chunk) on the aux stream overlapping the previous
 // chunk's kernel, then D2H(image).
 xrt_status xrt_adjoint_host(xrt_plan p, const float* sino_host, float* img_host, void* cuda_stream) {
+    NvtxRange nvtx_("xrt_adjoint_host");
     if (!p || !img_host || !sino_host) return fail(XRT_ERR_INVALID_ARG, "NULL argument");
     DevGuard guard(p->device);
     xrt_status st = alloc_stage(p);
@@ -992,6 +1013,7 @@ xrt_status xrt_adjoint_host(xrt_plan p, const float* sino_host, float* img_host,
 xrt_status xrt_ray_units(xrt_plan p, int64_t ray_begin, int64_t ray_end, int64_t* row_ptr,
                          int64_t* cols, double* lens, int64_t capacity, int64_t* nnz_out,
                          void* cuda_stream) {
+    NvtxRange nvtx_("xrt_ray_units");
     if (!p || !row_ptr || !nnz_out) return fail(XRT_ERR_INVALID_ARG, "NULL argument");
     if (ray_begin < 0 || ray_end < ray_begin || ray_end > p->n_rays)
         return fail(XRT_ERR_INVALID_ARG, "ray range [%lld, %lld) outside [0, %lld)", (long long)ray_begin,
