@@ -326,7 +326,8 @@ xrt_status adjoint_range(xrt_plan p, const float* sino, float* img, int64_t v0, 
         e = xrt::launch_adjoint_ray(p, sino, img, v0 * pv, v1 * pv, s);
     } else if (algo == XRT_ALGO_COLUMN && p->dim == 2) {
         if (!(v0 == 0 && v1 == p->n_views)) return fail(XRT_ERR_UNSUPPORTED, "2D slice kernels run all views at once");
-        e = xrt::launch_slice2d(p, true, nullptr, nullptr, sino, nullptr, img, p->d_img_t, s);
+        e = p->slice_v1 ? xrt::launch_slice2d(p, true, nullptr, nullptr, sino, nullptr, img, p->d_img_t, s)
+                        : xrt::launch_slice2d_adj(p, sino, img, p->d_img_t, s);
     } else if (algo == XRT_ALGO_COLUMN) {
         e = xrt::launch_adjoint_column(p, sino, p->d_work_adj, v0, v1, s);
     } else if (algo == XRT_ALGO_GATHER) {
@@ -475,6 +476,7 @@ xrt_status plan_create_impl(const xrt_geometry* g, int cuda_device, xrt_plan* ou
         // 2D gather: per-(view, column) rays in index space
         e = cudaMalloc(&p->d_raydesc2d, xrt::raydesc2d_bytes() * (size_t)(p->n_views * D.cols));
         if (e == cudaSuccess) e = cudaMalloc(&p->d_img_t, sizeof(float) * (size_t)G.nxy);
+        p->slice_v1 = std::getenv("XRT_SLICE_V1") != nullptr;
         if (e == cudaSuccess) e = xrt::launch_raydesc2d(p, (cudaStream_t)0);
         if (e == cudaSuccess) e = cudaDeviceSynchronize();
         if (e != cudaSuccess) {

@@ -277,6 +277,145 @@ __global__ void __launch_bounds__(kSliceWarps * 32) k_slice2d(const ViewRec* __r
     if (!kAdj && col_ok) sino_out[(int64_t)v * dc.cols + c] = acc;
 }
 
+// ---------------------------------------------------------------------------------------------
+// Slice adjoint v2 (AUTO on the 2D beams): the same lockstep walk, with at most TWO units per major
+// slice for every lane whose ray is no steeper than the warp's major axis (|w_b| <= |w_a|: within one
+// slice the minor coordinate changes by <= 1 cell, so the valid band of eq:restriction_j P:197-212 is
+// {c_b, c_b + s_b}).  Per slice and lane, branch-free: the slice's span [t_lo, t_hi], the minor
+// crossing T_b, cr = [T_b < t_hi], l_e = max(t_hi - T_b, 0) (C_up - C_low of the second unit,
+// eq:range_length P:217-220), l_s = (t_hi - t_lo) - l_e.  Crossing values are T(m) = t1 + m dt (FFMA
+// of the count, shared by the two units they separate): red.global.add of y l_s and (if cr) y l_e,
+// the address of the minor cell a magic-float add (no conversion).  Lanes steeper than the major
+// axis or travelling against the warp walk their rays alone (RAY walk).
+constexpr float kMagic2 = 12582912.0f;          // 1.5 * 2^23: bits(kMagic2 + c) = 0x4B400000 + c
+constexpr unsigned kMagicBits2 = 0x4B400000u;
+
+__device__ __forceinline__ float gt0f(float x) {
+    float r;
+    asm("set.gt.f32.f32 %0, %1, 0f00000000;" : "=f"(r) : "f"(x));
+    return r;
+}
+
+__device__ __forceinline__ void red_f(float* a, float v) {
+    asm volatile("red.global.add.f32 [%0], %1;" :: "l"(a), "f"(v) : "memory");
+}
+
+#ifndef XRT_SLICE2_WARPS
+#define XRT_SLICE2_WARPS 4
+#endif
+constexpr int kSlice2Warps = XRT_SLICE2_WARPS;
+
+// (adjoint only: the forward variant on (f, f[+-1] - f) rows, and a variant staging 128^2 image
+// tiles in shared memory, measured slower than the RAY forward on cfg 2 -- profiles/r2_2d.md)
+__global__ void __launch_bounds__(kSlice2Warps * 32) k_slice2d_adj(const ViewRec* __restrict__ views, DetC dc, GridC g,
+                                                 const float* __restrict__ y_in,
+                                                 float* __restrict__ acc_img, float* __restrict__ acc_imgT,
+                                                 int n_views, int groups_per_view) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int gid = blockIdx.x * kSlice2Warps + warp;
+    const int v = gid / groups_per_view, cgp = gid - v * groups_per_view;
+    if (v >= n_views) return;                              // warp-uniform
+    const int c = cgp * 32 + lane;
+    Ray64 R;
+    bool hit = false;
+    if (c < dc.cols) hit = setup_ray(views[v], dc, g, 0, c, R);
+    const unsigned bh = __ballot_sync(0xffffffffu, hit);
+    if (bh == 0u) return;
+    const unsigned bx = __ballot_sync(0xffffffffu, hit && fabs(R.w[0]) >= fabs(R.w[1]));
+    const int a = 2 * __popc(bx) >= __popc(bh) ? 0 : 1, b = 1 - a;
+    const int na = g.n[a], nb = g.n[b];
+    // per-ray fp32 state relative to its entry (the RAY kernel's construction)
+    float ta1 = INFINITY, dta = 0.f, tb1 = INFINITY, dtb = 0.f, tend = 0.f;
+    int ca = 0, cb = 0, sa = 0, sb = 0;
+    float y = 0.f;
+    if (hit) {
+        float T1[2], DT[2];
+        int st[2];
+        tend = (float)(R.t_out - R.t_in);
+#pragma unroll
+        for (int x = 0; x < 2; ++x) {
+            if (!R.moving[x]) { T1[x] = INFINITY; DT[x] = 0.f; st[x] = 0; continue; }
+            const int pos = R.w[x] > 0.0;
+            const int bf = pos ? R.cell[x] + 1 : R.cell[x];
+            const int mface = pos ? (g.n[x] - bf) : bf;
+            T1[x] = (float)(((double)bf - R.u0[x]) * R.inv_w[x] - R.t_in);
+            DT[x] = (float)fabs(R.inv_w[x]);
+            st[x] = pos ? 1 : -1;
+            tend = fminf(tend, fmaf((float)mface, DT[x], T1[x]));   // never step through a face
+        }
+        ta1 = T1[a]; tb1 = T1[b]; dta = DT[a]; dtb = DT[b];
+        ca = R.cell[a]; cb = R.cell[b]; sa = st[a]; sb = st[b];
+        y = y_in[(int64_t)v * dc.cols + c];
+    }
+    const int dir = __shfl_sync(0xffffffffu, hit ? sa : 0, __ffs(bh) - 1);
+    // lanes that cannot take the lockstep walk: against the warp's direction, fixed major axis, or
+    // steeper than the major axis (more than one minor crossing per slice): the RAY walk, alone
+    const bool alone = hit && (sa != dir || dir == 0 || (sb != 0 && dtb < dta));
+    if (alone && y != 0.f) {
+        float tc = 0.f, Ta = ta1, Tb = tb1, ma = 0.f, mb = 0.f;
+        int cca = ca, ccb = cb;
+        for (int it = 0; it < na + nb + 2 && tc < tend; ++it) {
+            const float tn = fminf(fminf(Ta, Tb), tend);
+            const float l = tn - tc;
+            const int64_t I = a == 1 ? (int64_t)cca * g.n[0] + ccb : (int64_t)ccb * g.n[0] + cca;   // y-major
+            if (l > 0.f) red_f(acc_img + I, y * l);
+            tc = tn;
+            if (tn == Ta) { ma += 1.f; Ta = fmaf(ma, dta, ta1); cca += sa; }
+            else if (tn == Tb) { mb += 1.f; Tb = fmaf(mb, dtb, tb1); ccb += sb; }
+        }
+    }
+    const bool live = hit && !alone && y != 0.f;
+    // lockstep slices: lane's first major cell ca, n_sl slices (1 + major crossings inside the chord)
+    int n_sl = 0;
+    if (live) {
+        int m = tend > ta1 ? (int)((tend - ta1) / dta) : -1;
+        m = max(-1, min(m, na));
+        while (m + 1 <= na && fmaf((float)(m + 1), dta, ta1) < tend) ++m;
+        while (m >= 0 && !(fmaf((float)m, dta, ta1) < tend)) --m;
+        n_sl = m + 2;
+    }
+    int kfirst = live ? ca * dir : INT_MAX;   // position along dir
+    int klast = live ? (ca + dir * (n_sl - 1)) * dir : INT_MIN;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        kfirst = min(kfirst, __shfl_xor_sync(0xffffffffu, kfirst, o));
+        klast = max(klast, __shfl_xor_sync(0xffffffffu, klast, o));
+    }
+    if (kfirst > klast) return;
+    const int start = live ? ca * dir - kfirst : 0;     // lockstep trip at which this lane enters
+    // minor cell as a magic float: address = row + 4 bits(cbf)
+    float cbf = kMagic2 + (float)cb;
+    const float sbf = (float)sb;
+    const float ndtb = sb != 0 ? -dtb : 0.f;
+    const float ntb0 = sb != 0 ? -tb1 : -1.0e30f;
+    float ntb = ntb0;                        // -(next minor crossing)
+    float mb = 0.f, t_lo = 0.f, ma = 0.f;
+    float* acco = a == 1 ? acc_img : acc_imgT;   // y-major: img[j][i]; x-major: the transposed accumulator
+    const long long rstep = (long long)dir * 4ll * nb;   // bytes per major step
+    unsigned long long row = (unsigned long long)acco - 4ull * kMagicBits2 + (unsigned long long)((long long)ca * 4ll * nb);
+    const int n_trips = klast - kfirst + 1;
+    for (int k = 0; k < n_trips; ++k) {
+        const int rel = k - start;
+        if (live && (unsigned)rel < (unsigned)n_sl) {
+            const float Ta = fmaf(ma, dta, ta1);
+            const float t_hi = fminf(Ta, tend);
+            const float dlt = t_hi - t_lo;
+            const float le = t_hi + ntb;                    // t_hi - T_b
+            const float cr = gt0f(le);
+            const float lm = fmaxf(le, 0.f);
+            float* p0 = (float*)(row + 4ull * __float_as_uint(cbf));
+            red_f(p0, y * (dlt - lm));
+            if (cr != 0.f) red_f(p0 + sb, y * lm);
+            cbf = fmaf(cr, sbf, cbf);
+            mb += cr;
+            ntb = fmaf(mb, ndtb, ntb0);
+            ma += 1.f;
+            t_lo = t_hi;
+            row += (unsigned long long)rstep;
+        }
+    }
+}
+
 }  // namespace
 
 namespace {
@@ -304,6 +443,16 @@ cudaError_t launch_transpose2d(const float* in, float* out, int rows, int cols, 
     dim3 grid((unsigned)((cols + 31) / 32), (unsigned)((rows + 31) / 32));
     if (add) k_transpose2d<true><<<grid, dim3(32, 8), 0, s>>>(in, out, rows, cols);
     else k_transpose2d<false><<<grid, dim3(32, 8), 0, s>>>(in, out, rows, cols);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_slice2d_adj(const xrt_plan_s* p, const float* y_in, float* acc_img, float* acc_imgT,
+                               cudaStream_t s) {
+    const int gpv = (p->det.cols + 31) / 32;
+    const int64_t warps = p->n_views * (int64_t)gpv;
+    const unsigned blocks = (unsigned)((warps + kSlice2Warps - 1) / kSlice2Warps);
+    k_slice2d_adj<<<blocks, kSlice2Warps * 32, 0, s>>>(p->d_views, p->det, p->grid, y_in, acc_img, acc_imgT,
+                                                      (int)p->n_views, gpv);
     return cudaGetLastError();
 }
 

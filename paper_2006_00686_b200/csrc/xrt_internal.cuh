@@ -244,6 +244,7 @@ struct xrt_plan_s {
     double* d_rays = nullptr;          // explicit ray list (XRT_RAYS)
     void* d_raydesc2d = nullptr;       // per-(view, column) rays in index space (2D GATHER)
     float* d_img_t = nullptr;          // 2D COLUMN (slice) kernels: transposed image / accumulator
+    bool slice_v1 = false;             // XRT_SLICE_V1=1: the round-1 slice adjoint (A/B)
     float* d_gather_y = nullptr;       // GATHER workspace: rescaled, transposed sinogram of one view block
     int64_t gather_views = 0;          // views per GATHER launch
     // host-pipeline staging (allocated on first *_host call)
@@ -311,6 +312,8 @@ size_t raydesc2d_bytes();
 cudaError_t launch_raydesc2d(const xrt_plan_s* p, cudaStream_t s);
 cudaError_t launch_adjoint_gather2d(const xrt_plan_s* p, const float* sino, float* img, cudaStream_t s);
 cudaError_t launch_transpose2d(const float* in, float* out, int rows, int cols, bool add, cudaStream_t s);
+cudaError_t launch_slice2d_adj(const xrt_plan_s* p, const float* y_in, float* acc_img, float* acc_imgT,
+                               cudaStream_t s);
 cudaError_t launch_slice2d(const xrt_plan_s* p, bool adjoint, const float* img, const float* imgT,
                            const float* y_in, float* sino_out, float* acc_img, float* acc_imgT,
                            cudaStream_t s);

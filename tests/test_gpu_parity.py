@@ -687,5 +687,5 @@ def test_staged_adjoint(cuda_ok, idx, size):
         if k1 > k0:   # final rows: already equal to the full adjoint's
             assert H.rel_l2(out[k0:k1].cpu().numpy(), ref[k0:k1].cpu().numpy()) < 1e-6, (s, k0, k1)
     assert H.rel_l2(out.cpu().numpy(), ref.cpu().numpy()) < 1e-6
-    if size == "full" and idx == 4:
-        assert len(stages) > 1 and stages[0][1] > stages[0][0]   # cfg 4: the first band already finalises rows
+    if size == "full" and idx == 4:   # cfg 4: rows become final before the last band (something to overlap)
+        assert len(stages) > 1 and any(k1 > k0 for k0, k1 in stages[:-1]), stages
