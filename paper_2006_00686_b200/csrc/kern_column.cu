@@ -1116,12 +1116,13 @@ __device__ __forceinline__ void fd_segments(unsigned seg, int total, FdPair (&P)
     for (int s = 0; s < total; ++s) {
         const float qse = __uint_as_float(raw.z), qds = __uint_as_float(raw.w);
         const float2 se2 = make_float2(qse, qse);
-        const uint4 nraw = lds128(seg + 16u * (unsigned)min(s + 1, total - 1));   // last trip: reload
+        const uint4 nraw = lds128(seg + 16u * (unsigned)(s + 1));   // record `total` repeats the last one
 #pragma unroll
         for (int p = 0; p < NP; ++p) {
             const float2 le = __fadd2_rn(se2, P[p].ntz);                 // sigma_e - tau
             const float2 cr = make_float2(gt0(le.x), gt0(le.y));
-            const float lma = fmaxf(le.x, 0.f), lmb = fmaxf(le.y, 0.f);  // l_e
+            const float2 lm = __fmul2_rn(le, cr);                        // l_e = max(sigma_e - tau, 0)
+            const float lma = lm.x, lmb = lm.y;
             P[p].kpf = __ffma2_rn(cr, P[p].dkf, P[p].kpf);
             P[p].ntz = __ffma2_rn(cr, P[p].ndtz, P[p].ntz);
             const float2 na = ldg_f2(seg_ptr(nraw) + 8ull * __float_as_uint(P[p].kpf.x));
@@ -1155,7 +1156,7 @@ __global__ void __launch_bounds__(kFdWarps * 32, NP == 1 ? XRT_FD_MINB1 : XRT_FD
 k_fwd_fd(const ViewRec* __restrict__ views, DetC dc, GridC g, const float2* __restrict__ fd,
          float* __restrict__ sino_out, int view0, const ColDesc* __restrict__ desc, ColumnLaunch L) {
     constexpr int R = 2 * NP;
-    __shared__ Seg s_seg[kFdWarps][2 * 32];
+    __shared__ Seg s_seg[kFdWarps][2 * 32 + 1];   // + a copy of the chunk's last record (look-ahead)
     __shared__ float s_first[kFdWarps];
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
@@ -1239,6 +1240,12 @@ k_fwd_fd(const ViewRec* __restrict__ views, DetC dc, GridC g, const float2* __re
         }
         if (cnt > 1) sts_seg(seg_s + 16u * (unsigned)(b + 1), base + cstride * (unsigned)c1, a1e - sc, a1e - a1s);
         const int total = __shfl_sync(0xffffffffu, incl, 31);
+        // the lane holding the last record also writes it at index `total` (the walk's look-ahead
+        // reads one record past the end instead of clamping its index)
+        if (cnt > 0 && b + cnt == total) {
+            if (cnt > 1) sts_seg(seg_s + 16u * (unsigned)total, base + cstride * (unsigned)c1, a1e - sc, a1e - a1s);
+            else sts_seg(seg_s + 16u * (unsigned)total, base + cstride * (unsigned)c0, a0e - sc, a0e - a0s);
+        }
         __syncwarp();
         if (total > 0) {
             if (!zinit) {
