@@ -217,14 +217,3 @@ def grid_bounds(c: dict):
     return cx - nx * dx / 2.0, cy + ny * dy / 2.0, cz + nz * dz / 2.0
 
 
-def source_points(c: dict, views) -> np.ndarray:
-    """Physical source position per view for divergent beams (readings 7, 11):
-    fan S = D(-sin a, cos a, 0); cone S = (-D cos p, -D sin p, 0); helix adds H(p) to z."""
-    ang = np.asarray(c["angles"], dtype=np.float64)[np.asarray(views)]
-    D = c["sod"]
-    if c["beam"] == "fan2d":
-        return np.stack([-D * np.sin(ang), D * np.cos(ang), np.zeros_like(ang)], axis=-1)
-    H = np.zeros_like(ang)
-    if c["beam"] == "helical":
-        H = c["z0"] + c["pitch"] * ang / (2 * math.pi)
-    return np.stack([-D * np.cos(ang), -D * np.sin(ang), H], axis=-1)
