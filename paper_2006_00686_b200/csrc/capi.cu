@@ -251,6 +251,11 @@ xrt_status alloc_stage(xrt_plan p) {
         XRT_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
         p->aux_stream = s;
     }
+    if (!p->aux_stream2) {
+        cudaStream_t s;
+        XRT_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+        p->aux_stream2 = s;
+    }
     return XRT_OK;
 }
 
@@ -565,6 +570,18 @@ xrt_status plan_create_impl(const xrt_geometry* g, int cuda_device, xrt_plan* ou
             xrt_plan_destroy(p);
             return cuda_fail(e, "plan workspace");
         }
+        // forward bands' image rows (host pipeline: the image arrives in z chunks, band b starts once
+        // the rows it reaches are built)
+        {
+            const int nbf = xrt::column_bands(p, false), rbf = xrt::column_band_rows(p, false);
+            p->fwd_band_k.assign(2 * (size_t)nbf, 0);
+            for (int b = 0; b < nbf; ++b) {
+                double zlo, zhi;
+                band_z_range(g, G, (int64_t)b * rbf, std::min<int64_t>(g->det_rows, (int64_t)(b + 1) * rbf) - 1, zlo, zhi);
+                p->fwd_band_k[2 * b] = std::max<int64_t>(0, (int64_t)std::floor((G.z_hi - zhi) / G.d[2]) - 2);
+                p->fwd_band_k[2 * b + 1] = std::min<int64_t>(G.n[2], (int64_t)std::floor((G.z_hi - zlo) / G.d[2]) + 3);
+            }
+        }
         // staged adjoint (xrt_adjoint_stages): band b of the adjoint touches image rows
         // [klo_b, khi_b] (conservative, 2-cell margin); rows no later band touches are final after b.
         // Bands run in row order, i.e. monotone in z; a non-monotone tail folds into the last stage.
@@ -683,6 +700,7 @@ xrt_status xrt_plan_destroy(xrt_plan p) {
     cudaFree(p->d_stage_img);
     cudaFree(p->d_stage_sino);
     if (p->aux_stream) cudaStreamDestroy((cudaStream_t)p->aux_stream);
+    if (p->aux_stream2) cudaStreamDestroy((cudaStream_t)p->aux_stream2);
     delete p;
     return XRT_OK;
 }
@@ -879,6 +897,76 @@ xrt_status xrt_forward_host(xrt_plan p, const float* img_host, float* sino_host,
     xrt_status st = alloc_stage(p);
     if (st != XRT_OK) return st;
     cudaStream_t s = (cudaStream_t)cuda_stream, a = (cudaStream_t)p->aux_stream;
+    if (resolve(p, XRT_OP_FORWARD) == XRT_ALGO_COLUMN && p->dim == 3 && p->fd_forward && !p->fwd_band_k.empty()) {
+        // fd column forward: the image goes up in z chunks on the aux stream, each chunk's fd rows
+        // built there as soon as its neighbour rows are present; band b waits only for the rows
+        // it reaches (bands run in row order, i.e. monotone in z: the chunks are sent in the order
+        // the bands need them); band b's sinogram rows go down on a second aux stream
+        const int nz = p->grid.n[2];
+        const int64_t nxy = p->grid.nxy;
+        const int nb = xrt::column_bands(p, false), rb = xrt::column_band_rows(p, false);
+        const bool desc = p->fwd_band_k[0] + p->fwd_band_k[1] >= nz;    // band 0 at high k
+        const int CH = std::max(32, (nz + 15) / 16);
+        const int nch = (nz + CH - 1) / CH;
+        cudaStream_t d = (cudaStream_t)p->aux_stream2;
+        std::vector<cudaEvent_t> evc((size_t)nch), evb((size_t)nb);
+        for (auto& x : evc) XRT_CUDA(cudaEventCreateWithFlags(&x, cudaEventDisableTiming));
+        for (auto& x : evb) XRT_CUDA(cudaEventCreateWithFlags(&x, cudaEventDisableTiming));
+        // chunk i covers image rows [lo_i, hi_i) in send order; built fd rows after chunk i:
+        // desc: [lo_i + 1 .. nz] (row lo_i waits for its lower neighbour), asc: [-1 .. hi_i - 1)
+        cudaError_t e = cudaSuccess;
+        int built_lo = nz + 1, built_hi = -1;   // fd rows [built_lo, nz] (desc) or [-1, built_hi) (asc)
+        std::vector<int> done_lo((size_t)nch), done_hi((size_t)nch);
+        for (int i = 0; i < nch && e == cudaSuccess; ++i) {
+            const int lo = desc ? std::max(0, nz - (i + 1) * CH) : i * CH;
+            const int hi = desc ? nz - i * CH : std::min(nz, (i + 1) * CH);
+            e = cudaMemcpyAsync(p->d_stage_img + lo * nxy, img_host + lo * nxy, sizeof(float) * (size_t)((hi - lo) * nxy),
+                                cudaMemcpyHostToDevice, a);
+            if (desc) {
+                const int ka = lo == 0 ? -1 : lo + 1, kb = built_lo;
+                if (e == cudaSuccess) e = xrt::launch_to_fd_rows(p, p->d_stage_img, p->d_work_fd, ka, kb, a);
+                built_lo = ka;
+            } else {
+                const int ka = built_hi < 0 ? -1 : built_hi, kb = hi == nz ? nz + 1 : hi - 1;
+                if (e == cudaSuccess) e = xrt::launch_to_fd_rows(p, p->d_stage_img, p->d_work_fd, ka, kb, a);
+                built_hi = kb;
+            }
+            p->launches += 1;
+            done_lo[i] = desc ? built_lo : -1;
+            done_hi[i] = desc ? nz + 1 : built_hi;
+            if (e == cudaSuccess) e = cudaEventRecord(evc[i], a);
+        }
+        const size_t pitch = sizeof(float) * (size_t)p->det.per_view;
+        for (int b = 0; b < nb && e == cudaSuccess; ++b) {
+            // the first chunk after which the band's rows (with their fd neighbours) are built
+            const int k0 = (int)p->fwd_band_k[2 * b] - 1, k1 = (int)p->fwd_band_k[2 * b + 1] + 1;
+            int need = nch - 1;
+            for (int i = 0; i < nch; ++i)
+                if (done_lo[i] <= std::max(k0, -1) && done_hi[i] >= std::min(k1, nz + 1)) { need = i; break; }
+            e = cudaStreamWaitEvent(s, evc[need], 0);
+            if (e == cudaSuccess) e = xrt::launch_forward_fd_bands(p, p->d_work_fd, p->d_stage_sino, b, b + 1, s);
+            p->launches += 1;
+            const int r0 = b * rb, r1 = std::min(p->det.rows, r0 + rb);
+            if (e == cudaSuccess) e = cudaEventRecord(evb[b], s);
+            if (e == cudaSuccess) e = cudaStreamWaitEvent(d, evb[b], 0);
+            if (e == cudaSuccess)
+                e = cudaMemcpy2DAsync(sino_host + (int64_t)r0 * p->det.cols, pitch,
+                                      p->d_stage_sino + (int64_t)r0 * p->det.cols, pitch,
+                                      sizeof(float) * (size_t)(r1 - r0) * p->det.cols, (size_t)p->n_views,
+                                      cudaMemcpyDeviceToHost, d);
+        }
+        if (e == cudaSuccess) e = cudaStreamWaitEvent(s, evc[nch - 1], 0);   // the stage buffers are reused
+        cudaError_t e1 = cudaStreamSynchronize(a);
+        cudaError_t e2 = cudaStreamSynchronize(s);
+        cudaError_t e3 = cudaStreamSynchronize(d);
+        for (auto& x : evc) cudaEventDestroy(x);
+        for (auto& x : evb) cudaEventDestroy(x);
+        if (e != cudaSuccess) return cuda_fail(e, "forward_host chunked pipeline");
+        if (e1 != cudaSuccess) return cuda_fail(e1, "forward_host sync");
+        if (e2 != cudaSuccess) return cuda_fail(e2, "forward_host sync");
+        if (e3 != cudaSuccess) return cuda_fail(e3, "forward_host sync");
+        return XRT_OK;
+    }
     XRT_CUDA(cudaMemcpyAsync(p->d_stage_img, img_host, sizeof(float) * (size_t)p->grid.nxyz,
                              cudaMemcpyHostToDevice, s));
     st = fwd_prepare(p, p->d_stage_img, s);
@@ -948,13 +1036,18 @@ xrt_status xrt_adjoint_host(xrt_plan p, const float* sino_host, float* img_host,
     cudaStream_t s = (cudaStream_t)cuda_stream, a = (cudaStream_t)p->aux_stream;
     st = adj_begin(p, p->d_stage_img, s);
     if (st != XRT_OK) return st;
-    if (resolve(p, XRT_OP_ADJOINT) == XRT_ALGO_COLUMN && p->dim == 3) {
-        // COLUMN: the sinogram rows of band b (every view) are uploaded on the aux stream while
-        // band b - 1 computes; one launch per band
+    if (resolve(p, XRT_OP_ADJOINT) == XRT_ALGO_COLUMN && p->dim == 3 && !p->adj_stage_k.empty()) {
+        // COLUMN, staged: the sinogram rows of band b (every view) are uploaded on the aux stream
+        // while band b - 1 computes; after band b the image rows no later band reaches are
+        // transposed out and downloaded on a second aux stream while the next bands compute, so
+        // only the last stage's rows wait for the end (xrt_adjoint_stages)
         const int nb = xrt::column_bands(p, true), rb = xrt::column_band_rows(p, true);
         const size_t pitch = sizeof(float) * (size_t)p->det.per_view;
-        std::vector<cudaEvent_t> ev((size_t)nb);
+        cudaStream_t d = (cudaStream_t)p->aux_stream2;
+        std::vector<cudaEvent_t> ev((size_t)nb), evd((size_t)nb);
         for (auto& x : ev) XRT_CUDA(cudaEventCreateWithFlags(&x, cudaEventDisableTiming));
+        for (auto& x : evd) XRT_CUDA(cudaEventCreateWithFlags(&x, cudaEventDisableTiming));
+        const int64_t nxy = p->grid.nxy;
         for (int b = 0; b < nb && st == XRT_OK; ++b) {
             const int r0 = b * rb, r1 = std::min(p->det.rows, r0 + rb);
             cudaError_t e = cudaMemcpy2DAsync(p->d_stage_sino + (int64_t)r0 * p->det.cols, pitch,
@@ -965,20 +1058,27 @@ xrt_status xrt_adjoint_host(xrt_plan p, const float* sino_host, float* img_host,
             if (e == cudaSuccess) e = cudaStreamWaitEvent(s, ev[b], 0);
             if (e == cudaSuccess) e = xrt::launch_adjoint_column_bands(p, p->d_stage_sino, p->d_work_adj, b, b + 1, s);
             p->launches += 1;
-            if (e != cudaSuccess) st = cuda_fail(e, "adjoint_host band pipeline");
-        }
-        if (st == XRT_OK) st = adj_finish(p, p->d_stage_img, s);
-        if (st == XRT_OK) {
-            cudaError_t e = cudaMemcpyAsync(img_host, p->d_stage_img, sizeof(float) * (size_t)p->grid.nxyz,
-                                            cudaMemcpyDeviceToHost, s);
-            if (e != cudaSuccess) st = cuda_fail(e, "adjoint_host D2H");
+            const int64_t k0 = p->adj_stage_k[2 * b], k1 = p->adj_stage_k[2 * b + 1];
+            if (e == cudaSuccess && k1 > k0) {
+                e = xrt::launch_from_zfast_rows(p, p->d_work_adj, p->d_stage_img, k0, k1, s);
+                p->launches += 1;
+                if (e == cudaSuccess) e = cudaEventRecord(evd[b], s);
+                if (e == cudaSuccess) e = cudaStreamWaitEvent(d, evd[b], 0);
+                if (e == cudaSuccess)
+                    e = cudaMemcpyAsync(img_host + k0 * nxy, p->d_stage_img + k0 * nxy, sizeof(float) * (size_t)((k1 - k0) * nxy),
+                                        cudaMemcpyDeviceToHost, d);
+            }
+            if (e != cudaSuccess) st = cuda_fail(e, "adjoint_host staged pipeline");
         }
         cudaError_t e1 = cudaStreamSynchronize(s);
         cudaError_t e2 = cudaStreamSynchronize(a);
+        cudaError_t e3 = cudaStreamSynchronize(d);
         for (auto& x : ev) cudaEventDestroy(x);
+        for (auto& x : evd) cudaEventDestroy(x);
         if (st != XRT_OK) return st;
         if (e1 != cudaSuccess) return cuda_fail(e1, "adjoint_host sync");
         if (e2 != cudaSuccess) return cuda_fail(e2, "adjoint_host sync");
+        if (e3 != cudaSuccess) return cuda_fail(e3, "adjoint_host sync");
         return XRT_OK;
     }
     const bool whole = resolve(p, XRT_OP_ADJOINT) == XRT_ALGO_GATHER ||

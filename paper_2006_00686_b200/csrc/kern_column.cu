@@ -1024,10 +1024,10 @@ inline cudaError_t transpose(const float* in, float* out, int64_t rows, int64_t 
 // Tile of 32 columns x 32 k (+1 halo on each side) through shared memory; writes are coalesced
 // along k (float4 = two float2 cells of one half).
 __global__ void __launch_bounds__(256) k_to_fd(const float* __restrict__ img, float2* __restrict__ fd,
-                                               int64_t nxy, int nz, int64_t nzp, int pad) {
+                                               int64_t nxy, int nz, int64_t nzp, int pad, int ka, int kb) {
     __shared__ float t[34][33];
     const int64_t c0 = (int64_t)blockIdx.x * 32;
-    const int k0 = (int)blockIdx.y * 32 - 1;           // first k of this tile's rows (-1 .. nz)
+    const int k0 = ka + (int)blockIdx.y * 32;          // first k of this tile's rows (ka .. kb - 1)
     // load k = k0 - 1 .. k0 + 32 (34 rows), columns c0 .. c0 + 31
     for (int r = threadIdx.y; r < 34; r += 8) {
         const int k = k0 - 1 + r;
@@ -1039,7 +1039,7 @@ __global__ void __launch_bounds__(256) k_to_fd(const float* __restrict__ img, fl
     for (int cc = threadIdx.y; cc < 32; cc += 8) {
         const int64_t c = c0 + cc;
         const int k = k0 + (int)threadIdx.x;
-        if (c >= nxy || k > nz || k < -1) continue;
+        if (c >= nxy || k >= kb) continue;
         const float f = t[threadIdx.x + 1][cc];
         const float fp = t[threadIdx.x + 2][cc], fm = t[threadIdx.x][cc];
         float2* col = fd + c * 2 * nzp + pad + k;
@@ -1628,11 +1628,16 @@ int column_bands(const xrt_plan_s* p, bool adj) {
 }
 
 // ---- forward on the (f, delta f) volume (AUTO forward of the 3D column path)
-cudaError_t launch_to_fd(const xrt_plan_s* p, const float* img, float2* fd, cudaStream_t s) {
-    const int nz = p->grid.n[2];
-    dim3 grid((unsigned)((p->grid.nxy + 31) / 32), (unsigned)((nz + 2 + 31) / 32));
-    k_to_fd<<<grid, dim3(32, 8), 0, s>>>(img, fd, p->grid.nxy, nz, p->nzp, (int)p->zpad);
+// fd rows [ka, kb) (ka >= -1, kb <= N_z + 1; the rows -1 .. N_z are the ones with data)
+cudaError_t launch_to_fd_rows(const xrt_plan_s* p, const float* img, float2* fd, int ka, int kb, cudaStream_t s) {
+    if (kb <= ka) return cudaSuccess;
+    dim3 grid((unsigned)((p->grid.nxy + 31) / 32), (unsigned)((kb - ka + 31) / 32));
+    k_to_fd<<<grid, dim3(32, 8), 0, s>>>(img, fd, p->grid.nxy, p->grid.n[2], p->nzp, (int)p->zpad, ka, kb);
     return cudaGetLastError();
+}
+
+cudaError_t launch_to_fd(const xrt_plan_s* p, const float* img, float2* fd, cudaStream_t s) {
+    return launch_to_fd_rows(p, img, fd, -1, p->grid.n[2] + 1, s);
 }
 
 static cudaError_t launch_fd(const xrt_plan_s* p, const float2* fd, float* sino, const ColumnLaunch& L, int nblk,

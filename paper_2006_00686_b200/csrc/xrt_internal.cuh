@@ -251,10 +251,12 @@ struct xrt_plan_s {
     float* d_stage_img = nullptr;
     float* d_stage_sino = nullptr;
     void* aux_stream = nullptr;
+    void* aux_stream2 = nullptr;       // host pipelines: downloads of final image rows (staged adjoint)
     int algo_fwd = XRT_ALGO_AUTO;
     int algo_adj = XRT_ALGO_AUTO;
     bool column_ok = false;            // geometry admits the column-shared kernels
     std::vector<int64_t> adj_stage_k;  // staged adjoint: per band b, image rows [k0, k1) final after b
+    std::vector<int64_t> fwd_band_k;   // forward bands: per band b, the image rows [k0, k1) its rays reach
     int64_t launches = 0;
 };
 
@@ -321,6 +323,7 @@ int column_bands(const xrt_plan_s* p, bool adj);
 cudaError_t launch_forward_column_bands(const xrt_plan_s* p, const float* vol_zfast, float* sino, int b0,
                                         int b1, cudaStream_t s);
 cudaError_t launch_to_fd(const xrt_plan_s* p, const float* img, float2* fd, cudaStream_t s);
+cudaError_t launch_to_fd_rows(const xrt_plan_s* p, const float* img, float2* fd, int ka, int kb, cudaStream_t s);
 cudaError_t launch_forward_fd_bands(const xrt_plan_s* p, const float2* fd, float* sino, int b0, int b1,
                                     cudaStream_t s);
 cudaError_t launch_adjoint_column_bands(const xrt_plan_s* p, const float* sino, float* vol_zfast, int b0,

@@ -689,3 +689,20 @@ def test_staged_adjoint(cuda_ok, idx, size):
     assert H.rel_l2(out.cpu().numpy(), ref.cpu().numpy()) < 1e-6
     if size == "full" and idx == 4:   # cfg 4: rows become final before the last band (something to overlap)
         assert len(stages) > 1 and any(k1 > k0 for k0, k1 in stages[:-1]), stages
+
+
+@pytest.mark.parametrize("idx", [4, 5])
+def test_host_pipeline_full_size(cuda_ok, idx):
+    """The host-buffer entry points at full size: the image goes up in z chunks with each band
+    started once its rows are built (forward), final image rows come down while later bands compute
+    (staged adjoint) -- same results as the device entry points."""
+    c = workloads.config(idx)
+    p = _plan(c)
+    img = _image(c)
+    dev = p.forward(img)
+    host = p.forward_host(img.cpu().contiguous())
+    assert H.fwd_err(host.numpy().ravel(), dev.cpu().numpy().ravel()) <= 1e-6
+    y = workloads.make_sino_input(c)
+    a_dev = p.adjoint(y.cuda())
+    a_host = p.adjoint_host(y.contiguous())
+    assert H.rel_l2(a_host.numpy(), a_dev.cpu().numpy()) < 1e-6
