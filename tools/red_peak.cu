@@ -5,6 +5,9 @@
 //                 column adjoint's start-cell reductions on cfg 4)
 //   scattered  : 32 lanes -> 32 different sectors (1 element per sector)
 //   adjoint_dedup: the adjoint-like cells with the duplicate lanes idle (each cell once per warp)
+//   adj_cross_*: adjoint-like main cells plus a z-crossing unit (cell + 1) on every 5th lane, as two
+//                scalar reds, or as one 16-byte red.v4 of the quad holding both (spill: the crossing
+//                cell in the next quad -> a scalar red) -- "sectors_per_s" counts the main cells only
 // Prints one JSON line: elements/s, sectors/s and sectors per SM-cycle for each pattern.
 // nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o red_peak tools/red_peak.cu
 #include <cstdio>
@@ -20,7 +23,24 @@ __global__ void k_red(float* __restrict__ buf, unsigned mask_floats, int iters, 
         else if (pattern == 1) off = base + (lane * 2u) / 3u;
         else off = base + lane * 8u;
         float* a = buf + (off & mask_floats);
-        if (pattern == 3) {
+        if (pattern >= 4) {   // adjoint-like main cells + a z crossing on every 6th lane
+            off = base + (lane * 2u) / 3u;
+            const bool cross = lane % 5u == 2u;
+            if (pattern == 4) {   // scalar: main red, then the crossing red (cell + 1) where it crosses
+                a = buf + (off & mask_floats);
+                asm volatile("red.global.add.f32 [%0], %1;" :: "l"(a), "f"(1.0f) : "memory");
+                if (cross) asm volatile("red.global.add.f32 [%0], %1;" :: "l"(a + 1), "f"(0.5f) : "memory");
+            } else {              // v4: the 16-byte quad holding the main cell (and the crossing cell)
+                const unsigned j = off & 3u;
+                float c[4] = {0.f, 0.f, 0.f, 0.f};
+                c[0] = j == 0 ? 1.f : 0.f; c[1] = j == 1 ? 1.f : (cross && j == 0 ? .5f : 0.f);
+                c[2] = j == 2 ? 1.f : (cross && j == 1 ? .5f : 0.f); c[3] = j == 3 ? 1.f : (cross && j == 2 ? .5f : 0.f);
+                a = buf + ((off & ~3u) & mask_floats);
+                asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" :: "l"(a), "f"(c[0]), "f"(c[1]), "f"(c[2]), "f"(c[3]) : "memory");
+                if (pattern == 5 && cross && j == 3)
+                    asm volatile("red.global.add.f32 [%0], %1;" :: "l"(buf + ((off + 1u) & mask_floats)), "f"(0.5f) : "memory");
+            }
+        } else if (pattern == 3) {
             off = base + (lane * 2u) / 3u;
             a = buf + (off & mask_floats);
             const bool dup = lane > 0 && (lane * 2u) / 3u == ((lane - 1u) * 2u) / 3u;
@@ -42,14 +62,15 @@ int main() {
     cudaDeviceGetAttribute(&clk_khz, cudaDevAttrClockRate, 0);
     const int blocks = sms * 8, threads = 256, iters = 4096;
     const double warps = (double)blocks * threads / 32;
-    const double sectors_per_inst[4] = {4.0, 3.0, 32.0, 3.0};
+    const double sectors_per_inst[7] = {4.0, 3.0, 32.0, 3.0, 3.0, 3.0, 3.0};
     const double elems_per_inst = 32.0;   // for pattern 3: the 32 lanes' units, carried by 22 lanes
-    const char* names[4] = {"coalesced", "adjoint_like", "scattered", "adjoint_dedup"};
+    const char* names[7] = {"coalesced", "adjoint_like", "scattered", "adjoint_dedup", "adj_cross_scalar",
+                            "adj_cross_v4_spill", "adj_cross_v4"};
     cudaEvent_t e0, e1;
     cudaEventCreate(&e0);
     cudaEventCreate(&e1);
     printf("{\"sms\": %d, \"clock_mhz_attr\": %.0f", sms, clk_khz / 1e3);
-    for (int p = 0; p < 4; ++p) {
+    for (int p = 0; p < 7; ++p) {
         k_red<<<blocks, threads>>>(buf, (unsigned)(n - 1), 64, p);   // warm-up
         cudaEventRecord(e0);
         for (int r = 0; r < 5; ++r) k_red<<<blocks, threads>>>(buf, (unsigned)(n - 1), iters, p);
