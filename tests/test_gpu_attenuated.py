@@ -206,13 +206,15 @@ def test_view_sharding_equivalence(cuda_ok, idx):
     assert H.rel_l2(acc.cpu().numpy(), ref_b.cpu().numpy()) <= 1e-6
 
 
+@pytest.mark.parametrize("tile", ["16", "8"])
 @pytest.mark.parametrize("idx", [4, 5])
-def test_tiled_pieces_combine(cuda_ok, idx, monkeypatch):
-    """Forced xy tiling (XRT_COLUMN_TILE=16 at plan creation): the attenuated forward runs per tile
+def test_tiled_pieces_combine(cuda_ok, idx, tile, monkeypatch):
+    """Forced xy tiling (XRT_COLUMN_TILE at plan creation): the attenuated forward runs per tile
     piece, (sigma, S_t, A_t), and combines the pieces in path order -- against the oracle and the
-    RAY kernel (no tiling) on the whole sinogram."""
+    RAY kernel (no tiling) on the whole sinogram.  Tile 8 gives 36 / 64 tiles, more than the
+    combine's 16 piece slots: the attenuated operators then run untiled (att_tiled), still exact."""
     c = H.small_config(idx)
-    monkeypatch.setenv("XRT_COLUMN_TILE", "16")
+    monkeypatch.setenv("XRT_COLUMN_TILE", tile)
     pt = Plan(c, device=0)
     monkeypatch.delenv("XRT_COLUMN_TILE")
     pr = _plan(c, "ray")

@@ -320,11 +320,13 @@ def test_view_sharding_equivalence(cuda_ok, idx):
     assert H.rel_l2(acc.cpu().numpy(), back.cpu().numpy()) < 1e-6
 
 
+@pytest.mark.parametrize("tile", ["16", "8"])
 @pytest.mark.parametrize("idx", [3, 4, 5])
-def test_column_tiled_small(cuda_ok, idx, monkeypatch):
-    """Force the xy-tiled COLUMN launch (tile side 16) on oracle-sized configs: forward and adjoint
-    still match the oracle (partial sums per tile telescope exactly)."""
-    monkeypatch.setenv("XRT_COLUMN_TILE", "16")
+def test_column_tiled_small(cuda_ok, idx, tile, monkeypatch):
+    """Force the xy-tiled COLUMN launch (tile side 16: 3x3 / 4x4 tiles; 8: 25-64 tiles, a chord
+    crossing up to 15) on oracle-sized configs: forward and adjoint still match the oracle (partial
+    sums per tile telescope exactly)."""
+    monkeypatch.setenv("XRT_COLUMN_TILE", tile)
     c = H.small_config(idx)
     p = _plan(c, "column")
     img = _image(c)
