@@ -271,6 +271,10 @@ def main():
     ap.add_argument("--no-attenuated", action="store_true",
                     help="skip the attenuated-transform side measurement (SURVEY 8(f) N4)")
     ap.add_argument("--ref-rays", type=int, default=256)
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
+                    help="gloo: functional check of the N > 1 step with fewer GPUs than ranks (ranks share "
+                         "GPUs, collectives through the host; no kernel waits on another rank) -- not a "
+                         "measurement")
     args = ap.parse_args()
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -281,10 +285,15 @@ def main():
         run_reference(args, c, rank, world)
         return
 
+    if args.dist_backend == "gloo":
+        local = local % torch.cuda.device_count()
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group("gloo")
     from paper_2006_00686_b200 import Plan
     from paper_2006_00686_b200.dist import ShardedPlan
 
@@ -482,7 +491,10 @@ def main():
                            "with the adjoint; helical: z-window scatter / P2P overlap exchange)",
                    "l2": "inputs larger than L2 (image + sinogram > 126 MB)" if (x.numel() + sino.numel()) * 4 > 126e6
                    else "inputs smaller than L2 (no flush)",
-                   "parallelism": f"views/{world}"},
+                   "parallelism": f"views/{world}",
+                   **({"dist_backend": args.dist_backend + (" (functional check, ranks share GPUs: not a "
+                                                            "measurement)" if args.dist_backend == "gloo" else "")}
+                      if world > 1 else {})},
         "intersections_per_s": nnz_total * args.steps / (ms_max / 1e3),
         "forward": {"ms": fwd_avg, "ms_median": statistics.median(fwd_ms), "ms_min": min(fwd_ms),
                     "rays_per_s": M / world / (fwd_avg / 1e3),

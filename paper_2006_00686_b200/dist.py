@@ -111,15 +111,29 @@ class ShardedPlan:
             if hi <= lo:
                 continue
             buf = torch.empty_like(part[lo:hi])
-            ops.append(dist.P2POp(dist.isend, part[lo:hi].contiguous(), q, group=self.group))
-            ops.append(dist.P2POp(dist.irecv, buf, q, group=self.group))
+            ops.append((True, part[lo:hi].contiguous(), q))
+            ops.append((False, buf, q))
             bufs.append((lo, hi, buf))
-        if ops:
-            for w in dist.batch_isend_irecv(ops):
-                w.wait()
+        self._p2p(ops)
         for lo, hi, buf in bufs:
             part[lo:hi] += buf
         return part
+
+    def _p2p(self, ops) -> None:
+        """One batch of point-to-point transfers, ops = [(is_send, tensor, peer)].  With the gloo
+        backend (CPU tests; the functional N > 1 check of bench.py on fewer GPUs than ranks) CUDA
+        tensors are staged through host memory, which gloo's send / recv require."""
+        if not ops:
+            return
+        stage = dist.get_backend(self.group) == "gloo" and ops[0][1].is_cuda
+        work = [(snd, t.cpu() if stage else t, q) for snd, t, q in ops]
+        p2p = [dist.P2POp(dist.isend if snd else dist.irecv, t, q, group=self.group) for snd, t, q in work]
+        for w in dist.batch_isend_irecv(p2p):
+            w.wait()
+        if stage:
+            for (snd, t, _), (_, th, _) in zip(ops, work):
+                if not snd:
+                    t.copy_(th)
 
     def scatter_windows(self, img: torch.Tensor, src: int = 0) -> torch.Tensor:
         """Send every rank the rows of ``img`` (valid on ``src``) in its z window (P2P): the
@@ -131,14 +145,12 @@ class ShardedPlan:
             for q in range(self.world):
                 if q != src:
                     a0, a1 = self.window(q)
-                    ops.append(dist.P2POp(dist.isend, img[a0:a1].contiguous(), q, group=self.group))
+                    ops.append((True, img[a0:a1].contiguous(), q))
         else:
             k0, k1 = self.window()
             buf = torch.empty_like(img[k0:k1])
-            ops.append(dist.P2POp(dist.irecv, buf, src, group=self.group))
-        if ops:
-            for w in dist.batch_isend_irecv(ops):
-                w.wait()
+            ops.append((False, buf, src))
+        self._p2p(ops)
         if self.rank != src:
             img[k0:k1] = buf
         return img
