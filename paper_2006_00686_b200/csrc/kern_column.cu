@@ -322,6 +322,26 @@ __device__ __forceinline__ void load_path(const ColDesc* __restrict__ dsc, int n
     ca = q4.y;
 }
 
+// The in-plane fields slice_segments reads, re-read per chunk from the (L1-resident) descriptor with
+// volatile loads: not hoisted, so they do not stay live across the walk (at 64 registers they were
+// spilled to local memory and written back to L2 every chunk).
+__device__ __forceinline__ void load_path_chunk(const ColDesc* __restrict__ dsc, int nx, ColumnPath& P) {
+    unsigned a0, a1, a2, a3, b0, b1, b2, b3, c0, c1, c2, c3;
+    asm volatile("ld.global.nc.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(a0), "=r"(a1), "=r"(a2), "=r"(a3) : "l"(dsc));
+    asm volatile("ld.global.nc.v4.u32 {%0, %1, %2, %3}, [%4+16];" : "=r"(b0), "=r"(b1), "=r"(b2), "=r"(b3) : "l"(dsc));
+    asm volatile("ld.global.nc.v4.u32 {%0, %1, %2, %3}, [%4+32];" : "=r"(c0), "=r"(c1), "=r"(c2), "=r"(c3) : "l"(dsc));
+    P.L = __uint_as_float(a0); P.t0a = __uint_as_float(a1); P.dta = __uint_as_float(a2); P.t0b = __uint_as_float(a3);
+    P.dtb = __uint_as_float(b0); P.idtb = __uint_as_float(b1);
+    P.n_slices = (int)b2;
+    P.hit = b3 & 1;
+    P.a = (b3 >> 1) & 1;
+    P.cell_a0 = (int)c0; P.cell_b0 = (int)c1; P.nb_face = (int)c2;
+    P.step_a = (int)(c3 & 3) - 1;
+    P.step_b = (int)((c3 >> 2) & 3) - 1;
+    P.sa = P.a == 0 ? 1 : nx;
+    P.sb = P.a == 0 ? nx : 1;
+}
+
 // Per-ray z description along the shared path (sigma from the square entry): the z cell at the
 // square entry and the z-plane crossings tau_m = t0z + m dtz, evaluated in sigma (well conditioned
 // also for rays almost parallel to the z planes).
@@ -1057,8 +1077,6 @@ struct FdPair {
     float2 ndtz;   // -dtz (0 fixed)
     float2 t0z;    // first crossing, sigma from the square entry (kNoCrossPos fixed)
     float acc0a, acc0b, acc1a, acc1b;
-    float2 w;      // 1 / cos(beta)
-    bool live0, live1;
 };
 constexpr float kNoCrossPos = 1.0e30f;
 
@@ -1071,9 +1089,14 @@ __device__ __forceinline__ void fd_init(FdPair& P, const RayZ& Za, const RayZ& Z
     P.t0z = make_float2(Za.dk ? Za.t0z : kNoCrossPos, Zb.dk ? Zb.t0z : kNoCrossPos);
     P.ntz = make_float2(-P.t0z.x, -P.t0z.y);
     P.acc0a = P.acc0b = P.acc1a = P.acc1b = 0.f;
-    P.w = make_float2(Za.scale, Zb.scale);
-    P.live0 = Za.active;
-    P.live1 = Zb.active;
+}
+
+// 1 / cos(beta) of a ray from its z-crossing spacing: dtz = d_z / |tan(beta)| (ray_z); fixed-z
+// rays (tan(beta) snapped to 0) have 1
+__device__ __forceinline__ float fd_scale(float ndtz, float dz) {
+    if (ndtz == 0.f) return 1.f;
+    const float tb = dz / ndtz;
+    return sqrtf(fmaf(tb, tb, 1.f));
 }
 
 // crossings tau_m = t0z + m dtz with tau_m < sf taken (the ray's state at sigma_first, tiled)
@@ -1211,7 +1234,7 @@ k_fwd_fd(const ViewRec* __restrict__ views, DetC dc, GridC g, const float2* __re
         ray_z(V, dc, g, Pth, ca, ra, L.pad, Za);
         ray_z(V, dc, g, Pth, ca, rb, L.pad, Zb);
         fd_init(P[p], Za, Zb, L.nzp);
-        any_live |= P[p].live0 | P[p].live1;
+        any_live |= Za.active | Zb.active;
     }
     if (!__any_sync(0xffffffffu, any_live)) return;
     Seg* seg = s_seg[warp];
@@ -1220,13 +1243,17 @@ k_fwd_fd(const ViewRec* __restrict__ views, DetC dc, GridC g, const float2* __re
     const unsigned long long base = (unsigned long long)fd - 8ull * kMagicBits;
     const unsigned long long cstride = 16ull * (unsigned long long)L.nzp;
     bool zinit = !tiled;  // untiled: the z state at sigma = 0 is the initial one
+    const ColDesc* dsc = desc + ((int64_t)v * dc.cols + c);
     for (int n0 = na; n0 < nb; n0 += 32) {
+        ColumnPath Pc;
+        if constexpr (NP == 2) load_path_chunk(dsc, g.n[0], Pc);   // (NP = 1 has registers to spare)
+        else Pc = Pth;
         // chunk origin: the start of slice n0 (the same fmaf every lane and the slices use)
-        const float sc = n0 == 0 ? 0.f : fminf(fmaf((float)(n0 - 1), Pth.dta, Pth.t0a), Pth.L);
+        const float sc = n0 == 0 ? 0.f : fminf(fmaf((float)(n0 - 1), Pc.dta, Pc.t0a), Pc.L);
         const int n = n0 + lane;
         float a0s = 0.f, a0e = 0.f, a1s = 0.f, a1e = 0.f;
         int c0 = 0, c1 = 0, cnt = 0;
-        if (n < nb) cnt = slice_segments(Pth, n, ti0, ti1, tj0, tj1, a0s, a0e, c0, a1s, a1e, c1);
+        if (n < nb) cnt = slice_segments(Pc, n, ti0, ti1, tj0, tj1, a0s, a0e, c0, a1s, a1e, c1);
         int incl = cnt;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
@@ -1266,9 +1293,11 @@ k_fwd_fd(const ViewRec* __restrict__ views, DetC dc, GridC g, const float2* __re
 #pragma unroll
     for (int q = 0; q < R; ++q) {
         const FdPair& Q = P[q >> 1];
-        if (!((q & 1) ? Q.live1 : Q.live0)) continue;
-        const float a = (q & 1) ? (Q.acc0b + Q.acc1b) * Q.w.y : (Q.acc0a + Q.acc1a) * Q.w.x;
-        const int64_t m = ((int64_t)v * dc.rows + (band * R + q) * 32 + lane) * dc.cols + c;
+        const int r = (band * R + q) * 32 + lane;
+        if (r >= dc.rows) continue;                // ray_z's `active` (the column hits the square)
+        const float a = (q & 1) ? (Q.acc0b + Q.acc1b) * fd_scale(Q.ndtz.y, (float)g.d[2])
+                                : (Q.acc0a + Q.acc1a) * fd_scale(Q.ndtz.x, (float)g.d[2]);
+        const int64_t m = ((int64_t)v * dc.rows + r) * dc.cols + c;
         if (tiled) { if (a != 0.f) red_sino(sino_out + m, a, l2_evict_first()); }
         else __stcs(sino_out + m, a);
     }
