@@ -1126,8 +1126,14 @@ __device__ __forceinline__ float2 ldg_f2(unsigned long long a) {
 // the chunk's segments for the lane's 2 NP rays: per segment (pointer, sigma_e - sigma_c, d_sigma)
 // and ray, z crossing cr = [tau < sigma_e], l_e = max(sigma_e - tau, 0), then the state advances;
 // software-pipelined one segment deep (the next segment's loads issue before this one's FMAs).
+// segments per trip: cfg 4 (NP = 2) 121.0 ms at 2 vs 140.2 (1) / 134.2 (4); cfg 5 (NP = 1) 18.4 ms at
+// 4 vs 19.6 (2)
+#ifndef XRT_FD_UNROLL
+#define XRT_FD_UNROLL 0   // 0: by NP
+#endif
 template <int NP>
 __device__ __forceinline__ void fd_segments(unsigned seg, int total, FdPair (&P)[NP]) {
+    constexpr int kFdUnroll = XRT_FD_UNROLL > 0 ? XRT_FD_UNROLL : (NP == 1 ? 4 : 2);
     uint4 raw = lds128(seg);
     float2 va[NP], vb[NP];
 #pragma unroll
@@ -1135,7 +1141,7 @@ __device__ __forceinline__ void fd_segments(unsigned seg, int total, FdPair (&P)
         va[p] = ldg_f2(seg_ptr(raw) + 8ull * __float_as_uint(P[p].kpf.x));
         vb[p] = ldg_f2(seg_ptr(raw) + 8ull * __float_as_uint(P[p].kpf.y));
     }
-#pragma unroll 2
+#pragma unroll kFdUnroll
     for (int s = 0; s < total; ++s) {
         const float qse = __uint_as_float(raw.z), qds = __uint_as_float(raw.w);
         const float2 se2 = make_float2(qse, qse);
@@ -1166,7 +1172,7 @@ __device__ __forceinline__ void fd_segments(unsigned seg, int total, FdPair (&P)
 #define XRT_FD_THREADS 1024  // resident threads per SM targeted by the launch bounds (2 pairs per lane):
 #endif                       // cfg 4 124.0 ms vs 136.0 (768), 138.9 (512); 4 x 4 CTAs 126.6
 #ifndef XRT_FD_THREADS1
-#define XRT_FD_THREADS1 768  // ... 1 pair per lane
+#define XRT_FD_THREADS1 1024 // ... 1 pair per lane (cfg 5: 18.2 ms vs 18.4 at 768, 19.6 at 512)
 #endif
 #define XRT_FD_MINB (XRT_FD_THREADS / (32 * kFdWarps) > 0 ? XRT_FD_THREADS / (32 * kFdWarps) : 1)
 
@@ -1246,8 +1252,7 @@ k_fwd_fd(const ViewRec* __restrict__ views, DetC dc, GridC g, const float2* __re
     const ColDesc* dsc = desc + ((int64_t)v * dc.cols + c);
     for (int n0 = na; n0 < nb; n0 += 32) {
         ColumnPath Pc;
-        if constexpr (NP == 2) load_path_chunk(dsc, g.n[0], Pc);   // (NP = 1 has registers to spare)
-        else Pc = Pth;
+        load_path_chunk(dsc, g.n[0], Pc);
         // chunk origin: the start of slice n0 (the same fmaf every lane and the slices use)
         const float sc = n0 == 0 ? 0.f : fminf(fmaf((float)(n0 - 1), Pc.dta, Pc.t0a), Pc.L);
         const int n = n0 + lane;
