@@ -628,6 +628,10 @@ __device__ __forceinline__ void column_segments_adj_flat(unsigned seg, int total
     }
 }
 
+#ifndef XRT_ADJ_UNROLL
+#define XRT_ADJ_UNROLL 2
+#endif
+constexpr int kAdjUnroll = XRT_ADJ_UNROLL;
 // Adjoint: the same units, y l scattered with red.global.add (the second unit only when the z
 // crossing lies inside the segment).
 template <int NP, int DK>
@@ -636,7 +640,7 @@ __device__ __forceinline__ void column_segments_adj(unsigned seg, int total, Ray
     const float2 m1 = make_float2(-1.f, -1.f);
     const unsigned long long pol = l2_evict_last();
     float kpf_in0[NP], kpf_in1[NP];
-#pragma unroll 2
+#pragma unroll kAdjUnroll
     for (int s = 0; s < total; ++s) {
         const uint4 raw = lds128(seg + 16u * (unsigned)s);
         const float qse = __uint_as_float(raw.z), qds = __uint_as_float(raw.w);
