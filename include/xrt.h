@@ -186,6 +186,15 @@ xrt_status xrt_adjoint_stage(xrt_plan p, const float* sino, float* img, int32_t 
 xrt_status xrt_forward_f64(xrt_plan p, const double* img, double* sino, void* cuda_stream);
 xrt_status xrt_adjoint_f64(xrt_plan p, const double* sino, double* img, void* cuda_stream);
 
+/* Mixed precision (SURVEY 8(f) N2's "fp32-length / fp64-accumulate"): the fp32 unit walk of
+ * the RAY family (the telescoped fp32 lengths C_up - C_low of xrt_forward), each product and every
+ * sum in fp64.  img / sino: device fp64, layouts as xrt_forward_f64; the output is fully overwritten.
+ * Forward and adjoint walk identical fp32 lengths, so <A x, y> = <x, A^T y> to fp64 rounding; the
+ * adjoint accumulates with fp64 atomics (last bits order dependent).  Errors: XRT_ERR_INVALID_ARG
+ * on NULL pointers; launch errors as XRT_ERR_CUDA. */
+xrt_status xrt_forward_mixed(xrt_plan p, const double* img, double* sino, void* cuda_stream);
+xrt_status xrt_adjoint_mixed(xrt_plan p, const double* sino, double* img, void* cuda_stream);
+
 /* Attenuated X-ray transform (the generalized transform R_Phi of eq:generalizedRadontransform,
  * P:36-40, with the SPECT weight Phi(theta, x, t) = exp(-int_t^inf mu(x + s theta) ds); SURVEY 8(f)
  * N4, reading 23).  f = img and mu are unit-basis images on the plan's grid (eq:f_represent,

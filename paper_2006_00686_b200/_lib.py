@@ -26,6 +26,7 @@ ALGOS = {"auto": 0, "ray": 1, "column": 2, "gather": 3}
 EXPORTS = ("xrt_plan_create", "xrt_plan_create_rays", "xrt_plan_destroy", "xrt_plan_query", "xrt_plan_set_algorithm",
            "xrt_plan_launch_count", "xrt_forward", "xrt_adjoint", "xrt_forward_host",
            "xrt_adjoint_host", "xrt_forward_f64", "xrt_adjoint_f64",
+           "xrt_forward_mixed", "xrt_adjoint_mixed",
            "xrt_forward_attenuated", "xrt_adjoint_attenuated", "xrt_ray_units", "xrt_last_error", "xrt_version",
            "xrt_adjoint_stages", "xrt_adjoint_stage")
 
@@ -86,6 +87,8 @@ def load(path: str | None = None) -> ctypes.CDLL:
             "xrt_forward_host": (i32, [vp, vp, vp, vp]),
             "xrt_forward_f64": (i32, [vp, vp, vp, vp]),
             "xrt_adjoint_f64": (i32, [vp, vp, vp, vp]),
+            "xrt_forward_mixed": (i32, [vp, vp, vp, vp]),
+            "xrt_adjoint_mixed": (i32, [vp, vp, vp, vp]),
             "xrt_forward_attenuated": (i32, [vp, vp, vp, vp, vp]),
             "xrt_adjoint_attenuated": (i32, [vp, vp, vp, vp, vp]),
             "xrt_adjoint_host": (i32, [vp, vp, vp, vp]),

@@ -778,6 +778,28 @@ xrt_status xrt_adjoint_f64(xrt_plan p, const double* sino, double* img, void* cu
     return XRT_OK;
 }
 
+xrt_status xrt_forward_mixed(xrt_plan p, const double* img, double* sino, void* cuda_stream) {
+    NvtxRange nvtx_("xrt_forward_mixed");
+    if (!p || !img || !sino) return fail(XRT_ERR_INVALID_ARG, "NULL argument");
+    DevGuard guard(p->device);
+    cudaError_t e = xrt::launch_forward_mixed(p, img, sino, 0, p->n_rays, (cudaStream_t)cuda_stream);
+    p->launches += 1;
+    if (e != cudaSuccess) return cuda_fail(e, "forward_mixed launch");
+    return XRT_OK;
+}
+
+xrt_status xrt_adjoint_mixed(xrt_plan p, const double* sino, double* img, void* cuda_stream) {
+    NvtxRange nvtx_("xrt_adjoint_mixed");
+    if (!p || !img || !sino) return fail(XRT_ERR_INVALID_ARG, "NULL argument");
+    DevGuard guard(p->device);
+    cudaStream_t s = (cudaStream_t)cuda_stream;
+    XRT_CUDA(cudaMemsetAsync(img, 0, sizeof(double) * (size_t)p->grid.nxyz, s));
+    cudaError_t e = xrt::launch_adjoint_mixed(p, sino, img, 0, p->n_rays, s);
+    p->launches += 1;
+    if (e != cudaSuccess) return cuda_fail(e, "adjoint_mixed launch");
+    return XRT_OK;
+}
+
 // Attenuated transform: the column kernels for the 3D beams they serve (tiled per
 // band with a per-ray combine of the tile pieces, xrt::att_tiled; untiled otherwise), else the RAY
 // family.  Workspace on first use: the forward's interleaved (f, mu) z-fastest volume, the tile

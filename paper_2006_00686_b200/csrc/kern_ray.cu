@@ -143,6 +143,55 @@ __global__ void __launch_bounds__(256) k_adjoint_ray(const ViewRec* __restrict__
     }
 }
 
+// fp32 lengths / fp64 accumulation (SURVEY 8(f) N2's mixed mode): the fp32 walk of
+// k_forward_ray (the same telescoped lengths C_up - C_low), products and sums in fp64 over fp64
+// images / sinograms.  The adjoint walks the same lengths, so the pair is adjoint to fp64 rounding.
+__global__ void __launch_bounds__(128) k_forward_mixed(const ViewRec* __restrict__ views, DetC dc, GridC g,
+                                                       const double* __restrict__ img, double* __restrict__ sino,
+                                                       int64_t ray0, int64_t ray1) {
+    const int64_t m = ray0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (m >= ray1) return;
+    int v, r, c;
+    ray_of(m, dc, v, r, c);
+    Ray64 R;
+    double acc = 0.0;
+    if (setup_ray(views[v], dc, g, r, c, R)) {
+        Ray32 S;
+        to_ray32(R, g, S);
+        float tc = 0.f;
+        for (int it = 0; tc < S.tend && it < S.budget; ++it) {
+            const float tn = fminf(fminf(S.T[0], S.T[1]), fminf(S.T[2], S.tend));
+            acc = fma(__ldg(img + S.idx), (double)(tn - tc), acc);
+            tc = tn;
+            advance(S, tn);
+        }
+    }
+    sino[m] = acc;
+}
+
+__global__ void __launch_bounds__(128) k_adjoint_mixed(const ViewRec* __restrict__ views, DetC dc, GridC g,
+                                                       const double* __restrict__ sino, double* __restrict__ img,
+                                                       int64_t ray0, int64_t ray1) {
+    const int64_t m = ray0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (m >= ray1) return;
+    const double y = sino[m];
+    if (y == 0.0) return;
+    int v, r, c;
+    ray_of(m, dc, v, r, c);
+    Ray64 R;
+    if (!setup_ray(views[v], dc, g, r, c, R)) return;
+    Ray32 S;
+    to_ray32(R, g, S);
+    float tc = 0.f;
+    for (int it = 0; tc < S.tend && it < S.budget; ++it) {
+        const float tn = fminf(fminf(S.T[0], S.T[1]), fminf(S.T[2], S.tend));
+        const float l = tn - tc;
+        if (l > 0.f) atomicAdd(img + S.idx, y * (double)l);
+        tc = tn;
+        advance(S, tn);
+    }
+}
+
 // fp64 enumeration for the CSR dump: crossing values recomputed exactly as the clip computed
 // the face values, so an axis never steps through the image face (see setup_ray).
 template <bool kFill>
@@ -425,6 +474,20 @@ cudaError_t launch_adjoint64(const xrt_plan_s* p, const double* sino, double* im
                              int64_t ray1, cudaStream_t s) {
     if (ray1 <= ray0) return cudaSuccess;
     k_adjoint64<<<blocks_for(ray1 - ray0, 128), 128, 0, s>>>(p->d_views, p->det, p->grid, sino, img, ray0, ray1);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_forward_mixed(const xrt_plan_s* p, const double* img, double* sino, int64_t ray0,
+                                 int64_t ray1, cudaStream_t s) {
+    if (ray1 <= ray0) return cudaSuccess;
+    k_forward_mixed<<<blocks_for(ray1 - ray0, 128), 128, 0, s>>>(p->d_views, p->det, p->grid, img, sino, ray0, ray1);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_adjoint_mixed(const xrt_plan_s* p, const double* sino, double* img, int64_t ray0,
+                                 int64_t ray1, cudaStream_t s) {
+    if (ray1 <= ray0) return cudaSuccess;
+    k_adjoint_mixed<<<blocks_for(ray1 - ray0, 128), 128, 0, s>>>(p->d_views, p->det, p->grid, sino, img, ray0, ray1);
     return cudaGetLastError();
 }
 

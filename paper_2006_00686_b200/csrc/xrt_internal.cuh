@@ -287,6 +287,10 @@ cudaError_t launch_forward64(const xrt_plan_s* p, const double* img, double* sin
                              int64_t ray1, cudaStream_t s);
 cudaError_t launch_adjoint64(const xrt_plan_s* p, const double* sino, double* img, int64_t ray0,
                              int64_t ray1, cudaStream_t s);
+cudaError_t launch_forward_mixed(const xrt_plan_s* p, const double* img, double* sino, int64_t ray0,
+                                 int64_t ray1, cudaStream_t s);
+cudaError_t launch_adjoint_mixed(const xrt_plan_s* p, const double* sino, double* img, int64_t ray0,
+                                 int64_t ray1, cudaStream_t s);
 cudaError_t launch_units_fill(const xrt_plan_s* p, int64_t ray0, int64_t ray1,
                               const int64_t* row_ptr, int64_t* cols, double* lens, cudaStream_t s);
 // kernels (kern_column.cu)

@@ -185,6 +185,24 @@ class Plan:
         check(self._lib.xrt_adjoint_f64(self._h, sino.data_ptr(), out.data_ptr(), _stream_handle(stream, self.device)))
         return out
 
+    def forward_mixed(self, img: torch.Tensor, out: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+        """xrt_forward_mixed: fp32 lengths, fp64 products and sums (fp64 buffers)."""
+        self._check_dev(img, self.image_shape, "img", torch.float64)
+        if out is None:
+            out = torch.empty(self.sino_shape, dtype=torch.float64, device=img.device)
+        self._check_dev(out, self.sino_shape, "sino", torch.float64)
+        check(self._lib.xrt_forward_mixed(self._h, img.data_ptr(), out.data_ptr(), _stream_handle(stream, self.device)))
+        return out
+
+    def adjoint_mixed(self, sino: torch.Tensor, out: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+        """xrt_adjoint_mixed."""
+        self._check_dev(sino, self.sino_shape, "sino", torch.float64)
+        if out is None:
+            out = torch.empty(self.image_shape, dtype=torch.float64, device=sino.device)
+        self._check_dev(out, self.image_shape, "img", torch.float64)
+        check(self._lib.xrt_adjoint_mixed(self._h, sino.data_ptr(), out.data_ptr(), _stream_handle(stream, self.device)))
+        return out
+
     def forward_attenuated(self, img: torch.Tensor, mu: torch.Tensor, out: torch.Tensor | None = None,
                            stream=None) -> torch.Tensor:
         """xrt_forward_attenuated: sino[m] = sum_I img[I] exp(-A_mI) (1 - exp(-mu_I l_mI)) / mu_I

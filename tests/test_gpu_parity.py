@@ -394,6 +394,44 @@ def test_forward64_agrees_with_fp32(cuda_ok):
     assert H.fwd_err(a.cpu().numpy().ravel(), b.cpu().numpy().ravel()) <= H.FWD_TOL
 
 
+# ------------------------------------------- fp32 lengths / fp64 accumulation
+@pytest.mark.parametrize("idx", [1, 2, 3, 4, 5])
+def test_forward_mixed_small_every_ray(cuda_ok, idx):
+    """xrt_forward_mixed against the fp64 oracle on every ray: only the fp32 lengths round (the
+    north_star 1e-5 bar), and no worse than 2x the fp32 forward's own error."""
+    c = H.small_config(idx)
+    p = _plan(c)
+    img = _image(c)
+    mixed = p.forward_mixed(img.double()).cpu().numpy().ravel()
+    ref = H.oracle_forward(c, img.cpu(), H.ray_ids_all(c))
+    err = H.fwd_err(mixed, ref)
+    assert err <= H.FWD_TOL
+    err32 = H.fwd_err(_plan(c, "ray").forward(img).double().cpu().numpy().ravel(), ref)
+    assert err <= 2 * err32 + 1e-9
+
+
+@pytest.mark.parametrize("idx", [1, 2, 3, 4, 5])
+def test_mixed_pair_adjoint_to_fp64_rounding(cuda_ok, idx):
+    """Forward and adjoint of the mixed mode walk identical fp32 lengths: <A x, y> = <x, A^T y> to
+    fp64 rounding (sums of ~1e6 products), far tighter than the fp32 pair's 1e-5; the sparse adjoint
+    matches the oracle's scatter."""
+    c = H.small_config(idx)
+    p = _plan(c)
+    rng = np.random.Generator(np.random.PCG64(970 + idx))
+    x = torch.from_numpy(rng.uniform(0, 1, p.image_shape)).cuda()
+    y = torch.from_numpy(rng.uniform(-1, 1, p.sino_shape)).cuda()
+    ax = p.forward_mixed(x)
+    aty = p.adjoint_mixed(y)
+    lhs, rhs = float((ax * y).sum()), float((x * aty).sum())
+    scale = float(ax.norm() * y.norm() + x.norm() * aty.norm())
+    assert abs(lhs - rhs) <= 1e-12 * scale
+    ids = workloads.sample_rays(c, min(p.n_rays, 2000), seed=980 + idx)
+    ys = np.zeros(p.n_rays)
+    ys[ids] = rng.uniform(-1, 1, size=ids.size)
+    back = p.adjoint_mixed(torch.from_numpy(ys).reshape(p.sino_shape).cuda())
+    assert H.rel_l2(back.cpu().numpy().ravel(), H.oracle_adjoint(c, ys[ids], ids)) <= 1e-5
+
+
 # ------------------------------------------------------------------- cylindrical detector (N1)
 def _curved(idx):
     c = H.small_config(idx)
