@@ -254,6 +254,16 @@ class Plan:
         check(self._lib.xrt_adjoint_host(self._h, sino.data_ptr(), out.data_ptr(), _stream_handle(stream, self.device)))
         return out
 
+    def ray_unit_counts(self, ray_begin: int, ray_end: int, stream=None) -> torch.Tensor:
+        """xrt_ray_units count-only (cols = lens = NULL): |index set| of every ray in the range, int64
+        CUDA tensor (the fp64 enumeration's drop threshold applies)."""
+        n = int(ray_end) - int(ray_begin)
+        row_ptr = torch.empty(max(n, 0) + 1, dtype=torch.int64, device=torch.device("cuda", self.device))
+        nnz = ctypes.c_int64()
+        check(self._lib.xrt_ray_units(self._h, int(ray_begin), int(ray_end), row_ptr.data_ptr(), None, None,
+                                      0, ctypes.byref(nnz), _stream_handle(stream, self.device)))
+        return row_ptr[1:] - row_ptr[:-1]
+
     def ray_units(self, ray_begin: int, ray_end: int, stream=None):
         """xrt_ray_units (two-phase): CSR (row_ptr, cols, lens) as CUDA tensors (int64, int64, fp64)."""
         n = int(ray_end) - int(ray_begin)
