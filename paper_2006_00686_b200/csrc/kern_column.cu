@@ -522,6 +522,21 @@ __device__ __forceinline__ unsigned long long seg_ptr(const uint4& raw) {
     return ((unsigned long long)raw.y << 32) | raw.x;
 }
 
+// segment pointer + 4 bits(kpf) (float cells): shift-and-add (LEA / LEA.HI.X on the ALU pipe) or
+// IMAD.WIDE (FMA-heavy pipe) -- XRT_COL_LEA
+#ifndef XRT_COL_LEA
+#define XRT_COL_LEA 0
+#endif
+__device__ __forceinline__ float* col_addr(unsigned long long ptr, float kpf) {
+#if XRT_COL_LEA
+    unsigned long long a;
+    asm("{ .reg .u64 t; cvt.u64.u32 t, %2; shl.b64 t, t, 2; add.s64 %0, %1, t; }" : "=l"(a) : "l"(ptr), "r"(__float_as_uint(kpf)));
+    return (float*)a;
+#else
+    return (float*)(ptr + 4ull * __float_as_uint(kpf));
+#endif
+}
+
 // z crossing inside the segment: cr = 1 if tau < sigma_e, lm = l_e = max(sigma_e - tau, 0); then
 // the ray's z state advances to the next segment.
 template <int DK>
@@ -558,8 +573,8 @@ __device__ __forceinline__ void column_segments_fwd(unsigned seg, int total, Ray
     float2 f0[NP], f1[NP];
 #pragma unroll
     for (int p = 0; p < NP; ++p) {
-        const float* a0 = (const float*)(seg_ptr(raw) + 4ull * __float_as_uint(P[p].kpf.x));
-        const float* a1 = (const float*)(seg_ptr(raw) + 4ull * __float_as_uint(P[p].kpf.y));
+        const float* a0 = col_addr(seg_ptr(raw), P[p].kpf.x);
+        const float* a1 = col_addr(seg_ptr(raw), P[p].kpf.y);
         const int o0 = DK != 0 ? DK : P[p].dk0, o1 = DK != 0 ? DK : P[p].dk1;
         f0[p] = make_float2(__ldg(a0), __ldg(a1));
         f1[p] = make_float2(__ldg(a0 + o0), __ldg(a1 + o1));
@@ -574,8 +589,8 @@ __device__ __forceinline__ void column_segments_fwd(unsigned seg, int total, Ray
             float2 cr, lm;
             z_step<DK>(P[p], se2, cr, lm);
             // next segment's loads (cells from the advanced z state)
-            const float* a0 = (const float*)(seg_ptr(nraw) + 4ull * __float_as_uint(P[p].kpf.x));
-            const float* a1 = (const float*)(seg_ptr(nraw) + 4ull * __float_as_uint(P[p].kpf.y));
+            const float* a0 = col_addr(seg_ptr(nraw), P[p].kpf.x);
+            const float* a1 = col_addr(seg_ptr(nraw), P[p].kpf.y);
             const int o0 = DK != 0 ? DK : P[p].dk0, o1 = DK != 0 ? DK : P[p].dk1;
             const float2 g0 = make_float2(__ldg(a0), __ldg(a1));
             const float2 g1 = make_float2(__ldg(a0 + o0), __ldg(a1 + o1));
@@ -601,8 +616,8 @@ __device__ __forceinline__ void column_segments_fwd_flat(unsigned seg, int total
         const float2 ds2 = make_float2(qds, qds);
 #pragma unroll
         for (int p = 0; p < NP; ++p) {
-            const float* a0 = (const float*)(seg_ptr(raw) + 4ull * __float_as_uint(P[p].kpf.x));
-            const float* a1 = (const float*)(seg_ptr(raw) + 4ull * __float_as_uint(P[p].kpf.y));
+            const float* a0 = col_addr(seg_ptr(raw), P[p].kpf.x);
+            const float* a1 = col_addr(seg_ptr(raw), P[p].kpf.y);
             P[p].acc0 = __ffma2_rn(make_float2(__ldg(a0), __ldg(a1)), ds2, P[p].acc0);
         }
     }
@@ -619,8 +634,8 @@ __device__ __forceinline__ void column_segments_adj_flat(unsigned seg, int total
         const float2 ds2 = make_float2(qds, qds);
 #pragma unroll
         for (int p = 0; p < NP; ++p) {
-            float* a0 = (float*)(seg_ptr(raw) + 4ull * __float_as_uint(P[p].kpf.x));
-            float* a1 = (float*)(seg_ptr(raw) + 4ull * __float_as_uint(P[p].kpf.y));
+            float* a0 = col_addr(seg_ptr(raw), P[p].kpf.x);
+            float* a1 = col_addr(seg_ptr(raw), P[p].kpf.y);
             const float2 ws = __fmul2_rn(P[p].w, ds2);
             if (P[p].live0 && __float_as_uint(P[p].kpf.x) - klo < kn) red_add(a0, ws.x, pol);
             if (P[p].live1 && __float_as_uint(P[p].kpf.y) - klo < kn) red_add(a1, ws.y, pol);
@@ -647,8 +662,8 @@ __device__ __forceinline__ void column_segments_adj(unsigned seg, int total, Ray
         const float2 se2 = make_float2(qse, qse), ds2 = make_float2(qds, qds);
 #pragma unroll
         for (int p = 0; p < NP; ++p) {
-            float* a0 = (float*)(seg_ptr(raw) + 4ull * __float_as_uint(P[p].kpf.x));
-            float* a1 = (float*)(seg_ptr(raw) + 4ull * __float_as_uint(P[p].kpf.y));
+            float* a0 = col_addr(seg_ptr(raw), P[p].kpf.x);
+            float* a1 = col_addr(seg_ptr(raw), P[p].kpf.y);
             const int o0 = DK != 0 ? DK : P[p].dk0, o1 = DK != 0 ? DK : P[p].dk1;
             kpf_in0[p] = P[p].kpf.x;
             kpf_in1[p] = P[p].kpf.y;
@@ -738,8 +753,8 @@ __device__ __forceinline__ void column_segments_adj_att(unsigned seg, int total,
         const float2 se2 = make_float2(qse, qse), ds2 = make_float2(qds, qds);
 #pragma unroll
         for (int p = 0; p < NP; ++p) {
-            const float* a0 = (const float*)(seg_ptr(raw) + 4ull * __float_as_uint(P[p].kpf.x));
-            const float* a1 = (const float*)(seg_ptr(raw) + 4ull * __float_as_uint(P[p].kpf.y));
+            const float* a0 = col_addr(seg_ptr(raw), P[p].kpf.x);
+            const float* a1 = col_addr(seg_ptr(raw), P[p].kpf.y);
             const int o0 = DK != 0 ? DK : P[p].dk0, o1 = DK != 0 ? DK : P[p].dk1;
             const float2 mus = make_float2(__ldg(a0), __ldg(a1)), mue = make_float2(__ldg(a0 + o0), __ldg(a1 + o1));
             const unsigned kb0 = __float_as_uint(P[p].kpf.x) - klo, kb1 = __float_as_uint(P[p].kpf.y) - klo;
@@ -1121,6 +1136,21 @@ __device__ __forceinline__ void fd_anchor(FdPair& P, float sc) {
     P.ntz = make_float2(sc - tau.x, sc - tau.y);
 }
 
+// segment pointer + 8 bits(kpf): shift-and-add (LEA / LEA.HI.X, ALU pipe) instead of IMAD.WIDE
+// (FMA-heavy pipe, which the walk's packed FP32 ops keep ~61 % busy) -- XRT_FD_LEA
+#ifndef XRT_FD_LEA
+#define XRT_FD_LEA 1   // cfg 4 121.0 -> 116.5 ms, cfg 5 17.5 -> 16.7
+#endif
+__device__ __forceinline__ unsigned long long fd_addr(unsigned long long ptr, float kpf) {
+#if XRT_FD_LEA
+    unsigned long long a;
+    asm("{ .reg .u64 t; cvt.u64.u32 t, %2; shl.b64 t, t, 3; add.s64 %0, %1, t; }" : "=l"(a) : "l"(ptr), "r"(__float_as_uint(kpf)));
+    return a;
+#else
+    return ptr + 8ull * __float_as_uint(kpf);
+#endif
+}
+
 __device__ __forceinline__ float2 ldg_f2(unsigned long long a) {
     float2 v;
     asm("ld.global.nc.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "l"(a));
@@ -1142,8 +1172,8 @@ __device__ __forceinline__ void fd_segments(unsigned seg, int total, FdPair (&P)
     float2 va[NP], vb[NP];
 #pragma unroll
     for (int p = 0; p < NP; ++p) {
-        va[p] = ldg_f2(seg_ptr(raw) + 8ull * __float_as_uint(P[p].kpf.x));
-        vb[p] = ldg_f2(seg_ptr(raw) + 8ull * __float_as_uint(P[p].kpf.y));
+        va[p] = ldg_f2(fd_addr(seg_ptr(raw), P[p].kpf.x));
+        vb[p] = ldg_f2(fd_addr(seg_ptr(raw), P[p].kpf.y));
     }
 #pragma unroll kFdUnroll
     for (int s = 0; s < total; ++s) {
@@ -1158,8 +1188,8 @@ __device__ __forceinline__ void fd_segments(unsigned seg, int total, FdPair (&P)
             const float lma = lm.x, lmb = lm.y;
             P[p].kpf = __ffma2_rn(cr, P[p].dkf, P[p].kpf);
             P[p].ntz = __ffma2_rn(cr, P[p].ndtz, P[p].ntz);
-            const float2 na = ldg_f2(seg_ptr(nraw) + 8ull * __float_as_uint(P[p].kpf.x));
-            const float2 nb = ldg_f2(seg_ptr(nraw) + 8ull * __float_as_uint(P[p].kpf.y));
+            const float2 na = ldg_f2(fd_addr(seg_ptr(nraw), P[p].kpf.x));
+            const float2 nb = ldg_f2(fd_addr(seg_ptr(nraw), P[p].kpf.y));
             P[p].acc0a = fmaf(va[p].x, qds, P[p].acc0a);                  // f_s d_sigma
             P[p].acc1a = fmaf(va[p].y, lma, P[p].acc1a);                  // (f_e - f_s) l_e
             P[p].acc0b = fmaf(vb[p].x, qds, P[p].acc0b);
