@@ -5,6 +5,7 @@
 //                 column adjoint's start-cell reductions on cfg 4)
 //   scattered  : 32 lanes -> 32 different sectors (1 element per sector)
 //   adjoint_dedup: the adjoint-like cells with the duplicate lanes idle (each cell once per warp)
+//   adjoint_dedup_shfl: the adjoint-like cells, each duplicate pair merged by 3 shuffles (the kernel's way)
 //   adj_cross_*: adjoint-like main cells plus a z-crossing unit (cell + 1) on every 5th lane, as two
 //                scalar reds, or as one 16-byte red.v4 of the quad holding both (spill: the crossing
 //                cell in the next quad -> a scalar red) -- "sectors_per_s" counts the main cells only
@@ -23,7 +24,16 @@ __global__ void k_red(float* __restrict__ buf, unsigned mask_floats, int iters, 
         else if (pattern == 1) off = base + (lane * 2u) / 3u;
         else off = base + lane * 8u;
         float* a = buf + (off & mask_floats);
-        if (pattern >= 4) {   // adjoint-like main cells + a z crossing on every 6th lane
+        if (pattern == 7) {   // adjoint-like cells, duplicates merged into the lower lane by shuffles
+            off = base + (lane * 2u) / 3u;
+            const float v = 1.0f;
+            const unsigned offn = __shfl_down_sync(0xffffffffu, off, 1);
+            const float vn = __shfl_down_sync(0xffffffffu, v, 1);
+            const unsigned offp = __shfl_up_sync(0xffffffffu, off, 1);
+            const float w = v + ((lane < 31 && offn == off) ? vn : 0.f);
+            if (!(lane > 0 && offp == off))
+                asm volatile("red.global.add.f32 [%0], %1;" :: "l"(buf + (off & mask_floats)), "f"(w) : "memory");
+        } else if (pattern >= 4) {   // adjoint-like main cells + a z crossing on every 6th lane
             off = base + (lane * 2u) / 3u;
             const bool cross = lane % 5u == 2u;
             if (pattern == 4) {   // scalar: main red, then the crossing red (cell + 1) where it crosses
@@ -62,15 +72,15 @@ int main() {
     cudaDeviceGetAttribute(&clk_khz, cudaDevAttrClockRate, 0);
     const int blocks = sms * 8, threads = 256, iters = 4096;
     const double warps = (double)blocks * threads / 32;
-    const double sectors_per_inst[7] = {4.0, 3.0, 32.0, 3.0, 3.0, 3.0, 3.0};
+    const double sectors_per_inst[8] = {4.0, 3.0, 32.0, 3.0, 3.0, 3.0, 3.0, 3.0};
     const double elems_per_inst = 32.0;   // for pattern 3: the 32 lanes' units, carried by 22 lanes
-    const char* names[7] = {"coalesced", "adjoint_like", "scattered", "adjoint_dedup", "adj_cross_scalar",
-                            "adj_cross_v4_spill", "adj_cross_v4"};
+    const char* names[8] = {"coalesced", "adjoint_like", "scattered", "adjoint_dedup", "adj_cross_scalar",
+                            "adj_cross_v4_spill", "adj_cross_v4", "adjoint_dedup_shfl"};
     cudaEvent_t e0, e1;
     cudaEventCreate(&e0);
     cudaEventCreate(&e1);
     printf("{\"sms\": %d, \"clock_mhz_attr\": %.0f", sms, clk_khz / 1e3);
-    for (int p = 0; p < 7; ++p) {
+    for (int p = 0; p < 8; ++p) {
         k_red<<<blocks, threads>>>(buf, (unsigned)(n - 1), 64, p);   // warm-up
         cudaEventRecord(e0);
         for (int r = 0; r < 5; ++r) k_red<<<blocks, threads>>>(buf, (unsigned)(n - 1), iters, p);
