@@ -507,6 +507,7 @@ xrt_status plan_create_impl(const xrt_geometry* g, int cuda_device, xrt_plan* ou
         // forward on the (f, delta f) volume, except where no ray crosses a z plane (3D parallel beam
         // without tilt: the legacy kernel's flat walk, one 4-byte load per unit, is faster there)
         p->fd_forward = !std::getenv("XRT_FWD_LEGACY") && !(g->beam == XRT_PAR3D && g->tilt == 0.0);
+        p->flat_z = g->beam == XRT_PAR3D && g->tilt == 0.0;
         if (e == cudaSuccess && p->fd_forward) {
             const size_t fdb = 2 * sizeof(float2) * (size_t)(G.nxy * p->nzp);
             e = cudaMalloc(&p->d_work_fd, fdb);
