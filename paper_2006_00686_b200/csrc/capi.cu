@@ -556,6 +556,25 @@ xrt_status plan_create_impl(const xrt_geometry* g, int cuda_device, xrt_plan* ou
                 if (!items.empty()) e = cudaMalloc(&T.d_items, sizeof(uint2) * items.size());
                 if (e == cudaSuccess && !items.empty())
                     e = cudaMemcpy(T.d_items, items.data(), sizeof(uint2) * items.size(), cudaMemcpyHostToDevice);
+                constexpr int Q = xrt_plan_s::kFwdParts;
+                if (op == 1 && e == cudaSuccess && !items.empty() && p->n_views >= Q) {
+                    // the adjoint items regrouped by view range (item .x = view), tile order kept
+                    std::vector<uint2> parts;
+                    parts.reserve(items.size());
+                    for (int q = 0; q < Q; ++q) {
+                        const int64_t v0 = p->n_views * q / Q, v1 = p->n_views * (q + 1) / Q;
+                        p->adj_part_off[q] = (int64_t)parts.size();
+                        p->adj_part_view[q] = v0;
+                        for (const uint2& w : items)
+                            if ((int64_t)w.x >= v0 && (int64_t)w.x < v1) parts.push_back(w);
+                    }
+                    p->adj_part_off[Q] = (int64_t)parts.size();
+                    p->adj_part_view[Q] = p->n_views;
+                    e = cudaMalloc(&p->d_adj_part_items, sizeof(uint2) * parts.size());
+                    if (e == cudaSuccess)
+                        e = cudaMemcpy(p->d_adj_part_items, parts.data(), sizeof(uint2) * parts.size(),
+                                       cudaMemcpyHostToDevice);
+                }
                 if (op == 0 && p->fd_forward && e == cudaSuccess) {   // the fd forward's CTAs: views x columns
                     xrt_plan_s::ColTiling& F = p->ct_fd;
                     F.tile = T.tile; F.n_tx = T.n_tx; F.n_ty = T.n_ty;
@@ -564,6 +583,26 @@ xrt_status plan_create_impl(const xrt_geometry* g, int cuda_device, xrt_plan* ou
                     if (!items.empty()) e = cudaMalloc(&F.d_items, sizeof(uint2) * items.size());
                     if (e == cudaSuccess && !items.empty())
                         e = cudaMemcpy(F.d_items, items.data(), sizeof(uint2) * items.size(), cudaMemcpyHostToDevice);
+                    // the same items regrouped by view range (parts of whole view blocks), tile order kept
+                    const int64_t VBk = xrt::fd_view_block();
+                    const int64_t nvb = (p->n_views + VBk - 1) / VBk;
+                    if (e == cudaSuccess && !items.empty() && nvb >= Q) {
+                        std::vector<uint2> parts;
+                        parts.reserve(items.size());
+                        for (int q = 0; q < Q; ++q) {
+                            const int64_t b0 = nvb * q / Q, b1 = nvb * (q + 1) / Q;
+                            p->fd_part_off[q] = (int64_t)parts.size();
+                            p->fd_part_view[q] = std::min<int64_t>(p->n_views, b0 * VBk);
+                            for (const uint2& w : items)
+                                if ((int64_t)w.x >= b0 && (int64_t)w.x < b1) parts.push_back(w);
+                        }
+                        p->fd_part_off[Q] = (int64_t)parts.size();
+                        p->fd_part_view[Q] = p->n_views;
+                        e = cudaMalloc(&p->d_fd_part_items, sizeof(uint2) * parts.size());
+                        if (e == cudaSuccess)
+                            e = cudaMemcpy(p->d_fd_part_items, parts.data(), sizeof(uint2) * parts.size(),
+                                           cudaMemcpyHostToDevice);
+                    }
                 }
             }
         }
@@ -693,6 +732,8 @@ xrt_status xrt_plan_destroy(xrt_plan p) {
     cudaFree(p->ct[0].d_items);
     cudaFree(p->ct[1].d_items);
     cudaFree(p->ct_fd.d_items);
+    cudaFree(p->d_fd_part_items);
+    cudaFree(p->d_adj_part_items);
     cudaFree(p->d_coldesc);
     cudaFree(p->d_gather_y);
     cudaFree(p->d_rays);
@@ -932,9 +973,10 @@ xrt_status xrt_forward_host(xrt_plan p, const float* img_host, float* sino_host,
         const int CH = std::max(32, (nz + 15) / 16);
         const int nch = (nz + CH - 1) / CH;
         cudaStream_t d = (cudaStream_t)p->aux_stream2;
-        std::vector<cudaEvent_t> evc((size_t)nch), evb((size_t)nb);
+        std::vector<cudaEvent_t> evc((size_t)nch), evb((size_t)nb), evp((size_t)xrt_plan_s::kFwdParts);
         for (auto& x : evc) XRT_CUDA(cudaEventCreateWithFlags(&x, cudaEventDisableTiming));
         for (auto& x : evb) XRT_CUDA(cudaEventCreateWithFlags(&x, cudaEventDisableTiming));
+        for (auto& x : evp) XRT_CUDA(cudaEventCreateWithFlags(&x, cudaEventDisableTiming));
         // chunk i covers image rows [lo_i, hi_i) in send order; built fd rows after chunk i:
         // desc: [lo_i + 1 .. nz] (row lo_i waits for its lower neighbour), asc: [-1 .. hi_i - 1)
         cudaError_t e = cudaSuccess;
@@ -967,9 +1009,26 @@ xrt_status xrt_forward_host(xrt_plan p, const float* img_host, float* sino_host,
             for (int i = 0; i < nch; ++i)
                 if (done_lo[i] <= std::max(k0, -1) && done_hi[i] >= std::min(k1, nz + 1)) { need = i; break; }
             e = cudaStreamWaitEvent(s, evc[need], 0);
+            const int r0 = b * rb, r1 = std::min(p->det.rows, r0 + rb);
+            if (b == nb - 1 && p->d_fd_part_items) {
+                // the last band part by part (view ranges): each part's rows go down while the next
+                // part computes, so only the last part's copy is exposed
+                for (int q = 0; q < xrt_plan_s::kFwdParts && e == cudaSuccess; ++q) {
+                    const int64_t v0 = p->fd_part_view[q], v1 = p->fd_part_view[q + 1];
+                    e = xrt::launch_forward_fd_band_part(p, p->d_work_fd, p->d_stage_sino, b, q, s);
+                    p->launches += 1;
+                    if (e == cudaSuccess) e = cudaEventRecord(evp[q], s);
+                    if (e == cudaSuccess) e = cudaStreamWaitEvent(d, evp[q], 0);
+                    if (e == cudaSuccess && v1 > v0)
+                        e = cudaMemcpy2DAsync(sino_host + v0 * p->det.per_view + (int64_t)r0 * p->det.cols, pitch,
+                                              p->d_stage_sino + v0 * p->det.per_view + (int64_t)r0 * p->det.cols, pitch,
+                                              sizeof(float) * (size_t)(r1 - r0) * p->det.cols, (size_t)(v1 - v0),
+                                              cudaMemcpyDeviceToHost, d);
+                }
+                continue;
+            }
             if (e == cudaSuccess) e = xrt::launch_forward_fd_bands(p, p->d_work_fd, p->d_stage_sino, b, b + 1, s);
             p->launches += 1;
-            const int r0 = b * rb, r1 = std::min(p->det.rows, r0 + rb);
             if (e == cudaSuccess) e = cudaEventRecord(evb[b], s);
             if (e == cudaSuccess) e = cudaStreamWaitEvent(d, evb[b], 0);
             if (e == cudaSuccess)
@@ -984,6 +1043,7 @@ xrt_status xrt_forward_host(xrt_plan p, const float* img_host, float* sino_host,
         cudaError_t e3 = cudaStreamSynchronize(d);
         for (auto& x : evc) cudaEventDestroy(x);
         for (auto& x : evb) cudaEventDestroy(x);
+        for (auto& x : evp) cudaEventDestroy(x);
         if (e != cudaSuccess) return cuda_fail(e, "forward_host chunked pipeline");
         if (e1 != cudaSuccess) return cuda_fail(e1, "forward_host sync");
         if (e2 != cudaSuccess) return cuda_fail(e2, "forward_host sync");
@@ -1071,16 +1131,36 @@ xrt_status xrt_adjoint_host(xrt_plan p, const float* sino_host, float* img_host,
         for (auto& x : ev) XRT_CUDA(cudaEventCreateWithFlags(&x, cudaEventDisableTiming));
         for (auto& x : evd) XRT_CUDA(cudaEventCreateWithFlags(&x, cudaEventDisableTiming));
         const int64_t nxy = p->grid.nxy;
+        std::vector<cudaEvent_t> evp((size_t)xrt_plan_s::kFwdParts);
+        for (auto& x : evp) XRT_CUDA(cudaEventCreateWithFlags(&x, cudaEventDisableTiming));
         for (int b = 0; b < nb && st == XRT_OK; ++b) {
             const int r0 = b * rb, r1 = std::min(p->det.rows, r0 + rb);
-            cudaError_t e = cudaMemcpy2DAsync(p->d_stage_sino + (int64_t)r0 * p->det.cols, pitch,
-                                              sino_host + (int64_t)r0 * p->det.cols, pitch,
-                                              sizeof(float) * (size_t)(r1 - r0) * p->det.cols,
-                                              (size_t)p->n_views, cudaMemcpyHostToDevice, a);
-            if (e == cudaSuccess) e = cudaEventRecord(ev[b], a);
-            if (e == cudaSuccess) e = cudaStreamWaitEvent(s, ev[b], 0);
-            if (e == cudaSuccess) e = xrt::launch_adjoint_column_bands(p, p->d_stage_sino, p->d_work_adj, b, b + 1, s);
-            p->launches += 1;
+            cudaError_t e = cudaSuccess;
+            if (b == 0 && p->d_adj_part_items) {
+                // the first band part by part (view ranges): each part computes as soon as its rows
+                // are up, so only the first part's upload is exposed
+                for (int q = 0; q < xrt_plan_s::kFwdParts && e == cudaSuccess; ++q) {
+                    const int64_t v0 = p->adj_part_view[q], v1 = p->adj_part_view[q + 1];
+                    if (v1 > v0)
+                        e = cudaMemcpy2DAsync(p->d_stage_sino + v0 * p->det.per_view + (int64_t)r0 * p->det.cols, pitch,
+                                              sino_host + v0 * p->det.per_view + (int64_t)r0 * p->det.cols, pitch,
+                                              sizeof(float) * (size_t)(r1 - r0) * p->det.cols, (size_t)(v1 - v0),
+                                              cudaMemcpyHostToDevice, a);
+                    if (e == cudaSuccess) e = cudaEventRecord(evp[q], a);
+                    if (e == cudaSuccess) e = cudaStreamWaitEvent(s, evp[q], 0);
+                    if (e == cudaSuccess) e = xrt::launch_adjoint_column_band_part(p, p->d_stage_sino, p->d_work_adj, b, q, s);
+                    p->launches += 1;
+                }
+            } else {
+                e = cudaMemcpy2DAsync(p->d_stage_sino + (int64_t)r0 * p->det.cols, pitch,
+                                      sino_host + (int64_t)r0 * p->det.cols, pitch,
+                                      sizeof(float) * (size_t)(r1 - r0) * p->det.cols,
+                                      (size_t)p->n_views, cudaMemcpyHostToDevice, a);
+                if (e == cudaSuccess) e = cudaEventRecord(ev[b], a);
+                if (e == cudaSuccess) e = cudaStreamWaitEvent(s, ev[b], 0);
+                if (e == cudaSuccess) e = xrt::launch_adjoint_column_bands(p, p->d_stage_sino, p->d_work_adj, b, b + 1, s);
+                p->launches += 1;
+            }
             const int64_t k0 = p->adj_stage_k[2 * b], k1 = p->adj_stage_k[2 * b + 1];
             if (e == cudaSuccess && k1 > k0) {
                 e = xrt::launch_from_zfast_rows(p, p->d_work_adj, p->d_stage_img, k0, k1, s);
@@ -1098,6 +1178,7 @@ xrt_status xrt_adjoint_host(xrt_plan p, const float* sino_host, float* img_host,
         cudaError_t e3 = cudaStreamSynchronize(d);
         for (auto& x : ev) cudaEventDestroy(x);
         for (auto& x : evd) cudaEventDestroy(x);
+        for (auto& x : evp) cudaEventDestroy(x);
         if (st != XRT_OK) return st;
         if (e1 != cudaSuccess) return cuda_fail(e1, "adjoint_host sync");
         if (e2 != cudaSuccess) return cuda_fail(e2, "adjoint_host sync");

@@ -1768,6 +1768,31 @@ cudaError_t launch_forward_fd_bands(const xrt_plan_s* p, const float2* fd, float
     return launch_fd(p, fd, sino, L, L.n_items * (b1 - b0), s);
 }
 
+int fd_view_block() { return kFdViews; }
+
+// band b, views [fd_part_view[part], fd_part_view[part + 1]) only (tiled plans; see xrt_plan_s::kFwdParts)
+cudaError_t launch_forward_fd_band_part(const xrt_plan_s* p, const float2* fd, float* sino, int b, int part,
+                                        cudaStream_t s) {
+    if (!p->d_fd_part_items || part < 0 || part >= xrt_plan_s::kFwdParts) return cudaErrorInvalidValue;
+    int nblk = 0;
+    ColumnLaunch L = make_launch(p, 0, p->n_views, nblk, false);
+    L.n_cgroups = (p->det.cols + kFdCols - 1) / kFdCols;
+    L.tile = p->ct_fd.tile;
+    L.n_tx = p->ct_fd.n_tx;
+    L.items = (const uint2*)p->d_fd_part_items + p->fd_part_off[part];
+    L.n_items = (int)(p->fd_part_off[part + 1] - p->fd_part_off[part]);
+    const int rb = column_band_rows(p, false);
+    const int r0 = b * rb, r1 = std::min(p->det.rows, (b + 1) * rb);
+    const int64_t v0 = p->fd_part_view[part], v1 = p->fd_part_view[part + 1];
+    if (r1 <= r0 || v1 <= v0) return cudaSuccess;
+    const size_t pitch = sizeof(float) * (size_t)p->det.per_view;
+    cudaError_t e = cudaMemset2DAsync(sino + v0 * p->det.per_view + (int64_t)r0 * p->det.cols, pitch, 0,
+                                      sizeof(float) * (size_t)(r1 - r0) * p->det.cols, (size_t)(v1 - v0), s);
+    if (e != cudaSuccess) return e;
+    L.band0 = b;
+    return launch_fd(p, fd, sino, L, L.n_items, s);
+}
+
 cudaError_t launch_forward_column_bands(const xrt_plan_s* p, const float* vol_zfast, float* sino, int b0,
                                         int b1, cudaStream_t s) {
     int nblk = 0;
@@ -1789,6 +1814,18 @@ cudaError_t launch_adjoint_column_bands(const xrt_plan_s* p, const float* sino, 
     ColumnLaunch L = make_launch(p, 0, p->n_views, nblk, true);
     L.band0 = b0;
     return launch_column<true>(p, nullptr, vol_zfast, sino, nullptr, 0, L, L.n_items * (b1 - b0), s);
+}
+
+// band b of the adjoint, views [adj_part_view[part], adj_part_view[part + 1]) only (tiled plans)
+cudaError_t launch_adjoint_column_band_part(const xrt_plan_s* p, const float* sino, float* vol_zfast, int b,
+                                            int part, cudaStream_t s) {
+    if (!p->d_adj_part_items || part < 0 || part >= xrt_plan_s::kFwdParts) return cudaErrorInvalidValue;
+    int nblk = 0;
+    ColumnLaunch L = make_launch(p, 0, p->n_views, nblk, true);
+    L.items = (const uint2*)p->d_adj_part_items + p->adj_part_off[part];
+    L.n_items = (int)(p->adj_part_off[part + 1] - p->adj_part_off[part]);
+    L.band0 = b;
+    return launch_column<true>(p, nullptr, vol_zfast, sino, nullptr, 0, L, L.n_items, s);
 }
 
 cudaError_t launch_adjoint_column(const xrt_plan_s* p, const float* sino, float* vol_zfast,

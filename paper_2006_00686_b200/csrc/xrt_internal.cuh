@@ -234,6 +234,18 @@ struct xrt_plan_s {
         void* d_items = nullptr;       // device uint2 work list (tiled) or nullptr (one tile)
         int64_t n_items = 0;
     } ct[2], ct_fd;                    // ct_fd: the (f, delta f) forward's items (view blocks x column groups)
+    // ct_fd's items regrouped into kFwdParts contiguous view ranges (each part still sorted by tile):
+    // the host pipeline launches the last band part by part, so a part's sinogram rows travel to the
+    // host while the next part computes
+    static constexpr int kFwdParts = 4;
+    void* d_fd_part_items = nullptr;
+    int64_t fd_part_off[kFwdParts + 1] = {0, 0, 0, 0, 0};
+    int64_t fd_part_view[kFwdParts + 1] = {0, 0, 0, 0, 0};   // first view of each part (+ end)
+    // the same for the adjoint's items (ct[1]): the host pipeline uploads and runs its FIRST band
+    // part by part, so only the first part's upload is exposed
+    void* d_adj_part_items = nullptr;
+    int64_t adj_part_off[kFwdParts + 1] = {0, 0, 0, 0, 0};
+    int64_t adj_part_view[kFwdParts + 1] = {0, 0, 0, 0, 0};
     int col_np = 2;                    // ray pairs per lane of the forward column kernel (rows per band = 64 col_np)
     int col_np_adj = 1;                // ... of the adjoint column kernel (measured: 1 pair is faster, cfg 3 / 4)
     // attenuated operators on the column path (allocated on first use)
@@ -331,6 +343,11 @@ cudaError_t launch_to_fd(const xrt_plan_s* p, const float* img, float2* fd, cuda
 cudaError_t launch_to_fd_rows(const xrt_plan_s* p, const float* img, float2* fd, int ka, int kb, cudaStream_t s);
 cudaError_t launch_forward_fd_bands(const xrt_plan_s* p, const float2* fd, float* sino, int b0, int b1,
                                     cudaStream_t s);
+int fd_view_block();                 // views per CTA of the fd forward (kFdViews)
+cudaError_t launch_adjoint_column_band_part(const xrt_plan_s* p, const float* sino, float* vol_zfast, int b,
+                                            int part, cudaStream_t s);
+cudaError_t launch_forward_fd_band_part(const xrt_plan_s* p, const float2* fd, float* sino, int b, int part,
+                                        cudaStream_t s);
 cudaError_t launch_adjoint_column_bands(const xrt_plan_s* p, const float* sino, float* vol_zfast, int b0,
                                         int b1, cudaStream_t s);
 }  // namespace xrt
