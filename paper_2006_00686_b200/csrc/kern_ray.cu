@@ -20,6 +20,8 @@
 // the half-open cell floor(u0_a) (ties to the bigger index).
 #include <cuda_runtime.h>
 
+#include <cstdlib>
+
 #include "xrt_internal.cuh"
 
 namespace xrt {
@@ -114,6 +116,44 @@ __global__ void __launch_bounds__(XRT_RAY_BS, XRT_RAY_MINB) k_forward_ray(const 
             acc = fmaf(__ldg(img + S.idx), tn - tc, acc);  // f_I * (C_up - C_low)
             tc = tn;
             advance(S, tn);
+        }
+    }
+    sino[m] = acc;
+}
+
+// 2D beams: the same merged walk with two moving axes at most and a branch-free advance (the axis
+// whose crossing defined tn steps; on a tie x first, y on the next trip after a zero-length unit --
+// the generic walk's order), 32-bit cell index.  cfg 2 0.438 -> 0.412 ms (loading the next unit
+// one trip ahead: 0.445; 64 / 256-thread blocks: 0.409 / 0.439, cfg 1 slower at 64).
+__global__ void __launch_bounds__(XRT_RAY_BS, XRT_RAY_MINB) k_forward_ray2d(const ViewRec* __restrict__ views, DetC dc,
+                                                        GridC g, const float* __restrict__ img,
+                                                        float* __restrict__ sino, int64_t ray0,
+                                                        int64_t ray1) {
+    const int64_t m = ray0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (m >= ray1) return;
+    int v, r, c;
+    ray_of(m, dc, v, r, c);
+    Ray64 R;
+    float acc = 0.f;
+    if (setup_ray(views[v], dc, g, r, c, R)) {
+        Ray32 S;
+        to_ray32(R, g, S);
+        float tx = S.T[0], ty = S.T[1], mx = 0.f, my = 0.f;
+        const float t1x = S.t1[0], t1y = S.t1[1], dtx = S.dt[0], dty = S.dt[1], tend = S.tend;
+        const int sx = S.step[0], sy = S.step[1];
+        int idx = (int)S.idx;
+        float tc = 0.f;
+#pragma unroll 2
+        for (int it = 0; tc < tend && it < S.budget; ++it) {
+            const float tn = fminf(fminf(tx, ty), tend);
+            acc = fmaf(__ldg(img + idx), tn - tc, acc);   // f_I * (C_up - C_low)
+            tc = tn;
+            const bool bx = tn == tx, by = !bx && tn == ty;
+            mx = bx ? mx + 1.f : mx;
+            my = by ? my + 1.f : my;
+            tx = fmaf(mx, dtx, t1x);
+            ty = fmaf(my, dty, t1y);
+            idx += bx ? sx : (by ? sy : 0);
         }
     }
     sino[m] = acc;
@@ -434,8 +474,13 @@ inline unsigned blocks_for(int64_t n, int bs) { return (unsigned)((n + bs - 1) /
 cudaError_t launch_forward_ray(const xrt_plan_s* p, const float* img, float* sino, int64_t ray0,
                                int64_t ray1, cudaStream_t s) {
     if (ray1 <= ray0) return cudaSuccess;
-    k_forward_ray<<<blocks_for(ray1 - ray0, XRT_RAY_BS), XRT_RAY_BS, 0, s>>>(p->d_views, p->det, p->grid, img,
-                                                               sino, ray0, ray1);
+    static const bool generic = std::getenv("XRT_RAY_GENERIC") != nullptr;
+    if (p->dim == 2 && !generic)
+        k_forward_ray2d<<<blocks_for(ray1 - ray0, XRT_RAY_BS), XRT_RAY_BS, 0, s>>>(p->d_views, p->det, p->grid, img,
+                                                                     sino, ray0, ray1);
+    else
+        k_forward_ray<<<blocks_for(ray1 - ray0, XRT_RAY_BS), XRT_RAY_BS, 0, s>>>(p->d_views, p->det, p->grid, img,
+                                                                   sino, ray0, ray1);
     return cudaGetLastError();
 }
 
