@@ -53,9 +53,19 @@ __global__ void k_red(float* buf, const int* pages_die0, int n0, const int* page
     for (int it = 0; it < iters; ++it) {
         h = h * 1664525u + 1013904223u;
         int pg;
-        if (mode == 1) pg = mine[(h >> 8) % nm];
+        if (mode == 1 || mode >= 3) pg = mine[(h >> 8) % nm];
         else if (mode == 2) pg = other[(h >> 8) % no];
         else pg = ((h >> 8) & 1) ? pages_die0[(h >> 9) % n0] : pages_die1[(h >> 9) % n1];
+        if (mode >= 3) {   // scattered: every lane its own page (32 sectors per instruction)
+            const unsigned hl = (h ^ (lane * 0x9E3779B9u)) * 2246822519u;
+            const int m = mode - 3;
+            int pl;
+            if (m == 1) pl = mine[(hl >> 8) % nm];
+            else if (m == 2) pl = other[(hl >> 8) % no];
+            else pl = ((hl >> 8) & 1) ? pages_die0[(hl >> 9) % n0] : pages_die1[(hl >> 9) % n1];
+            asm volatile("red.global.add.f32 [%0], %1;" :: "l"(buf + (size_t)pl * 1024 + ((hl >> 22) & 1016u)), "f"(1.0f) : "memory");
+            continue;
+        }
         const unsigned off = ((h >> 20) & 960u) + (lane * 2u) / 3u;   // 21-22 consecutive floats in the page
         asm volatile("red.global.add.f32 [%0], %1;" :: "l"(buf + (size_t)pg * 1024 + off), "f"(1.0f) : "memory");
     }
@@ -102,9 +112,9 @@ int main() {
     cudaEventCreate(&e0);
     cudaEventCreate(&e1);
     const int blocks = 148 * 8, threads = 256, iters = 4096;
-    const char* names[3] = {"any_die", "own_die", "other_die"};
+    const char* names[6] = {"any_die", "own_die", "other_die", "scattered_any", "scattered_own", "scattered_other"};
     printf("{\"pages_near_sm0\": %zu, \"pages_far_sm0\": %zu, \"sms_on_die0\": %d", p0.size(), p1.size(), n_die0);
-    for (int mode = 0; mode < 3; ++mode) {
+    for (int mode = 0; mode < 6; ++mode) {
         k_red<<<blocks, threads>>>((float*)buf, d0, (int)p0.size(), d1, (int)p1.size(), d_smdie, 64, mode);
         cudaEventRecord(e0);
         for (int r = 0; r < 3; ++r)
@@ -115,7 +125,7 @@ int main() {
         cudaEventElapsedTime(&ms, e0, e1);
         const double insts = 3.0 * blocks * threads / 32.0 * iters;
         printf(", \"%s\": {\"ms\": %.3f, \"warp_reds_per_s\": %.4g, \"sectors_per_s\": %.4g}", names[mode], ms,
-               insts / (ms / 1e3), 3.0 * insts / (ms / 1e3));
+               insts / (ms / 1e3), (mode >= 3 ? 32.0 : 3.0) * insts / (ms / 1e3));
     }
     printf(", \"error\": \"%s\"}\n", cudaGetErrorString(cudaGetLastError()));
     return 0;
