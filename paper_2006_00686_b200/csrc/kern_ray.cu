@@ -474,7 +474,7 @@ inline unsigned blocks_for(int64_t n, int bs) { return (unsigned)((n + bs - 1) /
 cudaError_t launch_forward_ray(const xrt_plan_s* p, const float* img, float* sino, int64_t ray0,
                                int64_t ray1, cudaStream_t s) {
     if (ray1 <= ray0) return cudaSuccess;
-    static const bool generic = std::getenv("XRT_RAY_GENERIC") != nullptr;
+    const bool generic = std::getenv("XRT_RAY_GENERIC") != nullptr;   // (read per launch: tests toggle it)
     if (p->dim == 2 && !generic)
         k_forward_ray2d<<<blocks_for(ray1 - ray0, XRT_RAY_BS), XRT_RAY_BS, 0, s>>>(p->d_views, p->det, p->grid, img,
                                                                      sino, ray0, ray1);

@@ -421,6 +421,33 @@ def test_forward64_agrees_with_fp32(cuda_ok):
     assert H.fwd_err(a.cpu().numpy().ravel(), b.cpu().numpy().ravel()) <= H.FWD_TOL
 
 
+# ------------------------------------------- specialised kernels vs the general ones they replace
+@pytest.mark.parametrize("idx", [1, 2])
+def test_ray2d_forward_bitwise_generic(cuda_ok, idx, monkeypatch):
+    """k_forward_ray2d (AUTO forward of the 2D beams) walks the same crossings in the same order with
+    the same fp32 operations as the generic RAY walk: bitwise equal, full size."""
+    c = workloads.config(idx)
+    p = Plan(c, device=0)
+    img = _image(c)
+    a = p.forward(img)
+    monkeypatch.setenv("XRT_RAY_GENERIC", "1")
+    b = p.forward(img)
+    assert torch.equal(a, b)
+
+
+@pytest.mark.parametrize("full", [False, True])
+def test_flat_kernel_bitwise_general(cuda_ok, full, monkeypatch):
+    """The flat-only forward instantiation (3D parallel beam without tilt) equals the general column
+    kernel's flat walk bitwise (same walk, fewer registers)."""
+    c = workloads.config(3) if full else H.small_config(3)
+    p = Plan(c, device=0)
+    img = _image(c)
+    a = p.forward(img)
+    monkeypatch.setenv("XRT_NO_FLAT_KERNEL", "1")
+    b = p.forward(img)
+    assert torch.equal(a, b)
+
+
 # ------------------------------------------- fp32 lengths / fp64 accumulation (SURVEY 8(f) N2)
 @pytest.mark.parametrize("idx", [1, 2, 3, 4, 5])
 def test_forward_mixed_small_every_ray(cuda_ok, idx):
