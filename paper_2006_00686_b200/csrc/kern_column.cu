@@ -43,6 +43,7 @@
 #include <algorithm>
 #include <climits>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <vector>
 
@@ -464,9 +465,32 @@ __device__ __forceinline__ void z_skip(float& kpf, int dk, float& mzv, float& nt
     ntzv = -fmaf(mzv, dtz, t0z);
 }
 
+// Debug build (-DXRT_DEBUG_BOUNDS=1, tests only): every walk load / reduction address is checked
+// against the buffer the launch walks (set per launch, stream-ordered); a miss prints and traps.
+#ifndef XRT_DEBUG_BOUNDS
+#define XRT_DEBUG_BOUNDS 0
+#endif
+#if XRT_DEBUG_BOUNDS
+__device__ unsigned long long g_dbg_range[2];
+#endif
+__device__ __forceinline__ void dbg_chk(const void* a, int bytes) {
+#if XRT_DEBUG_BOUNDS
+    const unsigned long long x = (unsigned long long)a;
+    if (x < g_dbg_range[0] || x + (unsigned long long)bytes > g_dbg_range[1]) {
+        printf("xrt debug: address %llx outside [%llx, %llx) block %d thread %d\n", x, g_dbg_range[0],
+               g_dbg_range[1], (int)blockIdx.x, (int)threadIdx.x);
+        __trap();
+    }
+#else
+    (void)a; (void)bytes;
+#endif
+}
+__device__ __forceinline__ float ldg_chk(const float* a) { dbg_chk(a, 4); return __ldg(a); }
+
 // red.global.add.f32 on an address built by integer arithmetic (a plain atomicAdd on such a generic
 // pointer compiles to a generic ATOM with a shared-window check and CAS fallback)
 __device__ __forceinline__ void red_add(float* a, float v, unsigned long long pol) {
+    dbg_chk(a, 4);
     asm volatile("red.global.add.L2::cache_hint.f32 [%0], %1, %2;" :: "l"(a), "f"(v), "l"(pol) : "memory");
 }
 
@@ -576,8 +600,8 @@ __device__ __forceinline__ void column_segments_fwd(unsigned seg, int total, Ray
         const float* a0 = col_addr(seg_ptr(raw), P[p].kpf.x);
         const float* a1 = col_addr(seg_ptr(raw), P[p].kpf.y);
         const int o0 = DK != 0 ? DK : P[p].dk0, o1 = DK != 0 ? DK : P[p].dk1;
-        f0[p] = make_float2(__ldg(a0), __ldg(a1));
-        f1[p] = make_float2(__ldg(a0 + o0), __ldg(a1 + o1));
+        f0[p] = make_float2(ldg_chk(a0), ldg_chk(a1));
+        f1[p] = make_float2(ldg_chk(a0 + o0), ldg_chk(a1 + o1));
     }
 #pragma unroll kFwdUnroll
     for (int s = 0; s < total; ++s) {
@@ -592,8 +616,8 @@ __device__ __forceinline__ void column_segments_fwd(unsigned seg, int total, Ray
             const float* a0 = col_addr(seg_ptr(nraw), P[p].kpf.x);
             const float* a1 = col_addr(seg_ptr(nraw), P[p].kpf.y);
             const int o0 = DK != 0 ? DK : P[p].dk0, o1 = DK != 0 ? DK : P[p].dk1;
-            const float2 g0 = make_float2(__ldg(a0), __ldg(a1));
-            const float2 g1 = make_float2(__ldg(a0 + o0), __ldg(a1 + o1));
+            const float2 g0 = make_float2(ldg_chk(a0), ldg_chk(a1));
+            const float2 g1 = make_float2(ldg_chk(a0 + o0), ldg_chk(a1 + o1));
             // this segment's arithmetic
             P[p].acc0 = __ffma2_rn(f0[p], ds2, P[p].acc0);        // f_s * d_sigma
             const float2 d = __ffma2_rn(f0[p], m1, f1[p]);        // f_e - f_s
@@ -618,7 +642,7 @@ __device__ __forceinline__ void column_segments_fwd_flat(unsigned seg, int total
         for (int p = 0; p < NP; ++p) {
             const float* a0 = col_addr(seg_ptr(raw), P[p].kpf.x);
             const float* a1 = col_addr(seg_ptr(raw), P[p].kpf.y);
-            P[p].acc0 = __ffma2_rn(make_float2(__ldg(a0), __ldg(a1)), ds2, P[p].acc0);
+            P[p].acc0 = __ffma2_rn(make_float2(ldg_chk(a0), ldg_chk(a1)), ds2, P[p].acc0);
         }
     }
 }
@@ -1160,6 +1184,7 @@ __device__ __forceinline__ unsigned long long fd_addr(unsigned long long ptr, fl
 }
 
 __device__ __forceinline__ float2 ldg_f2(unsigned long long a) {
+    dbg_chk((const void*)a, 8);
     float2 v;
     asm("ld.global.nc.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "l"(a));
     return v;
@@ -1657,6 +1682,16 @@ ColumnLaunch make_launch(const xrt_plan_s* p, int64_t v0, int64_t v1, int& nblk,
     return L;
 }
 
+static cudaError_t set_dbg_range(const void* lo, size_t bytes, cudaStream_t s) {
+#if XRT_DEBUG_BOUNDS
+    const unsigned long long r[2] = {(unsigned long long)lo, lo ? (unsigned long long)lo + bytes : ~0ull};
+    return cudaMemcpyToSymbolAsync(g_dbg_range, r, sizeof(r), 0, cudaMemcpyHostToDevice, s);
+#else
+    (void)lo; (void)bytes; (void)s;
+    return cudaSuccess;
+#endif
+}
+
 template <int kOp>
 cudaError_t launch_column_op(const xrt_plan_s* p, const float* vol, float* volw, const float* sino_in,
                              float* sino_out, int64_t v0, const ColumnLaunch& L, int nblk, cudaStream_t s,
@@ -1666,6 +1701,12 @@ cudaError_t launch_column_op(const xrt_plan_s* p, const float* vol, float* volw,
     const ColDesc* d = (const ColDesc*)p->d_coldesc;
     if (nblk <= 0) return cudaSuccess;
     const int np = np_override ? np_override : (kAdj ? p->col_np_adj : p->col_np);
+    {
+        const size_t vb = 4ull * (size_t)p->grid.nxy * (size_t)p->nzp;   // z-fastest float volume
+        const cudaError_t e = kOp == 0 ? set_dbg_range(vol, vb, s) : kOp == 1 ? set_dbg_range(volw, vb, s)
+                                                                        : set_dbg_range(nullptr, 0, s);
+        if (e != cudaSuccess) return e;
+    }
     // every ray keeps its z cell: the flat-only forward (cfg 3 1.99 -> 1.88 ms; the flat-only adjoint
     // measured 2.14 -> 2.17 ms, not used)
     if (kOp == 0 && p->flat_z && !std::getenv("XRT_NO_FLAT_KERNEL")) {
@@ -1732,6 +1773,7 @@ cudaError_t launch_to_fd(const xrt_plan_s* p, const float* img, float2* fd, cuda
 static cudaError_t launch_fd(const xrt_plan_s* p, const float2* fd, float* sino, const ColumnLaunch& L, int nblk,
                              cudaStream_t s) {
     if (nblk <= 0) return cudaSuccess;
+    if (cudaError_t e = set_dbg_range(fd, 16ull * (size_t)p->grid.nxy * (size_t)p->nzp, s); e != cudaSuccess) return e;
     const ColDesc* d = (const ColDesc*)p->d_coldesc;
     if (p->col_np == 1)
         k_fwd_fd<1><<<nblk, kFdWarps * 32, 0, s>>>(p->d_views, p->det, p->grid, fd, sino, 0, d, L);
