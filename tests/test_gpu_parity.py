@@ -385,6 +385,23 @@ def test_full_sinogram_unit_counts_vs_cpu_method(cuda_ok, idx, view_stride):
     assert total > 0
 
 
+@pytest.mark.parametrize("n_views", [1, 3, 5])
+def test_host_pipeline_view_parts(cuda_ok, n_views, monkeypatch):
+    """Tiled host pipelines with fewer views than the four view parts (1, 3: parts not built) and with
+    uneven parts (5): host results equal the device path."""
+    monkeypatch.setenv("XRT_COLUMN_TILE", "16")
+    c = workloads.scaled(4, n_views=n_views, n=(48, 48, 48), det_cols=97, det_rows=71)
+    p = Plan(c, device=0)
+    img = _image(c)
+    dev = p.forward(img)
+    host = p.forward_host(img.cpu().contiguous())
+    assert H.fwd_err(host.numpy().ravel(), dev.cpu().numpy().ravel()) <= 1e-6
+    y = workloads.make_sino_input(c)
+    a_dev = p.adjoint(y.cuda())
+    a_host = p.adjoint_host(y.contiguous())
+    assert H.rel_l2(a_host.numpy(), a_dev.cpu().numpy()) < 1e-6
+
+
 # ------------------------------------------------------------------- fp64 variant (SURVEY 8(f) N2)
 F64_TOL = 1e-11   # fp64 lengths and sums vs the fp64 brute-force oracle: rounding order only
 
