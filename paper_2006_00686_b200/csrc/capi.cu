@@ -256,6 +256,11 @@ xrt_status alloc_stage(xrt_plan p) {
         XRT_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
         p->aux_stream2 = s;
     }
+    if (!p->aux_stream3) {
+        cudaStream_t s;
+        XRT_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+        p->aux_stream3 = s;
+    }
     return XRT_OK;
 }
 
@@ -743,6 +748,7 @@ xrt_status xrt_plan_destroy(xrt_plan p) {
     cudaFree(p->d_stage_sino);
     if (p->aux_stream) cudaStreamDestroy((cudaStream_t)p->aux_stream);
     if (p->aux_stream2) cudaStreamDestroy((cudaStream_t)p->aux_stream2);
+    if (p->aux_stream3) cudaStreamDestroy((cudaStream_t)p->aux_stream3);
     delete p;
     return XRT_OK;
 }
@@ -973,10 +979,31 @@ xrt_status xrt_forward_host(xrt_plan p, const float* img_host, float* sino_host,
         const int CH = std::max(32, (nz + 15) / 16);
         const int nch = (nz + CH - 1) / CH;
         cudaStream_t d = (cudaStream_t)p->aux_stream2;
+        // bands alternate between two compute streams (disjoint sinogram rows), so one band's
+        // last CTAs overlap the next band's first ones; both start after the caller's prior work
+        // on s, as does the upload stream
+        cudaStream_t cs[2] = {s, (cudaStream_t)p->aux_stream3};
         std::vector<cudaEvent_t> evc((size_t)nch), evb((size_t)nb), evp((size_t)xrt_plan_s::kFwdParts);
         for (auto& x : evc) XRT_CUDA(cudaEventCreateWithFlags(&x, cudaEventDisableTiming));
         for (auto& x : evb) XRT_CUDA(cudaEventCreateWithFlags(&x, cudaEventDisableTiming));
         for (auto& x : evp) XRT_CUDA(cudaEventCreateWithFlags(&x, cudaEventDisableTiming));
+        cudaEvent_t ev0, ev_end;
+        XRT_CUDA(cudaEventCreateWithFlags(&ev0, cudaEventDisableTiming));
+        XRT_CUDA(cudaEventCreateWithFlags(&ev_end, cudaEventDisableTiming));
+        XRT_CUDA(cudaEventRecord(ev0, s));
+        XRT_CUDA(cudaStreamWaitEvent(a, ev0, 0));
+        XRT_CUDA(cudaStreamWaitEvent(cs[1], ev0, 0));
+        // XRT_HOST_TRACE=1: per-phase device times on stderr (diagnostic)
+        const bool trace = std::getenv("XRT_HOST_TRACE") != nullptr;
+        std::vector<cudaEvent_t> tev;
+        auto tmark = [&](cudaStream_t st) {
+            if (!trace) return;
+            cudaEvent_t x;
+            cudaEventCreate(&x);
+            cudaEventRecord(x, st);
+            tev.push_back(x);
+        };
+        tmark(s);
         // chunk i covers image rows [lo_i, hi_i) in send order; built fd rows after chunk i:
         // desc: [lo_i + 1 .. nz] (row lo_i waits for its lower neighbour), asc: [-1 .. hi_i - 1)
         cudaError_t e = cudaSuccess;
@@ -1008,16 +1035,17 @@ xrt_status xrt_forward_host(xrt_plan p, const float* img_host, float* sino_host,
             int need = nch - 1;
             for (int i = 0; i < nch; ++i)
                 if (done_lo[i] <= std::max(k0, -1) && done_hi[i] >= std::min(k1, nz + 1)) { need = i; break; }
-            e = cudaStreamWaitEvent(s, evc[need], 0);
             const int r0 = b * rb, r1 = std::min(p->det.rows, r0 + rb);
             if (b == nb - 1 && p->d_fd_part_items) {
                 // the last band part by part (view ranges): each part's rows go down while the next
                 // part computes, so only the last part's copy is exposed
                 for (int q = 0; q < xrt_plan_s::kFwdParts && e == cudaSuccess; ++q) {
                     const int64_t v0 = p->fd_part_view[q], v1 = p->fd_part_view[q + 1];
-                    e = xrt::launch_forward_fd_band_part(p, p->d_work_fd, p->d_stage_sino, b, q, s);
+                    cudaStream_t c = cs[(b + q) & 1];
+                    e = cudaStreamWaitEvent(c, evc[need], 0);
+                    if (e == cudaSuccess) e = xrt::launch_forward_fd_band_part(p, p->d_work_fd, p->d_stage_sino, b, q, c);
                     p->launches += 1;
-                    if (e == cudaSuccess) e = cudaEventRecord(evp[q], s);
+                    if (e == cudaSuccess) e = cudaEventRecord(evp[q], c);
                     if (e == cudaSuccess) e = cudaStreamWaitEvent(d, evp[q], 0);
                     if (e == cudaSuccess && v1 > v0)
                         e = cudaMemcpy2DAsync(sino_host + v0 * p->det.per_view + (int64_t)r0 * p->det.cols, pitch,
@@ -1027,9 +1055,13 @@ xrt_status xrt_forward_host(xrt_plan p, const float* img_host, float* sino_host,
                 }
                 continue;
             }
-            if (e == cudaSuccess) e = xrt::launch_forward_fd_bands(p, p->d_work_fd, p->d_stage_sino, b, b + 1, s);
+            cudaStream_t c = cs[b & 1];
+            e = cudaStreamWaitEvent(c, evc[need], 0);
+            tmark(c);
+            if (e == cudaSuccess) e = xrt::launch_forward_fd_bands(p, p->d_work_fd, p->d_stage_sino, b, b + 1, c);
+            tmark(c);
             p->launches += 1;
-            if (e == cudaSuccess) e = cudaEventRecord(evb[b], s);
+            if (e == cudaSuccess) e = cudaEventRecord(evb[b], c);
             if (e == cudaSuccess) e = cudaStreamWaitEvent(d, evb[b], 0);
             if (e == cudaSuccess)
                 e = cudaMemcpy2DAsync(sino_host + (int64_t)r0 * p->det.cols, pitch,
@@ -1037,13 +1069,31 @@ xrt_status xrt_forward_host(xrt_plan p, const float* img_host, float* sino_host,
                                       sizeof(float) * (size_t)(r1 - r0) * p->det.cols, (size_t)p->n_views,
                                       cudaMemcpyDeviceToHost, d);
         }
+        tmark(a);
+        tmark(d);
         if (e == cudaSuccess) e = cudaStreamWaitEvent(s, evc[nch - 1], 0);   // the stage buffers are reused
+        if (e == cudaSuccess) e = cudaEventRecord(ev_end, cs[1]);
+        if (e == cudaSuccess) e = cudaStreamWaitEvent(s, ev_end, 0);
         cudaError_t e1 = cudaStreamSynchronize(a);
         cudaError_t e2 = cudaStreamSynchronize(s);
         cudaError_t e3 = cudaStreamSynchronize(d);
+        cudaError_t e4 = cudaStreamSynchronize(cs[1]);
+        if (e3 == cudaSuccess) e3 = e4;
         for (auto& x : evc) cudaEventDestroy(x);
         for (auto& x : evb) cudaEventDestroy(x);
         for (auto& x : evp) cudaEventDestroy(x);
+        cudaEventDestroy(ev0);
+        cudaEventDestroy(ev_end);
+        if (trace && !tev.empty()) {
+            std::fprintf(stderr, "xrt forward_host trace (ms from start):");
+            for (size_t i = 1; i < tev.size(); ++i) {
+                float ms = 0.f;
+                cudaEventElapsedTime(&ms, tev[0], tev[i]);
+                std::fprintf(stderr, " %.2f", ms);
+            }
+            std::fprintf(stderr, "\n");
+        }
+        for (auto& x : tev) cudaEventDestroy(x);
         if (e != cudaSuccess) return cuda_fail(e, "forward_host chunked pipeline");
         if (e1 != cudaSuccess) return cuda_fail(e1, "forward_host sync");
         if (e2 != cudaSuccess) return cuda_fail(e2, "forward_host sync");

@@ -265,6 +265,7 @@ struct xrt_plan_s {
     float* d_stage_sino = nullptr;
     void* aux_stream = nullptr;
     void* aux_stream2 = nullptr;       // host pipelines: downloads of final image rows (staged adjoint)
+    void* aux_stream3 = nullptr;       // forward host pipeline: every other band's kernels (band tails overlap)
     int algo_fwd = XRT_ALGO_AUTO;
     int algo_adj = XRT_ALGO_AUTO;
     bool column_ok = false;            // geometry admits the column-shared kernels
