@@ -1193,10 +1193,21 @@ __device__ __forceinline__ unsigned long long fd_addr(unsigned long long ptr, fl
 #endif
 }
 
+#ifndef XRT_FD_LDHINT
+#define XRT_FD_LDHINT 1   // walk-load cache hint: 1 L1::evict_last (cfg 4 115.8 -> 115.5 ms), 2 L2::256B (115.9), 3 L1::evict_first (172.4: the L1 reuse between the CTA warps matters), 0 none
+#endif
 __device__ __forceinline__ float2 ldg_f2(unsigned long long a) {
     dbg_chk((const void*)a, 8);
     float2 v;
+#if XRT_FD_LDHINT == 1
+    asm("ld.global.nc.L1::evict_last.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "l"(a));
+#elif XRT_FD_LDHINT == 2
+    asm("ld.global.nc.L2::256B.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "l"(a));
+#elif XRT_FD_LDHINT == 3
+    asm("ld.global.nc.L1::evict_first.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "l"(a));
+#else
     asm("ld.global.nc.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "l"(a));
+#endif
     return v;
 }
 
