@@ -1196,6 +1196,21 @@ __device__ __forceinline__ unsigned long long fd_addr(unsigned long long ptr, fl
 #ifndef XRT_FD_LDHINT
 #define XRT_FD_LDHINT 1   // walk-load cache hint: 1 L1::evict_last (cfg 4 115.8 -> 115.5 ms), 2 L2::256B (115.9), 3 L1::evict_first (172.4: the L1 reuse between the CTA warps matters), 0 none
 #endif
+// the crossing flag [le > 0] as 1.0 / 0.0: FSET (ALU pipe) or le * 2^127 saturated (FMA pipe; exact:
+// with FTZ any positive le >= 2^-126 maps to >= 2 -> 1, le <= 0 -> 0) -- XRT_FD_CR_SAT
+#ifndef XRT_FD_CR_SAT
+#define XRT_FD_CR_SAT 1   // cfg 4 115.4 -> 114.7 ms (ALU 46 % vs FMA-heavy 38 % busy)
+#endif
+__device__ __forceinline__ float fd_cr(float le) {
+#if XRT_FD_CR_SAT
+    float r;
+    asm("mul.ftz.sat.f32 %0, %1, 0f7F000000;" : "=f"(r) : "f"(le));
+    return r;
+#else
+    return gt0(le);
+#endif
+}
+
 __device__ __forceinline__ float2 ldg_f2(unsigned long long a) {
     dbg_chk((const void*)a, 8);
     float2 v;
@@ -1237,7 +1252,7 @@ __device__ __forceinline__ void fd_segments(unsigned seg, int total, FdPair (&P)
 #pragma unroll
         for (int p = 0; p < NP; ++p) {
             const float2 le = __fadd2_rn(se2, P[p].ntz);                 // sigma_e - tau
-            const float2 cr = make_float2(gt0(le.x), gt0(le.y));
+            const float2 cr = make_float2(fd_cr(le.x), fd_cr(le.y));
             const float2 lm = __fmul2_rn(le, cr);                        // l_e = max(sigma_e - tau, 0)
             const float lma = lm.x, lmb = lm.y;
             P[p].kpf = __ffma2_rn(cr, P[p].dkf, P[p].kpf);
