@@ -125,7 +125,10 @@ __global__ void __launch_bounds__(XRT_RAY_BS, XRT_RAY_MINB) k_forward_ray(const 
 // whose crossing defined tn steps; on a tie x first, y on the next trip after a zero-length unit --
 // the generic walk's order), 32-bit cell index.  cfg 2 0.438 -> 0.412 ms (loading the next unit
 // one trip ahead: 0.445; 64 / 256-thread blocks: 0.409 / 0.439, cfg 1 slower at 64).
-__global__ void __launch_bounds__(XRT_RAY_BS, XRT_RAY_MINB) k_forward_ray2d(const ViewRec* __restrict__ views, DetC dc,
+#ifndef XRT_RAY2D_MINB
+#define XRT_RAY2D_MINB 16   // 2048 threads per SM (32 registers): cfg 2 0.412 -> 0.389 ms
+#endif
+__global__ void __launch_bounds__(XRT_RAY_BS, XRT_RAY2D_MINB) k_forward_ray2d(const ViewRec* __restrict__ views, DetC dc,
                                                         GridC g, const float* __restrict__ img,
                                                         float* __restrict__ sino, int64_t ray0,
                                                         int64_t ray1) {
