@@ -278,6 +278,13 @@ int resolve(const xrt_plan_s* p, int op) {
 // Forward over views [v0, v1).  COLUMN reads the plan's z-fastest copy of the image, which
 // fwd_prepare() builds once per call (img -> work_fwd transpose).
 xrt_status fwd_prepare(xrt_plan p, const float* img, cudaStream_t s) {
+    if (resolve(p, XRT_OP_FORWARD) == XRT_ALGO_RAY && p->dim == 2 && p->d_fwd_t) {
+        // 2D RAY forward in pieces: x-major rays walk the transposed image
+        cudaError_t e = xrt::launch_transpose2d(img, p->d_fwd_t, p->grid.n[1], p->grid.n[0], false, s);
+        p->launches += 1;
+        if (e != cudaSuccess) return cuda_fail(e, "transpose launch");
+        return XRT_OK;
+    }
     if (resolve(p, XRT_OP_FORWARD) != XRT_ALGO_COLUMN) return XRT_OK;
     if (p->dim == 2) {   // slice kernels: x-major warps read the transposed image
         cudaError_t e = xrt::launch_transpose2d(img, p->d_img_t, p->grid.n[1], p->grid.n[0], false, s);
@@ -492,6 +499,17 @@ xrt_status plan_create_impl(const xrt_geometry* g, int cuda_device, xrt_plan* ou
         if (e != cudaSuccess) {
             xrt_plan_destroy(p);
             return cuda_fail(e, "2D ray descriptors");
+        }
+    }
+    if (p->dim == 2 && (int64_t)p->n_rays < (1ll << 26)) {
+        // 2D RAY forward in pieces: per-ray fp32 walk state (32 B per ray; cfg 2: 17.7 MB)
+        e = cudaMalloc(&p->d_ray2d_walk, xrt::ray2d_walk_bytes() * (size_t)p->n_rays);
+        if (e == cudaSuccess) e = cudaMalloc(&p->d_fwd_t, sizeof(float) * (size_t)G.nxy);
+        if (e == cudaSuccess) e = xrt::launch_ray2d_walk_desc(p, (cudaStream_t)0);
+        if (e == cudaSuccess) e = cudaDeviceSynchronize();
+        if (e != cudaSuccess) {
+            xrt_plan_destroy(p);
+            return cuda_fail(e, "2D walk descriptors");
         }
     }
     p->column_ok = !rays && (g->beam == XRT_PAR3D || g->beam == XRT_CONE || g->beam == XRT_HELICAL) &&
@@ -743,6 +761,8 @@ xrt_status xrt_plan_destroy(xrt_plan p) {
     cudaFree(p->d_gather_y);
     cudaFree(p->d_rays);
     cudaFree(p->d_raydesc2d);
+    cudaFree(p->d_ray2d_walk);
+    cudaFree(p->d_fwd_t);
     cudaFree(p->d_img_t);
     cudaFree(p->d_stage_img);
     cudaFree(p->d_stage_sino);

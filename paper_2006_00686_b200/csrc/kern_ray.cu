@@ -162,6 +162,133 @@ __global__ void __launch_bounds__(XRT_RAY_BS, XRT_RAY2D_MINB) k_forward_ray2d(co
     sino[m] = acc;
 }
 
+// 2D beams, pieces: the same walk split into K pieces per ray along the major axis (the axis with
+// the most crossings), one thread per piece, the K partial sums combined in shared memory in a fixed
+// order.  Piece p covers major slices [p S, (p + 1) S) (S = ceil(slices / K); slice n spans
+// [T_a(n - 1), T_a(n)], T_a(-1) = 0, T_a(n_a) = tend) and starts in the state the sequential walk has
+// after taking major crossing p S - 1: the minor crossings T_b(m) < t_s taken (a minor crossing AT
+// t_s is then taken on the first trip with a zero-length unit, as the sequential walk's tie order
+// may do).  Every crossing value is the same fmaf(m, dt, t1) the sequential walk evaluates, so each
+// unit's C_up - C_low is bit-identical to k_forward_ray2d's; only the summation order differs.
+// The per-ray fp32 state (Ray2DW) is built once at plan creation (k_ray2d_walk_desc) from the fp64
+// setup, so a piece costs a 32-byte load instead of the fp64 ray setup.
+struct __align__(16) Ray2DW {
+    float t1a, dta, t1b, dtb;   // major / minor first crossing and spacing (minor fixed: INF, 0)
+    float tend;                 // end of the last unit (0: the ray misses the image)
+    int idx0;                   // flat index of the entry unit (~index into imgT for x-major rays)
+    int sa, sb;                 // signed flat strides of the major / minor axis (in the image walked)
+};
+
+__global__ void k_ray2d_walk_desc(const ViewRec* __restrict__ views, DetC dc, GridC g, int64_t n,
+                                  Ray2DW* __restrict__ out) {
+    const int64_t m = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (m >= n) return;
+    int v, r, c;
+    ray_of(m, dc, v, r, c);
+    Ray2DW d;
+    d.t1a = d.t1b = INFINITY; d.dta = d.dtb = 0.f; d.tend = 0.f; d.idx0 = 0; d.sa = d.sb = 0;
+    Ray64 R;
+    if (setup_ray(views[v], dc, g, r, c, R)) {
+        Ray32 S;
+        to_ray32(R, g, S);
+        // major axis: the moving one with the smaller crossing spacing
+        const int a = (S.step[0] != 0 && (S.step[1] == 0 || S.dt[0] <= S.dt[1])) ? 0 : 1, b = 1 - a;
+        d.t1a = S.t1[a]; d.dta = S.dt[a];
+        d.t1b = S.t1[b]; d.dtb = S.dt[b];
+        d.tend = S.tend;
+        const int cx = (int)(S.idx % g.n[0]), cy = (int)(S.idx / g.n[0]);
+        if (a == 0) {
+            // x-major: walk the transposed copy imgT[i][j] (flat i N_y + j), so the adjacent rays of a
+            // warp, one x slice apart at most, read adjacent addresses; flagged by idx0 < 0
+            d.idx0 = ~(cx * g.n[1] + cy);
+            d.sa = S.step[0] > 0 ? g.n[1] : -g.n[1];
+            d.sb = S.step[1] > 0 ? 1 : (S.step[1] < 0 ? -1 : 0);
+        } else {
+            d.idx0 = (int)S.idx;
+            d.sa = S.step[1];
+            d.sb = S.step[0];
+        }
+    }
+    out[m] = d;
+}
+
+#ifndef XRT_RAY2D_PIECES
+#define XRT_RAY2D_PIECES 4
+#endif
+template <int K>
+__global__ void __launch_bounds__(XRT_RAY_BS, XRT_RAY2D_MINB) k_forward_ray2d_pc(const Ray2DW* __restrict__ dsc,
+                                                                           const float* __restrict__ img,
+                                                                           const float* __restrict__ imgT,
+                                                                           float* __restrict__ sino, int64_t ray0,
+                                                                           int64_t ray1) {
+    // block = K groups of RB = XRT_RAY_BS / K adjacent rays; group p walks piece p of each (a warp's
+    // lanes walk adjacent rays, as in the sequential kernel)
+    constexpr int RB = XRT_RAY_BS / K;
+    __shared__ float part[XRT_RAY_BS];
+    const int p = (int)threadIdx.x / RB, rl = (int)threadIdx.x % RB;
+    const int64_t m = ray0 + (int64_t)blockIdx.x * RB + rl;
+    float acc = 0.f;
+    if (m < ray1) {   // no early exit: the block meets at the barrier below
+        const float4 q0 = __ldg(reinterpret_cast<const float4*>(dsc + m));
+        const int4 q1 = __ldg(reinterpret_cast<const int4*>(dsc + m) + 1);
+        const float t1a = q0.x, dta = q0.y, t1b = q0.z, dtb = q0.w;
+        const float tend = __int_as_float(q1.x);
+        const int sa = q1.z, sb = q1.w;
+        const bool tr = q1.y < 0;                       // x-major: the transposed copy
+        const int idx0 = tr ? ~q1.y : q1.y;
+        const float* __restrict__ src = tr ? imgT : img;
+        if (tend > 0.f) {
+            // major crossings strictly inside (0, tend): the slices are nm + 1
+            int nm = (int)((tend - t1a) / dta) + 1;
+            nm = nm < 0 ? 0 : nm;
+            while (nm > 0 && !(fmaf((float)(nm - 1), dta, t1a) < tend)) --nm;
+            while (fmaf((float)nm, dta, t1a) < tend) ++nm;
+            const int S = (nm + K) / K;
+            const int s0 = p * S;
+            if (s0 <= nm) {
+                const int s1 = min(s0 + S, nm + 1);
+                const float ts = s0 == 0 ? 0.f : fmaf((float)(s0 - 1), dta, t1a);
+                const float te = s1 == nm + 1 ? tend : fmaf((float)(s1 - 1), dta, t1a);
+                int mb = 0;
+                float tb = INFINITY;
+                int budget = s1 - s0 + 2;
+                if (dtb > 0.f) {
+                    mb = (int)ceilf((ts - t1b) / dtb);
+                    mb = mb < 0 ? 0 : mb;
+                    while (mb > 0 && !(fmaf((float)(mb - 1), dtb, t1b) < ts)) --mb;
+                    while (fmaf((float)mb, dtb, t1b) < ts) ++mb;
+                    tb = fmaf((float)mb, dtb, t1b);
+                    budget += (int)((te - ts) / dtb) + 2;
+                }
+                int idx = idx0 + s0 * sa + mb * sb;
+                float ma = (float)s0, mbf = (float)mb;
+                float ta = fmaf(ma, dta, t1a);
+                float tc = ts;
+#pragma unroll 2
+                for (int it = 0; tc < te && it < budget; ++it) {
+                    const float tn = fminf(fminf(ta, tb), te);
+                    acc = fmaf(__ldg(src + idx), tn - tc, acc);   // f_I * (C_up - C_low)
+                    tc = tn;
+                    const bool ba = tn == ta, bb = !ba && tn == tb;
+                    ma = ba ? ma + 1.f : ma;
+                    mbf = bb ? mbf + 1.f : mbf;
+                    ta = fmaf(ma, dta, t1a);
+                    tb = fmaf(mbf, dtb, t1b);
+                    idx += ba ? sa : (bb ? sb : 0);
+                }
+            }
+        }
+    }
+    part[threadIdx.x] = acc;
+    __syncthreads();
+    if (p == 0 && m < ray1) {
+        float sum = part[rl];
+#pragma unroll
+        for (int q = 1; q < K; ++q) sum += part[q * RB + rl];   // fixed order: deterministic
+        sino[m] = sum;
+    }
+}
+
 __global__ void __launch_bounds__(256) k_adjoint_ray(const ViewRec* __restrict__ views, DetC dc,
                                                       GridC g, const float* __restrict__ sino,
                                                       float* __restrict__ img, int64_t ray0,
@@ -478,7 +605,16 @@ cudaError_t launch_forward_ray(const xrt_plan_s* p, const float* img, float* sin
                                int64_t ray1, cudaStream_t s) {
     if (ray1 <= ray0) return cudaSuccess;
     const bool generic = std::getenv("XRT_RAY_GENERIC") != nullptr;   // (read per launch: tests toggle it)
-    if (p->dim == 2 && !generic)
+    int pieces = XRT_RAY2D_PIECES;
+    if (const char* e = std::getenv("XRT_RAY2D_PIECES")) pieces = std::atoi(e);   // experiments: 1, 2, 4, 8
+    if (p->dim == 2 && !generic && p->d_ray2d_walk && (pieces > 1 || pieces == -1)) {   // -1: one piece (A/B)
+        const unsigned nb = blocks_for((ray1 - ray0) * pieces, XRT_RAY_BS);
+        const Ray2DW* d = (const Ray2DW*)p->d_ray2d_walk;
+        if (pieces == -1) k_forward_ray2d_pc<1><<<blocks_for(ray1 - ray0, XRT_RAY_BS), XRT_RAY_BS, 0, s>>>(d, img, p->d_fwd_t, sino, ray0, ray1);
+        else if (pieces == 2) k_forward_ray2d_pc<2><<<nb, XRT_RAY_BS, 0, s>>>(d, img, p->d_fwd_t, sino, ray0, ray1);
+        else if (pieces == 8) k_forward_ray2d_pc<8><<<nb, XRT_RAY_BS, 0, s>>>(d, img, p->d_fwd_t, sino, ray0, ray1);
+        else k_forward_ray2d_pc<4><<<blocks_for((ray1 - ray0) * 4, XRT_RAY_BS), XRT_RAY_BS, 0, s>>>(d, img, p->d_fwd_t, sino, ray0, ray1);
+    } else if (p->dim == 2 && !generic)
         k_forward_ray2d<<<blocks_for(ray1 - ray0, XRT_RAY_BS), XRT_RAY_BS, 0, s>>>(p->d_views, p->det, p->grid, img,
                                                                      sino, ray0, ray1);
     else
@@ -536,6 +672,14 @@ cudaError_t launch_adjoint_mixed(const xrt_plan_s* p, const double* sino, double
                                  int64_t ray1, cudaStream_t s) {
     if (ray1 <= ray0) return cudaSuccess;
     k_adjoint_mixed<<<blocks_for(ray1 - ray0, 128), 128, 0, s>>>(p->d_views, p->det, p->grid, sino, img, ray0, ray1);
+    return cudaGetLastError();
+}
+
+size_t ray2d_walk_bytes() { return sizeof(Ray2DW); }
+
+cudaError_t launch_ray2d_walk_desc(const xrt_plan_s* p, cudaStream_t s) {
+    k_ray2d_walk_desc<<<blocks_for(p->n_rays, 128), 128, 0, s>>>(p->d_views, p->det, p->grid, p->n_rays,
+                                                                 (Ray2DW*)p->d_ray2d_walk);
     return cudaGetLastError();
 }
 

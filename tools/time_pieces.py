@@ -1,0 +1,25 @@
+"""2D RAY forward: sequential walk vs K pieces per ray (XRT_RAY2D_PIECES, read per launch), cfg 2 / 1.
+CUDA events on the launching stream, median of 30 after 5 warm-up calls."""
+import json, os, statistics, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch, workloads
+from paper_2006_00686_b200 import Plan
+
+def t(fn, reps=30):
+    for _ in range(5): fn()
+    torch.cuda.synchronize(); ms = []
+    for _ in range(reps):
+        a = torch.cuda.Event(enable_timing=True); b = torch.cuda.Event(enable_timing=True)
+        a.record(); fn(); b.record(); torch.cuda.synchronize(); ms.append(a.elapsed_time(b))
+    return round(statistics.median(ms), 4)
+
+for cfg in (2, 1):
+    c = workloads.config(cfg)
+    p = Plan(c, device=0)
+    x = workloads.make_image(c, device="cuda:0")
+    s = torch.empty(p.sino_shape, device="cuda:0")
+    out = {"cfg": cfg}
+    for k in sys.argv[1:] or ["1", "2", "4", "8"]:
+        os.environ["XRT_RAY2D_PIECES"] = k
+        out[k] = t(lambda: p.forward(x, out=s))
+    print(json.dumps(out), flush=True)
