@@ -279,8 +279,9 @@ int resolve(const xrt_plan_s* p, int op) {
 // fwd_prepare() builds once per call (img -> work_fwd transpose).
 xrt_status fwd_prepare(xrt_plan p, const float* img, cudaStream_t s) {
     if (resolve(p, XRT_OP_FORWARD) == XRT_ALGO_RAY && p->dim == 2 && p->d_fwd_t) {
-        // 2D RAY forward in pieces: x-major rays walk the transposed image
-        cudaError_t e = xrt::launch_transpose2d(img, p->d_fwd_t, p->grid.n[1], p->grid.n[0], false, s);
+        // 2D RAY forward in pieces: the (f, delta f) images, or x-major rays walk the transposed image
+        cudaError_t e = xrt::ray2d_fd_on(p) ? xrt::launch_fd2d(p, img, s)
+                                            : xrt::launch_transpose2d(img, p->d_fwd_t, p->grid.n[1], p->grid.n[0], false, s);
         p->launches += 1;
         if (e != cudaSuccess) return cuda_fail(e, "transpose launch");
         return XRT_OK;
@@ -344,7 +345,8 @@ xrt_status adjoint_range(xrt_plan p, const float* sino, float* img, int64_t v0, 
     } else if (algo == XRT_ALGO_COLUMN && p->dim == 2) {
         if (!(v0 == 0 && v1 == p->n_views)) return fail(XRT_ERR_UNSUPPORTED, "2D slice kernels run all views at once");
         e = p->slice_v1 ? xrt::launch_slice2d(p, true, nullptr, nullptr, sino, nullptr, img, p->d_img_t, s)
-                        : xrt::launch_slice2d_adj(p, sino, img, p->d_img_t, s);
+            : xrt::adjoint2d_pieces(p) ? xrt::launch_adjoint_ray2d_pc(p, sino, img, p->d_img_t, s)
+                                       : xrt::launch_slice2d_adj(p, sino, img, p->d_img_t, s);
     } else if (algo == XRT_ALGO_COLUMN) {
         e = xrt::launch_adjoint_column(p, sino, p->d_work_adj, v0, v1, s);
     } else if (algo == XRT_ALGO_GATHER) {
@@ -505,6 +507,8 @@ xrt_status plan_create_impl(const xrt_geometry* g, int cuda_device, xrt_plan* ou
         // 2D RAY forward in pieces: per-ray fp32 walk state (32 B per ray; cfg 2: 17.7 MB)
         e = cudaMalloc(&p->d_ray2d_walk, xrt::ray2d_walk_bytes() * (size_t)p->n_rays);
         if (e == cudaSuccess) e = cudaMalloc(&p->d_fwd_t, sizeof(float) * (size_t)G.nxy);
+        if (e == cudaSuccess && G.nxy < (1ll << 22))   // magic-float cell index: < 2^22 cells
+            e = cudaMalloc(&p->d_fd2d, 4 * sizeof(float2) * (size_t)G.nxy);
         if (e == cudaSuccess) e = xrt::launch_ray2d_walk_desc(p, (cudaStream_t)0);
         if (e == cudaSuccess) e = cudaDeviceSynchronize();
         if (e != cudaSuccess) {
@@ -763,6 +767,7 @@ xrt_status xrt_plan_destroy(xrt_plan p) {
     cudaFree(p->d_raydesc2d);
     cudaFree(p->d_ray2d_walk);
     cudaFree(p->d_fwd_t);
+    cudaFree(p->d_fd2d);
     cudaFree(p->d_img_t);
     cudaFree(p->d_stage_img);
     cudaFree(p->d_stage_sino);

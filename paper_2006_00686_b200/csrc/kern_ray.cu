@@ -213,8 +213,74 @@ __global__ void k_ray2d_walk_desc(const ViewRec* __restrict__ views, DetC dc, Gr
 }
 
 #ifndef XRT_RAY2D_PIECES
-#define XRT_RAY2D_PIECES 4
+#define XRT_RAY2D_PIECES 4   // cfg 2 forward on f (transposed x-major walk) 0.363 / 0.301 / 0.280 / 0.282 ms at
+                             // 1 / 2 / 4 / 8 pieces; on (f, delta f) 0.371 / 0.285 / 0.250 / 0.249 (AUTO: fd, 4)
 #endif
+#ifndef XRT_ADJ2D_PIECES
+#define XRT_ADJ2D_PIECES 4   // pieces when the 2D adjoint in pieces is selected (not AUTO)
+#endif
+// One piece of a ray: forward (kAdj false) acc += f_I l_I; adjoint red.add of y l_I into the
+// accumulator the ray walks (row-major for y-major rays, transposed for x-major rays).
+template <int K, bool kAdj>
+__device__ __forceinline__ float ray2d_piece(const Ray2DW* __restrict__ dsc, int64_t m, int p,
+                                             const float* __restrict__ img, const float* __restrict__ imgT,
+                                             float* acc_img, float* acc_imgT, float y) {
+    float acc = 0.f;
+    const float4 q0 = __ldg(reinterpret_cast<const float4*>(dsc + m));
+    const int4 q1 = __ldg(reinterpret_cast<const int4*>(dsc + m) + 1);
+    const float t1a = q0.x, dta = q0.y, t1b = q0.z, dtb = q0.w;
+    const float tend = __int_as_float(q1.x);
+    const int sa = q1.z, sb = q1.w;
+    const bool tr = q1.y < 0;                       // x-major: the transposed copy
+    const int idx0 = tr ? ~q1.y : q1.y;
+    const float* __restrict__ src = tr ? imgT : img;
+    float* dst = tr ? acc_imgT : acc_img;
+    if (!(tend > 0.f)) return 0.f;
+    // major crossings strictly inside (0, tend): the slices are nm + 1
+    int nm = (int)((tend - t1a) / dta) + 1;
+    nm = nm < 0 ? 0 : nm;
+    while (nm > 0 && !(fmaf((float)(nm - 1), dta, t1a) < tend)) --nm;
+    while (fmaf((float)nm, dta, t1a) < tend) ++nm;
+    const int S = (nm + K) / K;
+    const int s0 = p * S;
+    if (s0 > nm) return 0.f;
+    const int s1 = min(s0 + S, nm + 1);
+    const float ts = s0 == 0 ? 0.f : fmaf((float)(s0 - 1), dta, t1a);
+    const float te = s1 == nm + 1 ? tend : fmaf((float)(s1 - 1), dta, t1a);
+    int mb = 0;
+    float tb = INFINITY;
+    int budget = s1 - s0 + 2;
+    if (dtb > 0.f) {
+        mb = (int)ceilf((ts - t1b) / dtb);
+        mb = mb < 0 ? 0 : mb;
+        while (mb > 0 && !(fmaf((float)(mb - 1), dtb, t1b) < ts)) --mb;
+        while (fmaf((float)mb, dtb, t1b) < ts) ++mb;
+        tb = fmaf((float)mb, dtb, t1b);
+        budget += (int)((te - ts) / dtb) + 2;
+    }
+    int idx = idx0 + s0 * sa + mb * sb;
+    float ma = (float)s0, mbf = (float)mb;
+    float ta = fmaf(ma, dta, t1a);
+    float tc = ts;
+#pragma unroll 2
+    for (int it = 0; tc < te && it < budget; ++it) {
+        const float tn = fminf(fminf(ta, tb), te);
+        if (kAdj) {   // unconditional: a zero-length unit (a tie) adds 0 to an in-image cell
+            asm volatile("red.global.add.f32 [%0], %1;" :: "l"(dst + idx), "f"(y * (tn - tc)) : "memory");
+        } else {
+            acc = fmaf(__ldg(src + idx), tn - tc, acc);   // f_I * (C_up - C_low)
+        }
+        tc = tn;
+        const bool ba = tn == ta, bb = !ba && tn == tb;
+        ma = ba ? ma + 1.f : ma;
+        mbf = bb ? mbf + 1.f : mbf;
+        ta = fmaf(ma, dta, t1a);
+        tb = fmaf(mbf, dtb, t1b);
+        idx += ba ? sa : (bb ? sb : 0);
+    }
+    return acc;
+}
+
 template <int K>
 __global__ void __launch_bounds__(XRT_RAY_BS, XRT_RAY2D_MINB) k_forward_ray2d_pc(const Ray2DW* __restrict__ dsc,
                                                                            const float* __restrict__ img,
@@ -228,58 +294,8 @@ __global__ void __launch_bounds__(XRT_RAY_BS, XRT_RAY2D_MINB) k_forward_ray2d_pc
     const int p = (int)threadIdx.x / RB, rl = (int)threadIdx.x % RB;
     const int64_t m = ray0 + (int64_t)blockIdx.x * RB + rl;
     float acc = 0.f;
-    if (m < ray1) {   // no early exit: the block meets at the barrier below
-        const float4 q0 = __ldg(reinterpret_cast<const float4*>(dsc + m));
-        const int4 q1 = __ldg(reinterpret_cast<const int4*>(dsc + m) + 1);
-        const float t1a = q0.x, dta = q0.y, t1b = q0.z, dtb = q0.w;
-        const float tend = __int_as_float(q1.x);
-        const int sa = q1.z, sb = q1.w;
-        const bool tr = q1.y < 0;                       // x-major: the transposed copy
-        const int idx0 = tr ? ~q1.y : q1.y;
-        const float* __restrict__ src = tr ? imgT : img;
-        if (tend > 0.f) {
-            // major crossings strictly inside (0, tend): the slices are nm + 1
-            int nm = (int)((tend - t1a) / dta) + 1;
-            nm = nm < 0 ? 0 : nm;
-            while (nm > 0 && !(fmaf((float)(nm - 1), dta, t1a) < tend)) --nm;
-            while (fmaf((float)nm, dta, t1a) < tend) ++nm;
-            const int S = (nm + K) / K;
-            const int s0 = p * S;
-            if (s0 <= nm) {
-                const int s1 = min(s0 + S, nm + 1);
-                const float ts = s0 == 0 ? 0.f : fmaf((float)(s0 - 1), dta, t1a);
-                const float te = s1 == nm + 1 ? tend : fmaf((float)(s1 - 1), dta, t1a);
-                int mb = 0;
-                float tb = INFINITY;
-                int budget = s1 - s0 + 2;
-                if (dtb > 0.f) {
-                    mb = (int)ceilf((ts - t1b) / dtb);
-                    mb = mb < 0 ? 0 : mb;
-                    while (mb > 0 && !(fmaf((float)(mb - 1), dtb, t1b) < ts)) --mb;
-                    while (fmaf((float)mb, dtb, t1b) < ts) ++mb;
-                    tb = fmaf((float)mb, dtb, t1b);
-                    budget += (int)((te - ts) / dtb) + 2;
-                }
-                int idx = idx0 + s0 * sa + mb * sb;
-                float ma = (float)s0, mbf = (float)mb;
-                float ta = fmaf(ma, dta, t1a);
-                float tc = ts;
-#pragma unroll 2
-                for (int it = 0; tc < te && it < budget; ++it) {
-                    const float tn = fminf(fminf(ta, tb), te);
-                    acc = fmaf(__ldg(src + idx), tn - tc, acc);   // f_I * (C_up - C_low)
-                    tc = tn;
-                    const bool ba = tn == ta, bb = !ba && tn == tb;
-                    ma = ba ? ma + 1.f : ma;
-                    mbf = bb ? mbf + 1.f : mbf;
-                    ta = fmaf(ma, dta, t1a);
-                    tb = fmaf(mbf, dtb, t1b);
-                    idx += ba ? sa : (bb ? sb : 0);
-                }
-            }
-        }
-    }
-    part[threadIdx.x] = acc;
+    if (m < ray1) acc = ray2d_piece<K, false>(dsc, m, p, img, imgT, nullptr, nullptr, 0.f);
+    part[threadIdx.x] = acc;   // no early exit above: the block meets at the barrier
     __syncthreads();
     if (p == 0 && m < ray1) {
         float sum = part[rl];
@@ -287,6 +303,175 @@ __global__ void __launch_bounds__(XRT_RAY_BS, XRT_RAY2D_MINB) k_forward_ray2d_pc
         for (int q = 1; q < K; ++q) sum += part[q * RB + rl];   // fixed order: deterministic
         sino[m] = sum;
     }
+}
+
+// 2D forward in pieces on (f, delta f) images: per major slice n, [t_lo, t_hi] with t_hi = T_a(n) (the
+// piece's last slice of the ray: tend), the minor crossing tau = T_b(m) decides cr = [tau < t_hi] and
+// l_e = max(t_hi - tau, 0) (C_up - C_low of the second unit, eq:range_length P:217-220), and
+//     acc += f(c) (t_hi - t_lo) + (f(c + s_b) - f(c)) l_e  =  f(c) l_s + f(c + s_b) l_e,
+// one 8-byte load of (f, f[+-1] - f) per slice (the valid band of eq:restriction_j P:197-212 is
+// {c_b, c_b + s_b} when |w_b| <= |w_a|).  Crossing values are the same fmaf(m, dt, t1) as the
+// sequential walk's.  Rays within 2^-8 of 45 degrees (two minor crossings per slice possible in fp32)
+// take the unit walk on the f components.  The four images (row-major / transposed x minor step
+// +1 / -1) are built per call by k_fd2d.
+__global__ void __launch_bounds__(256) k_fd2d(const float* __restrict__ img, float2* __restrict__ fd, int nx,
+                                              int ny) {
+    __shared__ float t[34][35];
+    const int i0 = blockIdx.x * 32, j0 = blockIdx.y * 32;
+    for (int r = threadIdx.y; r < 34; r += 8)
+        for (int q = threadIdx.x; q < 34; q += 32) {
+            const int j = j0 - 1 + r, i = i0 - 1 + q;
+            t[r][q] = (j >= 0 && j < ny && i >= 0 && i < nx) ? img[(int64_t)j * nx + i] : 0.f;
+        }
+    __syncthreads();
+    const int64_t nxy = (int64_t)nx * ny;
+    for (int r = threadIdx.y; r < 32; r += 8) {       // row-major, minor = x: lane = i
+        const int j = j0 + r, i = i0 + (int)threadIdx.x;
+        if (j < ny && i < nx) {
+            const float f = t[r + 1][threadIdx.x + 1];
+            fd[(int64_t)j * nx + i] = make_float2(f, t[r + 1][threadIdx.x + 2] - f);
+            fd[nxy + (int64_t)j * nx + i] = make_float2(f, t[r + 1][threadIdx.x] - f);
+        }
+    }
+    for (int r = threadIdx.y; r < 32; r += 8) {       // transposed [i][j], minor = y: lane = j
+        const int i = i0 + r, j = j0 + (int)threadIdx.x;
+        if (j < ny && i < nx) {
+            const float f = t[threadIdx.x + 1][r + 1];
+            fd[2 * nxy + (int64_t)i * ny + j] = make_float2(f, t[threadIdx.x + 2][r + 1] - f);
+            fd[3 * nxy + (int64_t)i * ny + j] = make_float2(f, t[threadIdx.x][r + 1] - f);
+        }
+    }
+}
+
+constexpr float kMagicF = 12582912.0f;          // 1.5 * 2^23: bits(kMagicF + c) = 0x4B400000 + c (c < 2^22)
+constexpr unsigned kMagicFBits = 0x4B400000u;
+
+#ifndef XRT_RAY2D_FD_UNROLL
+#define XRT_RAY2D_FD_UNROLL 4
+#endif
+constexpr int kFdUnroll2d = XRT_RAY2D_FD_UNROLL;
+template <int K>
+__device__ __forceinline__ float ray2d_piece_fd(const Ray2DW* __restrict__ dsc, int64_t m, int p,
+                                                const float2* __restrict__ fd, int64_t nxy) {
+    const float4 q0 = __ldg(reinterpret_cast<const float4*>(dsc + m));
+    const int4 q1 = __ldg(reinterpret_cast<const int4*>(dsc + m) + 1);
+    const float t1a = q0.x, dta = q0.y, dtb = q0.w;
+    float t1b = q0.z;
+    const float tend = __int_as_float(q1.x);
+    const int sa = q1.z, sb = q1.w;
+    const bool tr = q1.y < 0;
+    const int idx0 = tr ? ~q1.y : q1.y;
+    if (!(tend > 0.f)) return 0.f;
+    int nm = (int)((tend - t1a) / dta) + 1;
+    nm = nm < 0 ? 0 : nm;
+    while (nm > 0 && !(fmaf((float)(nm - 1), dta, t1a) < tend)) --nm;
+    while (fmaf((float)nm, dta, t1a) < tend) ++nm;
+    const int S = (nm + K) / K;
+    const int s0 = p * S;
+    if (s0 > nm) return 0.f;
+    const int s1 = min(s0 + S, nm + 1);
+    const float ts = s0 == 0 ? 0.f : fmaf((float)(s0 - 1), dta, t1a);
+    int mb = 0;
+    if (dtb > 0.f) {
+        mb = (int)ceilf((ts - t1b) / dtb);
+        mb = mb < 0 ? 0 : mb;
+        while (mb > 0 && !(fmaf((float)(mb - 1), dtb, t1b) < ts)) --mb;
+        while (fmaf((float)mb, dtb, t1b) < ts) ++mb;
+    } else {
+        t1b = 1.0e30f;   // fixed minor axis: no crossing (finite, so l_e = d * 0 = 0)
+    }
+    const float2* __restrict__ img = fd + (tr ? 2 * nxy : 0) + (sb < 0 ? nxy : 0);
+    const int idx = idx0 + s0 * sa + mb * sb;
+    float acc0 = 0.f, acc1 = 0.f;
+    if (dtb > 0.f && dtb < dta * (1.f + 1.f / 256.f)) {
+        // near 45 degrees: the unit walk (ties: the major axis first, as the pieces walk)
+        const float* __restrict__ f = reinterpret_cast<const float*>(img);
+        const float te = s1 == nm + 1 ? tend : fmaf((float)(s1 - 1), dta, t1a);
+        float ma = (float)s0, mbf = (float)mb;
+        float ta = fmaf(ma, dta, t1a), tb = fmaf(mbf, dtb, t1b), tc = ts;
+        int id = idx;
+        const int budget = s1 - s0 + (int)((te - ts) / dtb) + 4;
+        for (int it = 0; tc < te && it < budget; ++it) {
+            const float tn = fminf(fminf(ta, tb), te);
+            acc0 = fmaf(__ldg(f + 2 * (int64_t)id), tn - tc, acc0);
+            tc = tn;
+            const bool ba = tn == ta, bb = !ba && tn == tb;
+            ma = ba ? ma + 1.f : ma;
+            mbf = bb ? mbf + 1.f : mbf;
+            ta = fmaf(ma, dta, t1a);
+            tb = fmaf(mbf, dtb, t1b);
+            id += ba ? sa : (bb ? sb : 0);
+        }
+        return acc0;
+    }
+    const unsigned long long base = (unsigned long long)img - 8ull * kMagicFBits;
+    const float saf = (float)sa, sbf = (float)sb;
+    float idxf = kMagicF + (float)idx, mbf = (float)mb, tb = fmaf(mbf, dtb, t1b), tlo = ts, nf = (float)s0;
+    const int nlast = min(s1, nm);   // slices ending at a major crossing T_a(n)
+#pragma unroll kFdUnroll2d
+    for (int n = s0; n < nlast; ++n) {
+        const float thi = fmaf(nf, dta, t1a);
+        nf += 1.f;
+        const float d = thi - tb;
+        float cr;
+        asm("mul.ftz.sat.f32 %0, %1, 0f7F000000;" : "=f"(cr) : "f"(d));   // [tau < t_hi]
+        float2 v;
+        asm("ld.global.nc.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "l"(base + 8ull * __float_as_uint(idxf)));
+        acc0 = fmaf(v.x, thi - tlo, acc0);
+        acc1 = fmaf(v.y, d * cr, acc1);
+        mbf += cr;
+        tb = fmaf(mbf, dtb, t1b);
+        idxf = fmaf(cr, sbf, idxf) + saf;
+        tlo = thi;
+    }
+    if (s1 == nm + 1) {   // the ray's last slice ends at tend
+        const float d = tend - tb;
+        float cr;
+        asm("mul.ftz.sat.f32 %0, %1, 0f7F000000;" : "=f"(cr) : "f"(d));
+        float2 v;
+        asm("ld.global.nc.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "l"(base + 8ull * __float_as_uint(idxf)));
+        acc0 = fmaf(v.x, tend - tlo, acc0);
+        acc1 = fmaf(v.y, d * cr, acc1);
+    }
+    return acc0 + acc1;
+}
+
+template <int K>
+__global__ void __launch_bounds__(XRT_RAY_BS, XRT_RAY2D_MINB) k_forward_ray2d_fd(const Ray2DW* __restrict__ dsc,
+                                                                           const float2* __restrict__ fd,
+                                                                           int64_t nxy, float* __restrict__ sino,
+                                                                           int64_t ray0, int64_t ray1) {
+    constexpr int RB = XRT_RAY_BS / K;
+    __shared__ float part[XRT_RAY_BS];
+    const int p = (int)threadIdx.x / RB, rl = (int)threadIdx.x % RB;
+    const int64_t m = ray0 + (int64_t)blockIdx.x * RB + rl;
+    float acc = 0.f;
+    if (m < ray1) acc = ray2d_piece_fd<K>(dsc, m, p, fd, nxy);
+    part[threadIdx.x] = acc;
+    __syncthreads();
+    if (p == 0 && m < ray1) {
+        float sum = part[rl];
+#pragma unroll
+        for (int q = 1; q < K; ++q) sum += part[q * RB + rl];
+        sino[m] = sum;
+    }
+}
+
+// 2D adjoint in pieces (the forward's pieces and transposed x-major walk; scatter with red.add into
+// acc_img / acc_imgT, summed by the plan's finishing transpose)
+template <int K>
+__global__ void __launch_bounds__(XRT_RAY_BS, XRT_RAY2D_MINB) k_adjoint_ray2d_pc(const Ray2DW* __restrict__ dsc,
+                                                                           const float* __restrict__ sino,
+                                                                           float* __restrict__ acc_img,
+                                                                           float* __restrict__ acc_imgT, int64_t ray0,
+                                                                           int64_t ray1) {
+    constexpr int RB = XRT_RAY_BS / K;
+    const int p = (int)threadIdx.x / RB, rl = (int)threadIdx.x % RB;
+    const int64_t m = ray0 + (int64_t)blockIdx.x * RB + rl;
+    if (m >= ray1) return;
+    const float y = __ldg(sino + m);
+    if (y == 0.f) return;
+    ray2d_piece<K, true>(dsc, m, p, nullptr, nullptr, acc_img, acc_imgT, y);
 }
 
 __global__ void __launch_bounds__(256) k_adjoint_ray(const ViewRec* __restrict__ views, DetC dc,
@@ -607,7 +792,15 @@ cudaError_t launch_forward_ray(const xrt_plan_s* p, const float* img, float* sin
     const bool generic = std::getenv("XRT_RAY_GENERIC") != nullptr;   // (read per launch: tests toggle it)
     int pieces = XRT_RAY2D_PIECES;
     if (const char* e = std::getenv("XRT_RAY2D_PIECES")) pieces = std::atoi(e);   // experiments: 1, 2, 4, 8
-    if (p->dim == 2 && !generic && p->d_ray2d_walk && (pieces > 1 || pieces == -1)) {   // -1: one piece (A/B)
+    if (p->dim == 2 && !generic && ray2d_fd_on(p) && (pieces > 1 || pieces == -1)) {
+        const unsigned nb = blocks_for((ray1 - ray0) * (pieces > 0 ? pieces : 1), XRT_RAY_BS);
+        const Ray2DW* d = (const Ray2DW*)p->d_ray2d_walk;
+        const int64_t nxy = p->grid.nxy;
+        if (pieces == -1) k_forward_ray2d_fd<1><<<nb, XRT_RAY_BS, 0, s>>>(d, p->d_fd2d, nxy, sino, ray0, ray1);
+        else if (pieces == 2) k_forward_ray2d_fd<2><<<nb, XRT_RAY_BS, 0, s>>>(d, p->d_fd2d, nxy, sino, ray0, ray1);
+        else if (pieces == 8) k_forward_ray2d_fd<8><<<nb, XRT_RAY_BS, 0, s>>>(d, p->d_fd2d, nxy, sino, ray0, ray1);
+        else k_forward_ray2d_fd<4><<<blocks_for((ray1 - ray0) * 4, XRT_RAY_BS), XRT_RAY_BS, 0, s>>>(d, p->d_fd2d, nxy, sino, ray0, ray1);
+    } else if (p->dim == 2 && !generic && p->d_ray2d_walk && (pieces > 1 || pieces == -1)) {   // -1: one piece (A/B)
         const unsigned nb = blocks_for((ray1 - ray0) * pieces, XRT_RAY_BS);
         const Ray2DW* d = (const Ray2DW*)p->d_ray2d_walk;
         if (pieces == -1) k_forward_ray2d_pc<1><<<blocks_for(ray1 - ray0, XRT_RAY_BS), XRT_RAY_BS, 0, s>>>(d, img, p->d_fwd_t, sino, ray0, ray1);
@@ -620,6 +813,27 @@ cudaError_t launch_forward_ray(const xrt_plan_s* p, const float* img, float* sin
     else
         k_forward_ray<<<blocks_for(ray1 - ray0, XRT_RAY_BS), XRT_RAY_BS, 0, s>>>(p->d_views, p->det, p->grid, img,
                                                                    sino, ray0, ray1);
+    return cudaGetLastError();
+}
+
+// The 2D adjoint in pieces is an A/B option (XRT_ADJ2D_PIECES=K, read per launch): cfg 2 0.78 ms at
+// K = 4 (1.01 / 0.88 / 0.80 at 1 / 2 / 8) vs 0.45 ms for the lockstep slice adjoint (AUTO), whose
+// warps reduce into consecutive addresses; the free-running pieces' reductions do not coalesce.
+bool adjoint2d_pieces(const xrt_plan_s* p) {
+    const char* e = std::getenv("XRT_ADJ2D_PIECES");
+    return p->d_ray2d_walk && e && std::atoi(e) > 0;
+}
+
+cudaError_t launch_adjoint_ray2d_pc(const xrt_plan_s* p, const float* sino, float* acc_img, float* acc_imgT,
+                                    cudaStream_t s) {
+    int pieces = XRT_ADJ2D_PIECES;
+    if (const char* e = std::getenv("XRT_ADJ2D_PIECES")) pieces = std::atoi(e);
+    const int64_t n = p->n_rays;
+    const Ray2DW* d = (const Ray2DW*)p->d_ray2d_walk;
+    if (pieces == 1) k_adjoint_ray2d_pc<1><<<blocks_for(n, XRT_RAY_BS), XRT_RAY_BS, 0, s>>>(d, sino, acc_img, acc_imgT, 0, n);
+    else if (pieces == 2) k_adjoint_ray2d_pc<2><<<blocks_for(2 * n, XRT_RAY_BS), XRT_RAY_BS, 0, s>>>(d, sino, acc_img, acc_imgT, 0, n);
+    else if (pieces == 8) k_adjoint_ray2d_pc<8><<<blocks_for(8 * n, XRT_RAY_BS), XRT_RAY_BS, 0, s>>>(d, sino, acc_img, acc_imgT, 0, n);
+    else k_adjoint_ray2d_pc<4><<<blocks_for(4 * n, XRT_RAY_BS), XRT_RAY_BS, 0, s>>>(d, sino, acc_img, acc_imgT, 0, n);
     return cudaGetLastError();
 }
 
@@ -676,6 +890,18 @@ cudaError_t launch_adjoint_mixed(const xrt_plan_s* p, const double* sino, double
 }
 
 size_t ray2d_walk_bytes() { return sizeof(Ray2DW); }
+
+// the 2D forward in pieces on (f, delta f) images (AUTO; XRT_RAY2D_FD=0: on f, read per launch)
+bool ray2d_fd_on(const xrt_plan_s* p) {
+    const char* e = std::getenv("XRT_RAY2D_FD");
+    return p->d_ray2d_walk && p->d_fd2d && !(e && std::atoi(e) == 0);
+}
+
+cudaError_t launch_fd2d(const xrt_plan_s* p, const float* img, cudaStream_t s) {
+    const int nx = p->grid.n[0], ny = p->grid.n[1];
+    k_fd2d<<<dim3((unsigned)((nx + 31) / 32), (unsigned)((ny + 31) / 32)), dim3(32, 8), 0, s>>>(img, p->d_fd2d, nx, ny);
+    return cudaGetLastError();
+}
 
 cudaError_t launch_ray2d_walk_desc(const xrt_plan_s* p, cudaStream_t s) {
     k_ray2d_walk_desc<<<blocks_for(p->n_rays, 128), 128, 0, s>>>(p->d_views, p->det, p->grid, p->n_rays,

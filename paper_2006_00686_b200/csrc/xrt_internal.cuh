@@ -258,6 +258,7 @@ struct xrt_plan_s {
     void* d_raydesc2d = nullptr;       // per-(view, column) rays in index space (2D GATHER)
     void* d_ray2d_walk = nullptr;      // 2D RAY forward in pieces: per-ray fp32 walk state (32 B per ray)
     float* d_fwd_t = nullptr;          // 2D RAY forward in pieces: transposed input (x-major rays walk it)
+    float2* d_fd2d = nullptr;          // 2D forward in pieces on (f, f[+-1] - f): 4 images (row-major / transposed, +-1)
     float* d_img_t = nullptr;          // 2D COLUMN (slice) kernels: transposed image / accumulator
     bool slice_v1 = false;             // XRT_SLICE_V1=1: the round-1 slice adjoint (A/B)
     float* d_gather_y = nullptr;       // GATHER workspace: rescaled, transposed sinogram of one view block
@@ -285,6 +286,11 @@ cudaError_t launch_adjoint_ray(const xrt_plan_s* p, const float* sino, float* im
 cudaError_t launch_units_count(const xrt_plan_s* p, int64_t ray0, int64_t ray1, int64_t* counts,
                                cudaStream_t s);
 size_t ray2d_walk_bytes();
+bool adjoint2d_pieces(const xrt_plan_s* p);
+bool ray2d_fd_on(const xrt_plan_s* p);
+cudaError_t launch_fd2d(const xrt_plan_s* p, const float* img, cudaStream_t s);
+cudaError_t launch_adjoint_ray2d_pc(const xrt_plan_s* p, const float* sino, float* acc_img, float* acc_imgT,
+                                    cudaStream_t s);
 cudaError_t launch_ray2d_walk_desc(const xrt_plan_s* p, cudaStream_t s);
 cudaError_t launch_forward_att(const xrt_plan_s* p, const float* img, const float* mu, float* sino, int64_t ray0,
                                int64_t ray1, cudaStream_t s);

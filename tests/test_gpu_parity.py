@@ -480,6 +480,25 @@ def test_ray2d_pieces_equal_sequential(cuda_ok, idx, pieces, monkeypatch):
         assert H.fwd_err(b, ref) <= H.FWD_TOL
 
 
+@pytest.mark.parametrize("idx", [1, 2])
+def test_adjoint2d_pieces(cuda_ok, idx, monkeypatch):
+    """The 2D adjoint in pieces (A/B option XRT_ADJ2D_PIECES, the forward's pieces and transposed
+    x-major walk with red.add) equals the AUTO slice adjoint to fp32 rounding, and with the AUTO
+    forward (pieces) passes the north_star dot-product test (1e-5)."""
+    c = workloads.config(idx)
+    p = Plan(c, device=0)
+    img = _image(c)
+    y = workloads.make_sino_input(c, device="cuda:0")
+    a = p.adjoint(y).cpu().numpy().ravel().astype(np.float64)
+    monkeypatch.setenv("XRT_ADJ2D_PIECES", "4")
+    b = p.adjoint(y).cpu().numpy().ravel().astype(np.float64)
+    assert H.rel_l2(b, a) <= 1e-5
+    ax = p.forward(img).cpu().numpy().ravel().astype(np.float64)
+    lhs = float(np.dot(ax, y.cpu().numpy().ravel().astype(np.float64)))
+    rhs = float(np.dot(img.cpu().numpy().ravel().astype(np.float64), b))
+    assert abs(lhs - rhs) <= 1e-5 * max(abs(lhs), abs(rhs))
+
+
 @pytest.mark.parametrize("full", [False, True])
 def test_flat_kernel_bitwise_general(cuda_ok, full, monkeypatch):
     """The flat-only forward instantiation (3D parallel beam without tilt) equals the general column

@@ -1,4 +1,5 @@
-"""2D RAY forward: sequential walk vs K pieces per ray (XRT_RAY2D_PIECES, read per launch), cfg 2 / 1.
+"""2D RAY forward: sequential walk vs K pieces per ray (XRT_RAY2D_PIECES, read per launch), cfg 2 / 1;
+adjoint: slice v2 vs K pieces (XRT_ADJ2D_PIECES).
 CUDA events on the launching stream, median of 30 after 5 warm-up calls."""
 import json, os, statistics, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
@@ -22,4 +23,9 @@ for cfg in (2, 1):
     for k in sys.argv[1:] or ["1", "2", "4", "8"]:
         os.environ["XRT_RAY2D_PIECES"] = k
         out[k] = t(lambda: p.forward(x, out=s))
+    y = workloads.make_sino_input(c, device="cuda:0")
+    xo = torch.empty_like(x)
+    for k in ["0", "1", "2", "4", "8"]:   # adjoint: 0 = slice v2, else K pieces
+        os.environ["XRT_ADJ2D_PIECES"] = k
+        out["adj" + k] = t(lambda: p.adjoint(y, out=xo))
     print(json.dumps(out), flush=True)
