@@ -346,7 +346,8 @@ xrt_status adjoint_range(xrt_plan p, const float* sino, float* img, int64_t v0, 
         if (!(v0 == 0 && v1 == p->n_views)) return fail(XRT_ERR_UNSUPPORTED, "2D slice kernels run all views at once");
         e = p->slice_v1 ? xrt::launch_slice2d(p, true, nullptr, nullptr, sino, nullptr, img, p->d_img_t, s)
             : xrt::adjoint2d_pieces(p) ? xrt::launch_adjoint_ray2d_pc(p, sino, img, p->d_img_t, s)
-                                       : xrt::launch_slice2d_adj(p, sino, img, p->d_img_t, s);
+            : xrt::slice2d_pieces_on(p) ? xrt::launch_slice2d_adj_pc(p, sino, img, p->d_img_t, s)
+                                        : xrt::launch_slice2d_adj(p, sino, img, p->d_img_t, s);
     } else if (algo == XRT_ALGO_COLUMN) {
         e = xrt::launch_adjoint_column(p, sino, p->d_work_adj, v0, v1, s);
     } else if (algo == XRT_ALGO_GATHER) {

@@ -20,6 +20,7 @@
 // the half-open cell floor(u0_a) (ties to the bigger index).
 #include <cuda_runtime.h>
 
+#include <climits>
 #include <cstdlib>
 
 #include "xrt_internal.cuh"
@@ -457,6 +458,134 @@ __global__ void __launch_bounds__(XRT_RAY_BS, XRT_RAY2D_MINB) k_forward_ray2d_fd
     }
 }
 
+// 2D slice adjoint in pieces (AUTO for the 2D beams): the lockstep slice adjoint of kern_gather2d.cu
+// (k_slice2d_adj: a warp = 32 adjacent detector columns of one view walking major slice by major
+// slice, at most two units per slice, reductions to consecutive addresses), its lockstep trips split
+// into K pieces run by K warps (the r2k capture of k_slice2d_adj had 58 % warps active: warps of very
+// different lengths).  A lane enters a piece in the state the walk has after its previous slices:
+// slice n0, t_lo = T_a(n0 - 1), the minor crossings T_b(m) < t_lo taken (a crossing AT a slice end is
+// taken in the next slice, le = t_hi - T_b > 0 there) -- the same fmaf values, so each unit's y l is
+// bit-identical to the unsplit kernel's.  Per-ray fp32 state from the plan's Ray2DW descriptors (no
+// fp64 setup per warp).  Lanes whose ray is steeper than the warp's major axis or travels against it
+// walk their ray alone (piece 0 only).
+template <int K>
+__global__ void __launch_bounds__(128) k_slice2d_adj_pc(const Ray2DW* __restrict__ dsc, DetC dc, GridC g,
+                                                       const float* __restrict__ y_in, float* __restrict__ acc_img,
+                                                       float* __restrict__ acc_imgT, int n_views, int gpv) {
+    const int lane = threadIdx.x & 31;
+    const int64_t gw = ((int64_t)blockIdx.x * 128 + threadIdx.x) >> 5;
+    const int p = (int)(gw % K);
+    const int64_t grp = gw / K;
+    const int v = (int)(grp / gpv), cgp = (int)(grp - (int64_t)v * gpv);
+    if (v >= n_views) return;                               // warp-uniform
+    const int c = cgp * 32 + lane;
+    const int nx = g.n[0], ny = g.n[1];
+    float t1a = INFINITY, dta = 0.f, t1b = INFINITY, dtb = 0.f, tend = 0.f, y = 0.f;
+    int idx0 = 0, sa = 0, sb = 0;
+    bool tr = false, hit = false;
+    if (c < dc.cols) {
+        const int64_t m = (int64_t)v * dc.cols + c;
+        const float4 q0 = __ldg(reinterpret_cast<const float4*>(dsc + m));
+        const int4 q1 = __ldg(reinterpret_cast<const int4*>(dsc + m) + 1);
+        t1a = q0.x; dta = q0.y; t1b = q0.z; dtb = q0.w;
+        tend = __int_as_float(q1.x);
+        tr = q1.y < 0; idx0 = tr ? ~q1.y : q1.y; sa = q1.z; sb = q1.w;
+        hit = tend > 0.f;
+        y = __ldg(y_in + m);
+    }
+    const unsigned bh = __ballot_sync(0xffffffffu, hit);
+    if (bh == 0u) return;
+    // warp major axis by majority of the lanes' own major axes (x-major rays walk the transposed image)
+    const unsigned bx = __ballot_sync(0xffffffffu, hit && tr);
+    const bool wtr = 2 * __popc(bx) >= __popc(bh);
+    const int len = wtr ? ny : nx;                          // walked row length (minor extent)
+    const int sgn = sa > 0 ? 1 : -1;
+    const unsigned bw = __ballot_sync(0xffffffffu, hit && tr == wtr);
+    const int dir = __shfl_sync(0xffffffffu, hit && tr == wtr ? sgn : 0, bw ? __ffs(bw) - 1 : 0);   // common travel direction
+    const bool alone = hit && (tr != wtr || sgn != dir || dir == 0);
+    if (alone && p == 0 && y != 0.f) {
+        // the ray's own unit walk (its own major axis, its own walked image)
+        float* dst = tr ? acc_imgT : acc_img;
+        float tc = 0.f, ta = t1a, tb = t1b, ma = 0.f, mbf = 0.f;
+        int id = idx0;
+        const int budget = (tr ? nx : ny) + (tr ? ny : nx) + 2;
+        for (int it = 0; it < budget && tc < tend; ++it) {
+            const float tn = fminf(fminf(ta, tb), tend);
+            const float l = tn - tc;
+            if (l > 0.f) asm volatile("red.global.add.f32 [%0], %1;" :: "l"(dst + id), "f"(y * l) : "memory");
+            tc = tn;
+            if (tn == ta) { ma += 1.f; ta = fmaf(ma, dta, t1a); id += sa; }
+            else if (tn == tb) { mbf += 1.f; tb = fmaf(mbf, dtb, t1b); id += sb; }
+        }
+    }
+    const bool live = hit && !alone && y != 0.f;
+    const int ca = live ? idx0 / len : 0, cb = live ? idx0 - ca * len : 0;
+    int n_sl = 0;
+    if (live) {
+        int m = (int)((tend - t1a) / dta) + 1;
+        m = m < 0 ? 0 : m;
+        while (m > 0 && !(fmaf((float)(m - 1), dta, t1a) < tend)) --m;
+        while (fmaf((float)m, dta, t1a) < tend) ++m;
+        n_sl = m + 1;
+    }
+    int kfirst = live ? ca * dir : INT_MAX;
+    int klast = live ? (ca + dir * (n_sl - 1)) * dir : INT_MIN;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        kfirst = min(kfirst, __shfl_xor_sync(0xffffffffu, kfirst, o));
+        klast = max(klast, __shfl_xor_sync(0xffffffffu, klast, o));
+    }
+    if (kfirst > klast) return;
+    const int n_trips = klast - kfirst + 1;
+    const int B = (n_trips + K - 1) / K;
+    const int k0 = p * B, k1 = min(n_trips, k0 + B);
+    if (k0 >= k1) return;
+    const int start = live ? ca * dir - kfirst : 0;        // lockstep trip of the lane's first slice
+    const int n0 = max(k0 - start, 0);                     // the lane's first slice in this piece
+    float mb = 0.f, t_lo = 0.f;
+    if (live && n0 > 0 && n0 < n_sl) {
+        t_lo = fmaf((float)(n0 - 1), dta, t1a);
+        if (sb != 0) {
+            int q = (int)ceilf((t_lo - t1b) / dtb);
+            q = q < 0 ? 0 : q;
+            while (q > 0 && !(fmaf((float)(q - 1), dtb, t1b) < t_lo)) --q;
+            while (fmaf((float)q, dtb, t1b) < t_lo) ++q;
+            mb = (float)q;
+        }
+    }
+    float cbf = kMagicF + (float)(cb + (int)mb * sb);
+    const float sbf = (float)sb;
+    const float ndtb = sb != 0 ? -dtb : 0.f;
+    const float ntb0 = sb != 0 ? -t1b : -1.0e30f;
+    float ntb = fmaf(mb, ndtb, ntb0);
+    float ma = (float)n0;
+    float* acco = wtr ? acc_imgT : acc_img;
+    const long long rstep = (long long)dir * 4ll * len;
+    unsigned long long row = (unsigned long long)acco - 4ull * kMagicFBits +
+                             (unsigned long long)((long long)(ca + dir * n0) * 4ll * len);
+    for (int k = k0; k < k1; ++k) {
+        const int rel = k - start;
+        if (live && (unsigned)rel < (unsigned)n_sl) {
+            const float Ta = fmaf(ma, dta, t1a);
+            const float t_hi = fminf(Ta, tend);
+            const float dlt = t_hi - t_lo;
+            const float le = t_hi + ntb;                    // t_hi - T_b
+            float cr;
+            asm("set.gt.f32.f32 %0, %1, 0f00000000;" : "=f"(cr) : "f"(le));
+            const float lm = fmaxf(le, 0.f);
+            float* p0 = (float*)(row + 4ull * __float_as_uint(cbf));
+            asm volatile("red.global.add.f32 [%0], %1;" :: "l"(p0), "f"(y * (dlt - lm)) : "memory");
+            if (cr != 0.f) asm volatile("red.global.add.f32 [%0], %1;" :: "l"(p0 + sb), "f"(y * lm) : "memory");
+            cbf = fmaf(cr, sbf, cbf);
+            mb += cr;
+            ntb = fmaf(mb, ndtb, ntb0);
+            ma += 1.f;
+            t_lo = t_hi;
+            row += (unsigned long long)rstep;
+        }
+    }
+}
+
 // 2D adjoint in pieces (the forward's pieces and transposed x-major walk; scatter with red.add into
 // acc_img / acc_imgT, summed by the plan's finishing transpose)
 template <int K>
@@ -834,6 +963,31 @@ cudaError_t launch_adjoint_ray2d_pc(const xrt_plan_s* p, const float* sino, floa
     else if (pieces == 2) k_adjoint_ray2d_pc<2><<<blocks_for(2 * n, XRT_RAY_BS), XRT_RAY_BS, 0, s>>>(d, sino, acc_img, acc_imgT, 0, n);
     else if (pieces == 8) k_adjoint_ray2d_pc<8><<<blocks_for(8 * n, XRT_RAY_BS), XRT_RAY_BS, 0, s>>>(d, sino, acc_img, acc_imgT, 0, n);
     else k_adjoint_ray2d_pc<4><<<blocks_for(4 * n, XRT_RAY_BS), XRT_RAY_BS, 0, s>>>(d, sino, acc_img, acc_imgT, 0, n);
+    return cudaGetLastError();
+}
+
+#ifndef XRT_SLICE2D_PIECES
+#define XRT_SLICE2D_PIECES 4
+#endif
+// 2D slice adjoint in pieces (AUTO when the plan has the walk descriptors; XRT_SLICE2D_PIECES=0:
+// the unsplit k_slice2d_adj, read per launch)
+bool slice2d_pieces_on(const xrt_plan_s* p) {
+    const char* e = std::getenv("XRT_SLICE2D_PIECES");
+    return p->d_ray2d_walk && !(e && std::atoi(e) == 0);
+}
+
+cudaError_t launch_slice2d_adj_pc(const xrt_plan_s* p, const float* y_in, float* acc_img, float* acc_imgT,
+                                  cudaStream_t s) {
+    int pieces = XRT_SLICE2D_PIECES;
+    if (const char* e = std::getenv("XRT_SLICE2D_PIECES")) pieces = std::atoi(e);
+    const int gpv = (p->det.cols + 31) / 32;
+    const Ray2DW* d = (const Ray2DW*)p->d_ray2d_walk;
+    const int64_t warps = p->n_views * (int64_t)gpv * pieces;
+    const unsigned nb = blocks_for(warps * 32, 128);
+    if (pieces == 1) k_slice2d_adj_pc<1><<<nb, 128, 0, s>>>(d, p->det, p->grid, y_in, acc_img, acc_imgT, (int)p->n_views, gpv);
+    else if (pieces == 2) k_slice2d_adj_pc<2><<<nb, 128, 0, s>>>(d, p->det, p->grid, y_in, acc_img, acc_imgT, (int)p->n_views, gpv);
+    else if (pieces == 8) k_slice2d_adj_pc<8><<<nb, 128, 0, s>>>(d, p->det, p->grid, y_in, acc_img, acc_imgT, (int)p->n_views, gpv);
+    else k_slice2d_adj_pc<4><<<blocks_for(p->n_views * (int64_t)gpv * 4 * 32, 128), 128, 0, s>>>(d, p->det, p->grid, y_in, acc_img, acc_imgT, (int)p->n_views, gpv);
     return cudaGetLastError();
 }
 

@@ -288,6 +288,9 @@ cudaError_t launch_units_count(const xrt_plan_s* p, int64_t ray0, int64_t ray1, 
 size_t ray2d_walk_bytes();
 bool adjoint2d_pieces(const xrt_plan_s* p);
 bool ray2d_fd_on(const xrt_plan_s* p);
+bool slice2d_pieces_on(const xrt_plan_s* p);
+cudaError_t launch_slice2d_adj_pc(const xrt_plan_s* p, const float* y_in, float* acc_img, float* acc_imgT,
+                                  cudaStream_t s);
 cudaError_t launch_fd2d(const xrt_plan_s* p, const float* img, cudaStream_t s);
 cudaError_t launch_adjoint_ray2d_pc(const xrt_plan_s* p, const float* sino, float* acc_img, float* acc_imgT,
                                     cudaStream_t s);

@@ -499,6 +499,22 @@ def test_adjoint2d_pieces(cuda_ok, idx, monkeypatch):
     assert abs(lhs - rhs) <= 1e-5 * max(abs(lhs), abs(rhs))
 
 
+@pytest.mark.parametrize("idx", [1, 2])
+@pytest.mark.parametrize("pieces", [1, 2, 4, 8])
+def test_slice2d_adjoint_pieces(cuda_ok, idx, pieces, monkeypatch):
+    """The 2D slice adjoint in pieces (AUTO: 4) adds the same y l per unit as the unsplit slice
+    adjoint (the same fmaf crossing values; only the order of the fp32 reductions differs)."""
+    c = workloads.config(idx)
+    p = Plan(c, device=0)
+    y = workloads.make_sino_input(c, device="cuda:0")
+    monkeypatch.setenv("XRT_SLICE2D_PIECES", "0")
+    a = p.adjoint(y).cpu().numpy().ravel().astype(np.float64)
+    monkeypatch.setenv("XRT_SLICE2D_PIECES", str(pieces))
+    b = p.adjoint(y).cpu().numpy().ravel().astype(np.float64)
+    assert H.rel_l2(b, a) <= 1e-6
+    assert np.max(np.abs(b - a)) <= 1e-5 * np.max(np.abs(a))
+
+
 @pytest.mark.parametrize("full", [False, True])
 def test_flat_kernel_bitwise_general(cuda_ok, full, monkeypatch):
     """The flat-only forward instantiation (3D parallel beam without tilt) equals the general column

@@ -25,7 +25,11 @@ for cfg in (2, 1):
         out[k] = t(lambda: p.forward(x, out=s))
     y = workloads.make_sino_input(c, device="cuda:0")
     xo = torch.empty_like(x)
-    for k in ["0", "1", "2", "4", "8"]:   # adjoint: 0 = slice v2, else K pieces
+    for k in ["0", "4"]:   # adjoint: 0 = slice v2, else K free-running pieces
         os.environ["XRT_ADJ2D_PIECES"] = k
         out["adj" + k] = t(lambda: p.adjoint(y, out=xo))
+    os.environ["XRT_ADJ2D_PIECES"] = "0"
+    for k in ["0", "1", "2", "4", "8"]:   # slice adjoint: 0 = unsplit, else K lockstep pieces
+        os.environ["XRT_SLICE2D_PIECES"] = k
+        out["slice" + k] = t(lambda: p.adjoint(y, out=xo))
     print(json.dumps(out), flush=True)
