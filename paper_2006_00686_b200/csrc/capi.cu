@@ -536,6 +536,10 @@ xrt_status plan_create_impl(const xrt_geometry* g, int cuda_device, xrt_plan* ou
         // without tilt: the legacy kernel's flat walk, one 4-byte load per unit, is faster there)
         p->fd_forward = !std::getenv("XRT_FWD_LEGACY") && !(g->beam == XRT_PAR3D && g->tilt == 0.0);
         p->flat_z = g->beam == XRT_PAR3D && g->tilt == 0.0;
+        // circular cone symmetric in z (grid centred at z = 0, detector rows centred): the fd forward
+        // walks the upper rows and accumulates their mirror images from the same z state (k_fwd_fd<1, true>)
+        p->fd_mirror = p->fd_forward && g->beam == XRT_CONE && g->center[2] == 0.0 && D.off_v == 0.0 &&
+                       D.rows >= 2 && !std::getenv("XRT_NO_MIRROR");
         if (e == cudaSuccess && p->fd_forward) {
             const size_t fdb = 2 * sizeof(float2) * (size_t)(G.nxy * p->nzp);
             e = cudaMalloc(&p->d_work_fd, fdb);

@@ -1234,21 +1234,37 @@ __device__ __forceinline__ float2 ldg_f2(unsigned long long a) {
 #ifndef XRT_FD_UNROLL
 #define XRT_FD_UNROLL 0   // 0: by NP
 #endif
-template <int NP>
-__device__ __forceinline__ void fd_segments(unsigned seg, int total, FdPair (&P)[NP]) {
-    constexpr int kFdUnroll = XRT_FD_UNROLL > 0 ? XRT_FD_UNROLL : (NP == 1 ? 4 : 2);
+// mirrored ray (kM): the cell z -> -z of the walked ray's, address = ptr + K8 - 8 bits(kpf) (see
+// k_fwd_fd); one IMAD.WIDE with a negative multiplier
+__device__ __forceinline__ unsigned long long fd_addr_m(unsigned long long mptr, float kpf) {
+    return mptr + (unsigned long long)((long long)(int)__float_as_uint(kpf) * -8ll);
+}
+
+struct FdMirror {
+    float acc0a, acc0b, acc1a, acc1b;   // the mirrored rays of the pair's rays a / b
+};
+
+template <int NP, bool kM = false>
+__device__ __forceinline__ void fd_segments(unsigned seg, int total, FdPair (&P)[NP], FdMirror (&Mr)[NP],
+                                            unsigned long long K8) {
+    constexpr int kFdUnroll = XRT_FD_UNROLL > 0 ? XRT_FD_UNROLL : (NP == 1 && !kM ? 4 : 2);
     uint4 raw = lds128(seg);
-    float2 va[NP], vb[NP];
+    float2 va[NP], vb[NP], wa[NP], wb[NP];
 #pragma unroll
     for (int p = 0; p < NP; ++p) {
         va[p] = ldg_f2(fd_addr(seg_ptr(raw), P[p].kpf.x));
         vb[p] = ldg_f2(fd_addr(seg_ptr(raw), P[p].kpf.y));
+        if (kM) {
+            wa[p] = ldg_f2(fd_addr_m(seg_ptr(raw) + K8, P[p].kpf.x));
+            wb[p] = ldg_f2(fd_addr_m(seg_ptr(raw) + K8, P[p].kpf.y));
+        }
     }
 #pragma unroll kFdUnroll
     for (int s = 0; s < total; ++s) {
         const float qse = __uint_as_float(raw.z), qds = __uint_as_float(raw.w);
         const float2 se2 = make_float2(qse, qse);
         const uint4 nraw = lds128(seg + 16u * (unsigned)(s + 1));   // record `total` repeats the last one
+        const unsigned long long mptr = kM ? seg_ptr(nraw) + K8 : 0ull;
 #pragma unroll
         for (int p = 0; p < NP; ++p) {
             const float2 le = __fadd2_rn(se2, P[p].ntz);                 // sigma_e - tau
@@ -1259,12 +1275,25 @@ __device__ __forceinline__ void fd_segments(unsigned seg, int total, FdPair (&P)
             P[p].ntz = __ffma2_rn(cr, P[p].ndtz, P[p].ntz);
             const float2 na = ldg_f2(fd_addr(seg_ptr(nraw), P[p].kpf.x));
             const float2 nb = ldg_f2(fd_addr(seg_ptr(nraw), P[p].kpf.y));
+            float2 ma = make_float2(0.f, 0.f), mb = make_float2(0.f, 0.f);
+            if (kM) {
+                ma = ldg_f2(fd_addr_m(mptr, P[p].kpf.x));
+                mb = ldg_f2(fd_addr_m(mptr, P[p].kpf.y));
+            }
             P[p].acc0a = fmaf(va[p].x, qds, P[p].acc0a);                  // f_s d_sigma
             P[p].acc1a = fmaf(va[p].y, lma, P[p].acc1a);                  // (f_e - f_s) l_e
             P[p].acc0b = fmaf(vb[p].x, qds, P[p].acc0b);
             P[p].acc1b = fmaf(vb[p].y, lmb, P[p].acc1b);
             va[p] = na;
             vb[p] = nb;
+            if (kM) {
+                Mr[p].acc0a = fmaf(wa[p].x, qds, Mr[p].acc0a);
+                Mr[p].acc1a = fmaf(wa[p].y, lma, Mr[p].acc1a);
+                Mr[p].acc0b = fmaf(wb[p].x, qds, Mr[p].acc0b);
+                Mr[p].acc1b = fmaf(wb[p].y, lmb, Mr[p].acc1b);
+                wa[p] = ma;
+                wb[p] = mb;
+            }
         }
         raw = nraw;
     }
@@ -1283,11 +1312,22 @@ __device__ __forceinline__ void fd_segments(unsigned seg, int total, FdPair (&P)
 
 // CTA / warp / band layout as k_column (kOp 0): warp = one detector column, 2 NP rays per lane (rows
 // band 64 NP + 32 q + lane), band-major over (view, column group, tile) items.
-template <int NP>
+//
+// kM (mirror, circular cone symmetric in z: grid centred at z = 0, detector rows centred, H = 0):
+// the ray of row r' = rows - 1 - r is the mirror image of row r under z -> -z (v, tan(beta), z(sigma)
+// odd in v): it crosses the mirrored units (i, j, N_z - 1 - k) at the same sigma with the same lengths.
+// A lane walks rows r of the upper half (band b: rows 64 b + lane, + 32) and accumulates their
+// mirrors from the same z state: padded cell kp' = N_z - 1 + 2 pad - kp in the other half of the fd
+// column (the z direction flips), i.e. bits(kpf') = 2 kMagicBits + NzP + N_z - 1 + 2 pad - bits(kpf).
+// Each mirrored ray's units and C_up - C_low are those of its walked ray mirrored (the fp32 walk's
+// decisions, not an independent fp32 walk of row r'); the self-mirror middle row (odd rows) is walked
+// only.  Saves the z-state arithmetic of half the rays.
+template <int NP, bool kM>
 __global__ void __launch_bounds__(kFdWarps * 32, NP == 1 ? XRT_FD_MINB1 : XRT_FD_MINB)
 k_fwd_fd(const ViewRec* __restrict__ views, DetC dc, GridC g, const float2* __restrict__ fd,
          float* __restrict__ sino_out, int view0, const ColDesc* __restrict__ desc, ColumnLaunch L) {
     constexpr int R = 2 * NP;
+    const int rows_top = kM ? (dc.rows + 1) / 2 : dc.rows;
     __shared__ Seg s_seg[kFdWarps][2 * 32 + 1];   // + a copy of the chunk's last record (look-ahead)
     __shared__ float s_first[kFdWarps];
     const int lane = threadIdx.x & 31;
@@ -1335,6 +1375,7 @@ k_fwd_fd(const ViewRec* __restrict__ views, DetC dc, GridC g, const float2* __re
         nb = min(Pth.n_slices, __float2int_rd((hi - Pth.t0a) * ida) + 3);
     }
     FdPair P[NP];
+    FdMirror Mr[NP];
     bool any_live = false;
 #pragma unroll
     for (int p = 0; p < NP; ++p) {
@@ -1343,8 +1384,12 @@ k_fwd_fd(const ViewRec* __restrict__ views, DetC dc, GridC g, const float2* __re
         ray_z(V, dc, g, Pth, ca, ra, L.pad, Za);
         ray_z(V, dc, g, Pth, ca, rb, L.pad, Zb);
         fd_init(P[p], Za, Zb, L.nzp);
-        any_live |= Za.active | Zb.active;
+        Mr[p].acc0a = Mr[p].acc0b = Mr[p].acc1a = Mr[p].acc1b = 0.f;
+        any_live |= (Za.active && ra < rows_top) | (Zb.active && rb < rows_top);
     }
+    // mirrored address offset: 8 (2 kMagicBits + NzP + N_z - 1 + 2 pad)
+    const unsigned long long K8 =
+        8ull * (2ull * kMagicBits + (unsigned long long)L.nzp + (unsigned long long)(g.n[2] - 1 + 2 * L.pad));
     if (!__any_sync(0xffffffffu, any_live)) return;
     Seg* seg = s_seg[warp];
     const unsigned seg_s = (unsigned)__cvta_generic_to_shared(seg);
@@ -1394,7 +1439,7 @@ k_fwd_fd(const ViewRec* __restrict__ views, DetC dc, GridC g, const float2* __re
             }
 #pragma unroll
             for (int p = 0; p < NP; ++p) fd_anchor(P[p], sc);
-            fd_segments<NP>(seg_s, total, P);
+            fd_segments<NP, kM>(seg_s, total, P, Mr, K8);
         }
         __syncwarp();  // the next chunk overwrites the segments
     }
@@ -1402,12 +1447,22 @@ k_fwd_fd(const ViewRec* __restrict__ views, DetC dc, GridC g, const float2* __re
     for (int q = 0; q < R; ++q) {
         const FdPair& Q = P[q >> 1];
         const int r = (band * R + q) * 32 + lane;
-        if (r >= dc.rows) continue;                // ray_z's `active` (the column hits the square)
+        if (r >= rows_top) continue;               // ray_z's `active` (the column hits the square)
         const float a = (q & 1) ? (Q.acc0b + Q.acc1b) * fd_scale(Q.ndtz.y, (float)g.d[2])
                                 : (Q.acc0a + Q.acc1a) * fd_scale(Q.ndtz.x, (float)g.d[2]);
         const int64_t m = ((int64_t)v * dc.rows + r) * dc.cols + c;
         if (tiled) { if (a != 0.f) red_sino(sino_out + m, a, l2_evict_first()); }
         else __stcs(sino_out + m, a);
+        if constexpr (kM) {
+            const int rm = dc.rows - 1 - r;
+            if (rm == r) continue;                 // the self-mirror middle row
+            const FdMirror& M = Mr[q >> 1];
+            const float sc = (q & 1) ? fd_scale(Q.ndtz.y, (float)g.d[2]) : fd_scale(Q.ndtz.x, (float)g.d[2]);
+            const float b = ((q & 1) ? (M.acc0b + M.acc1b) : (M.acc0a + M.acc1a)) * sc;
+            const int64_t mm = ((int64_t)v * dc.rows + rm) * dc.cols + c;
+            if (tiled) { if (b != 0.f) red_sino(sino_out + mm, b, l2_evict_first()); }
+            else __stcs(sino_out + mm, b);
+        }
     }
 }
 
@@ -1815,12 +1870,18 @@ static cudaError_t launch_fd(const xrt_plan_s* p, const float2* fd, float* sino,
     if (cudaError_t e = set_dbg_range(fd, 16ull * (size_t)p->grid.nxy * (size_t)p->nzp, s); e != cudaSuccess) return e;
     const ColDesc* d = (const ColDesc*)p->d_coldesc;
     if (p->col_np == 1)
-        k_fwd_fd<1><<<nblk, kFdWarps * 32, 0, s>>>(p->d_views, p->det, p->grid, fd, sino, 0, d, L);
+        k_fwd_fd<1, false><<<nblk, kFdWarps * 32, 0, s>>>(p->d_views, p->det, p->grid, fd, sino, 0, d, L);
     else if (p->col_np == 2)
-        k_fwd_fd<2><<<nblk, kFdWarps * 32, 0, s>>>(p->d_views, p->det, p->grid, fd, sino, 0, d, L);
+        k_fwd_fd<2, false><<<nblk, kFdWarps * 32, 0, s>>>(p->d_views, p->det, p->grid, fd, sino, 0, d, L);
     else
         return cudaErrorInvalidValue;
     return cudaGetLastError();
+}
+
+// mirrored forward (k_fwd_fd<1, true>): read per launch, XRT_FWD_MIRROR=0 disables (A/B)
+static bool fd_mirror_on(const xrt_plan_s* p) {
+    const char* e = std::getenv("XRT_FWD_MIRROR");
+    return p->fd_mirror && !(e && std::atoi(e) == 0);
 }
 
 // all views and bands [b0, b1) (rows b * 64 NP ...); sinogram rows of those bands pre-zeroed
@@ -1845,6 +1906,17 @@ cudaError_t launch_forward_fd_bands(const xrt_plan_s* p, const float2* fd, float
     cudaError_t e = cudaMemset2DAsync(sino + (int64_t)r0 * p->det.cols, pitch, 0,
                                       sizeof(float) * (size_t)(r1 - r0) * p->det.cols, (size_t)p->n_views, s);
     if (e != cudaSuccess) return e;
+    if (fd_mirror_on(p) && r0 == 0 && r1 == p->det.rows) {
+        // all rows: bands of 64 upper-half rows, each with its mirrored rows (same L2 slab budget:
+        // two 64-row slabs per band instead of one 128-row slab)
+        const int nbm = ((p->det.rows + 1) / 2 + 63) / 64;
+        L.band0 = 0;
+        if (cudaError_t e2 = set_dbg_range(fd, 16ull * (size_t)p->grid.nxy * (size_t)p->nzp, s); e2 != cudaSuccess)
+            return e2;
+        k_fwd_fd<1, true><<<L.n_items * nbm, kFdWarps * 32, 0, s>>>(p->d_views, p->det, p->grid, fd, sino, 0,
+                                                                   (const ColDesc*)p->d_coldesc, L);
+        return cudaGetLastError();
+    }
     L.band0 = b0;
     return launch_fd(p, fd, sino, L, L.n_items * (b1 - b0), s);
 }

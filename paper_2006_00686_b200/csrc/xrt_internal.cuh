@@ -227,6 +227,7 @@ struct xrt_plan_s {
     float2* d_work_fd = nullptr;       // forward (COLUMN): per cell 2 x NzP (f, f[k+-1] - f[k]) cells
     bool fd_forward = true;            // AUTO forward on the (f, delta f) volume (XRT_FWD_LEGACY=1: k_column)
     bool flat_z = false;               // every ray keeps one z cell (par3d, tilt 0): flat column kernels
+    bool fd_mirror = false;            // circular cone symmetric in z: the fd forward walks the upper rows and their mirrors
     int64_t zpad = 0, nzp = 0;         // z padding per side and padded column length
     // xy tiling of the column kernels (L2 residency), per operator: [0] forward, [1] adjoint
     struct ColTiling {

@@ -515,6 +515,28 @@ def test_slice2d_adjoint_pieces(cuda_ok, idx, pieces, monkeypatch):
     assert np.max(np.abs(b - a)) <= 1e-5 * np.max(np.abs(a))
 
 
+@pytest.mark.parametrize("case", ["small_odd", "small_even", "full"])
+def test_fwd_mirror(cuda_ok, case, monkeypatch):
+    """Circular cone symmetric in z: the fd forward walks the upper rows and accumulates their mirror
+    images (k_fwd_fd<1, true>, AUTO).  Against the plain fd walk of every row (XRT_FWD_MIRROR=0) to
+    fp32 rounding (1e-5 of max |sino|: a mirrored ray's crossings are its walked ray's fp32 values,
+    not its own), and on the small geometries (odd rows: the self-mirror middle row lies in the
+    z = 0 grid plane; even rows) against the fp64 oracle on every ray."""
+    if case == "full":
+        c = workloads.config(4)
+    else:
+        c = workloads.scaled(4, n=(48, 48, 48), n_views=10, det_cols=97, det_rows=71 if case == "small_odd" else 72)
+    p = Plan(c, device=0)
+    img = _image(c)
+    a = p.forward(img).cpu().numpy().ravel().astype(np.float64)
+    monkeypatch.setenv("XRT_FWD_MIRROR", "0")
+    b = p.forward(img).cpu().numpy().ravel().astype(np.float64)
+    assert np.max(np.abs(a - b)) <= 1e-5 * np.max(np.abs(b))
+    if case != "full":
+        ref = H.oracle_forward(c, img.cpu(), H.ray_ids_all(c))
+        assert H.fwd_err(a, ref) <= H.FWD_TOL
+
+
 @pytest.mark.parametrize("full", [False, True])
 def test_flat_kernel_bitwise_general(cuda_ok, full, monkeypatch):
     """The flat-only forward instantiation (3D parallel beam without tilt) equals the general column
