@@ -653,6 +653,22 @@ xrt_status plan_create_impl(const xrt_geometry* g, int cuda_device, xrt_plan* ou
                 p->fwd_band_k[2 * b] = std::max<int64_t>(0, (int64_t)std::floor((G.z_hi - zhi) / G.d[2]) - 2);
                 p->fwd_band_k[2 * b + 1] = std::min<int64_t>(G.n[2], (int64_t)std::floor((G.z_hi - zlo) / G.d[2]) + 3);
             }
+            if (p->fd_mirror) {
+                const int64_t rows = g->det_rows, top = (rows + 1) / 2;
+                const int nbm = xrt::fd_mirror_bands(p);
+                p->fwdm_band_k.assign(4 * (size_t)nbm, 0);
+                for (int b = 0; b < nbm; ++b) {
+                    const int64_t r0 = 64ll * b, r1 = std::min<int64_t>(top, 64ll * (b + 1));
+                    const int64_t ra[2] = {r0, rows - r1}, rz[2] = {r1 - 1, rows - 1 - r0};
+                    for (int h = 0; h < 2; ++h) {
+                        double zlo, zhi;
+                        band_z_range(g, G, ra[h], rz[h], zlo, zhi);
+                        p->fwdm_band_k[4 * b + 2 * h] = std::max<int64_t>(0, (int64_t)std::floor((G.z_hi - zhi) / G.d[2]) - 2);
+                        p->fwdm_band_k[4 * b + 2 * h + 1] =
+                            std::min<int64_t>(G.n[2], (int64_t)std::floor((G.z_hi - zlo) / G.d[2]) + 3);
+                    }
+                }
+            }
         }
         // staged adjoint (xrt_adjoint_stages): band b of the adjoint touches image rows
         // [klo_b, khi_b] (conservative, 2-cell margin); rows no later band touches are final after b.
@@ -997,6 +1013,107 @@ xrt_status xrt_forward_host(xrt_plan p, const float* img_host, float* sino_host,
     xrt_status st = alloc_stage(p);
     if (st != XRT_OK) return st;
     cudaStream_t s = (cudaStream_t)cuda_stream, a = (cudaStream_t)p->aux_stream;
+    if (resolve(p, XRT_OP_FORWARD) == XRT_ALGO_COLUMN && p->dim == 3 && p->fd_forward && xrt::fd_mirror_active(p) &&
+        !p->fwdm_band_k.empty()) {
+        // z-mirror fd forward: mirror band b needs image rows at both ends of z, so the image goes up
+        // from both ends towards the middle (two fronts, alternating chunks on the aux stream), each
+        // front building its fd rows as soon as their neighbour rows are present; band b waits for
+        // the chunk after which both of its row ranges are built; its upper and mirrored sinogram
+        // rows go down on a second aux stream while later bands compute
+        const int nz = p->grid.n[2];
+        const int64_t nxy = p->grid.nxy;
+        const int nbm = xrt::fd_mirror_bands(p), rows = p->det.rows, top = (rows + 1) / 2;
+        const int CH = std::max(32, (nz + 15) / 16);
+        cudaStream_t d = (cudaStream_t)p->aux_stream2;
+        cudaStream_t cs[2] = {s, (cudaStream_t)p->aux_stream3};
+        struct Step { int lo, hi; bool asc; };
+        std::vector<Step> steps;
+        for (int alo = 0, dhi = nz; alo < dhi;) {
+            const int ahi = std::min(dhi, alo + CH);
+            steps.push_back({alo, ahi, true});
+            alo = ahi;
+            if (alo >= dhi) break;
+            const int dlo = std::max(alo, dhi - CH);
+            steps.push_back({dlo, dhi, false});
+            dhi = dlo;
+        }
+        const int nst = (int)steps.size();
+        std::vector<cudaEvent_t> evc((size_t)nst), evb((size_t)nbm);
+        for (auto& x : evc) XRT_CUDA(cudaEventCreateWithFlags(&x, cudaEventDisableTiming));
+        for (auto& x : evb) XRT_CUDA(cudaEventCreateWithFlags(&x, cudaEventDisableTiming));
+        cudaEvent_t ev0, ev_end;
+        XRT_CUDA(cudaEventCreateWithFlags(&ev0, cudaEventDisableTiming));
+        XRT_CUDA(cudaEventCreateWithFlags(&ev_end, cudaEventDisableTiming));
+        XRT_CUDA(cudaEventRecord(ev0, s));
+        XRT_CUDA(cudaStreamWaitEvent(a, ev0, 0));
+        XRT_CUDA(cudaStreamWaitEvent(cs[1], ev0, 0));
+        cudaError_t e = cudaSuccess;
+        int built_hi = -1, built_lo = nz + 1;     // fd rows [-1, built_hi) and [built_lo, nz] built
+        std::vector<int> done_hi((size_t)nst), done_lo((size_t)nst);
+        for (int i = 0; i < nst && e == cudaSuccess; ++i) {
+            const Step& S = steps[i];
+            e = cudaMemcpyAsync(p->d_stage_img + S.lo * nxy, img_host + S.lo * nxy,
+                                sizeof(float) * (size_t)((S.hi - S.lo) * nxy), cudaMemcpyHostToDevice, a);
+            if (i == nst - 1) {                   // the fronts met: every remaining row has its neighbours
+                if (e == cudaSuccess) e = xrt::launch_to_fd_rows(p, p->d_stage_img, p->d_work_fd, built_hi, built_lo, a);
+                built_hi = nz + 1; built_lo = -1;
+            } else if (S.asc) {
+                const int kb = S.hi - 1;          // row hi - 1 waits for its upper neighbour
+                if (e == cudaSuccess) e = xrt::launch_to_fd_rows(p, p->d_stage_img, p->d_work_fd, built_hi, kb, a);
+                built_hi = std::max(built_hi, kb);
+            } else {
+                const int ka = S.lo + 1;          // row lo waits for its lower neighbour
+                if (e == cudaSuccess) e = xrt::launch_to_fd_rows(p, p->d_stage_img, p->d_work_fd, ka, built_lo, a);
+                built_lo = std::min(built_lo, ka);
+            }
+            p->launches += 1;
+            done_hi[i] = built_hi;
+            done_lo[i] = built_lo;
+            if (e == cudaSuccess) e = cudaEventRecord(evc[i], a);
+        }
+        const size_t pitch = sizeof(float) * (size_t)p->det.per_view;
+        for (int b = 0; b < nbm && e == cudaSuccess; ++b) {
+            int need = nst - 1;
+            for (int i = 0; i < nst; ++i) {
+                bool ok = true;
+                for (int h = 0; h < 2; ++h) {
+                    const int x0 = (int)p->fwdm_band_k[4 * b + 2 * h] - 1, x1 = (int)p->fwdm_band_k[4 * b + 2 * h + 1] + 1;
+                    ok = ok && (x1 <= done_hi[i] || x0 >= done_lo[i] || done_hi[i] >= done_lo[i]);
+                }
+                if (ok) { need = i; break; }
+            }
+            cudaStream_t c = cs[b & 1];
+            e = cudaStreamWaitEvent(c, evc[need], 0);
+            if (e == cudaSuccess) e = xrt::launch_forward_fd_mirror_bands(p, p->d_work_fd, p->d_stage_sino, b, b + 1, c);
+            p->launches += 1;
+            if (e == cudaSuccess) e = cudaEventRecord(evb[b], c);
+            if (e == cudaSuccess) e = cudaStreamWaitEvent(d, evb[b], 0);
+            const int r0 = 64 * b, r1 = std::min(top, 64 * (b + 1));
+            const int q0[2] = {r0, rows - r1};
+            for (int h = 0; h < 2 && e == cudaSuccess; ++h)
+                e = cudaMemcpy2DAsync(sino_host + (int64_t)q0[h] * p->det.cols, pitch,
+                                      p->d_stage_sino + (int64_t)q0[h] * p->det.cols, pitch,
+                                      sizeof(float) * (size_t)(r1 - r0) * p->det.cols, (size_t)p->n_views,
+                                      cudaMemcpyDeviceToHost, d);
+        }
+        if (e == cudaSuccess) e = cudaStreamWaitEvent(s, evc[nst - 1], 0);   // the stage buffers are reused
+        if (e == cudaSuccess) e = cudaEventRecord(ev_end, cs[1]);
+        if (e == cudaSuccess) e = cudaStreamWaitEvent(s, ev_end, 0);
+        cudaError_t e1 = cudaStreamSynchronize(a);
+        cudaError_t e2 = cudaStreamSynchronize(s);
+        cudaError_t e3 = cudaStreamSynchronize(d);
+        cudaError_t e4 = cudaStreamSynchronize(cs[1]);
+        if (e3 == cudaSuccess) e3 = e4;
+        for (auto& x : evc) cudaEventDestroy(x);
+        for (auto& x : evb) cudaEventDestroy(x);
+        cudaEventDestroy(ev0);
+        cudaEventDestroy(ev_end);
+        if (e != cudaSuccess) return cuda_fail(e, "forward_host mirrored pipeline");
+        if (e1 != cudaSuccess) return cuda_fail(e1, "forward_host sync");
+        if (e2 != cudaSuccess) return cuda_fail(e2, "forward_host sync");
+        if (e3 != cudaSuccess) return cuda_fail(e3, "forward_host sync");
+        return XRT_OK;
+    }
     if (resolve(p, XRT_OP_FORWARD) == XRT_ALGO_COLUMN && p->dim == 3 && p->fd_forward && !p->fwd_band_k.empty()) {
         // fd column forward: the image goes up in z chunks on the aux stream, each chunk's fd rows
         // built there as soon as its neighbour rows are present; band b waits only for the rows

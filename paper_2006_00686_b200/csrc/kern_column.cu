@@ -65,7 +65,7 @@ constexpr int kWarps = XRT_COL_WARPS;  // warps per CTA = adjacent detector colu
 #define XRT_FD_COLS 4
 #endif
 #ifndef XRT_FD_VIEWS
-#define XRT_FD_VIEWS 2
+#define XRT_FD_VIEWS 1   // with the z-mirror forward (cfg 4): 4 x 1 100.4 ms vs 4 x 2 104.2, 4 x 4 106.7, 8 x 1 102.6
 #endif
 constexpr int kFdCols = XRT_FD_COLS, kFdViews = XRT_FD_VIEWS, kFdWarps = kFdCols * kFdViews;
 #ifndef XRT_KPASSES
@@ -1878,6 +1878,7 @@ static cudaError_t launch_fd(const xrt_plan_s* p, const float2* fd, float* sino,
     return cudaGetLastError();
 }
 
+int fd_mirror_bands(const xrt_plan_s* p);
 // mirrored forward (k_fwd_fd<1, true>): read per launch, XRT_FWD_MIRROR=0 disables (A/B)
 static bool fd_mirror_on(const xrt_plan_s* p) {
     const char* e = std::getenv("XRT_FWD_MIRROR");
@@ -1909,16 +1910,51 @@ cudaError_t launch_forward_fd_bands(const xrt_plan_s* p, const float2* fd, float
     if (fd_mirror_on(p) && r0 == 0 && r1 == p->det.rows) {
         // all rows: bands of 64 upper-half rows, each with its mirrored rows (same L2 slab budget:
         // two 64-row slabs per band instead of one 128-row slab)
-        const int nbm = ((p->det.rows + 1) / 2 + 63) / 64;
         L.band0 = 0;
         if (cudaError_t e2 = set_dbg_range(fd, 16ull * (size_t)p->grid.nxy * (size_t)p->nzp, s); e2 != cudaSuccess)
             return e2;
-        k_fwd_fd<1, true><<<L.n_items * nbm, kFdWarps * 32, 0, s>>>(p->d_views, p->det, p->grid, fd, sino, 0,
-                                                                   (const ColDesc*)p->d_coldesc, L);
+        k_fwd_fd<1, true><<<L.n_items * fd_mirror_bands(p), kFdWarps * 32, 0, s>>>(
+            p->d_views, p->det, p->grid, fd, sino, 0, (const ColDesc*)p->d_coldesc, L);
         return cudaGetLastError();
     }
     L.band0 = b0;
     return launch_fd(p, fd, sino, L, L.n_items * (b1 - b0), s);
+}
+
+bool fd_mirror_active(const xrt_plan_s* p) { return fd_mirror_on(p); }
+int fd_mirror_bands(const xrt_plan_s* p) { return ((p->det.rows + 1) / 2 + 63) / 64; }
+
+// mirror bands [b0, b1) (upper rows [64 b0, 64 b1) and their mirrors; those sinogram rows zeroed first)
+cudaError_t launch_forward_fd_mirror_bands(const xrt_plan_s* p, const float2* fd, float* sino, int b0, int b1,
+                                           cudaStream_t s) {
+    if (b1 <= b0) return cudaSuccess;
+    int nblk = 0;
+    ColumnLaunch L = make_launch(p, 0, p->n_views, nblk, false);
+    L.n_cgroups = (p->det.cols + kFdCols - 1) / kFdCols;
+    if (p->ct_fd.d_items) {
+        L.tile = p->ct_fd.tile;
+        L.n_tx = p->ct_fd.n_tx;
+        L.items = (const uint2*)p->ct_fd.d_items;
+        L.n_items = (int)p->ct_fd.n_items;
+    } else {
+        L.items = nullptr;
+        L.n_items = (int)((p->n_views + kFdViews - 1) / kFdViews) * L.n_cgroups;
+    }
+    const int rows = p->det.rows, top = (rows + 1) / 2;
+    const int r0 = 64 * b0, r1 = std::min(top, 64 * b1);
+    if (r1 <= r0) return cudaSuccess;
+    const size_t pitch = sizeof(float) * (size_t)p->det.per_view;
+    cudaError_t e = cudaMemset2DAsync(sino + (int64_t)r0 * p->det.cols, pitch, 0,
+                                      sizeof(float) * (size_t)(r1 - r0) * p->det.cols, (size_t)p->n_views, s);
+    if (e == cudaSuccess)
+        e = cudaMemset2DAsync(sino + (int64_t)(rows - r1) * p->det.cols, pitch, 0,
+                              sizeof(float) * (size_t)(r1 - r0) * p->det.cols, (size_t)p->n_views, s);
+    if (e != cudaSuccess) return e;
+    if (cudaError_t e2 = set_dbg_range(fd, 16ull * (size_t)p->grid.nxy * (size_t)p->nzp, s); e2 != cudaSuccess) return e2;
+    L.band0 = b0;
+    k_fwd_fd<1, true><<<L.n_items * (b1 - b0), kFdWarps * 32, 0, s>>>(p->d_views, p->det, p->grid, fd, sino, 0,
+                                                                     (const ColDesc*)p->d_coldesc, L);
+    return cudaGetLastError();
 }
 
 int fd_view_block() { return kFdViews; }

@@ -275,6 +275,7 @@ struct xrt_plan_s {
     bool column_ok = false;            // geometry admits the column-shared kernels
     std::vector<int64_t> adj_stage_k;  // staged adjoint: per band b, image rows [k0, k1) final after b
     std::vector<int64_t> fwd_band_k;   // forward bands: per band b, the image rows [k0, k1) its rays reach
+    std::vector<int64_t> fwdm_band_k;  // z-mirror forward bands: per band b, [k0, k1) of its upper rows, then of their mirrors
     int64_t launches = 0;
 };
 
@@ -359,6 +360,10 @@ cudaError_t launch_to_fd_rows(const xrt_plan_s* p, const float* img, float2* fd,
 cudaError_t launch_forward_fd_bands(const xrt_plan_s* p, const float2* fd, float* sino, int b0, int b1,
                                     cudaStream_t s);
 int fd_view_block();                 // views per CTA of the fd forward (kFdViews)
+bool fd_mirror_active(const xrt_plan_s* p);
+int fd_mirror_bands(const xrt_plan_s* p);
+cudaError_t launch_forward_fd_mirror_bands(const xrt_plan_s* p, const float2* fd, float* sino, int b0, int b1,
+                                           cudaStream_t s);
 cudaError_t launch_adjoint_column_band_part(const xrt_plan_s* p, const float* sino, float* vol_zfast, int b,
                                             int part, cudaStream_t s);
 cudaError_t launch_forward_fd_band_part(const xrt_plan_s* p, const float2* fd, float* sino, int b, int part,
