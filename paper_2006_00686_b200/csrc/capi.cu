@@ -537,7 +537,7 @@ xrt_status plan_create_impl(const xrt_geometry* g, int cuda_device, xrt_plan* ou
         p->fd_forward = !std::getenv("XRT_FWD_LEGACY") && !(g->beam == XRT_PAR3D && g->tilt == 0.0);
         p->flat_z = g->beam == XRT_PAR3D && g->tilt == 0.0;
         // circular cone symmetric in z (grid centred at z = 0, detector rows centred): the fd forward
-        // walks the upper rows and accumulates their mirror images from the same z state (k_fwd_fd<1, true>)
+        // walks the upper rows and accumulates their mirror images from the same z state (k_fwd_fd<NP, true>)
         p->fd_mirror = p->fd_forward && g->beam == XRT_CONE && g->center[2] == 0.0 && D.off_v == 0.0 &&
                        D.rows >= 2 && !std::getenv("XRT_NO_MIRROR");
         if (e == cudaSuccess && p->fd_forward) {
@@ -658,7 +658,8 @@ xrt_status plan_create_impl(const xrt_geometry* g, int cuda_device, xrt_plan* ou
                 const int nbm = xrt::fd_mirror_bands(p);
                 p->fwdm_band_k.assign(4 * (size_t)nbm, 0);
                 for (int b = 0; b < nbm; ++b) {
-                    const int64_t r0 = 64ll * b, r1 = std::min<int64_t>(top, 64ll * (b + 1));
+                    const int64_t mr = xrt::fd_mirror_band_rows();
+                    const int64_t r0 = mr * b, r1 = std::min<int64_t>(top, mr * (b + 1));
                     const int64_t ra[2] = {r0, rows - r1}, rz[2] = {r1 - 1, rows - 1 - r0};
                     for (int h = 0; h < 2; ++h) {
                         double zlo, zhi;
@@ -1088,7 +1089,8 @@ xrt_status xrt_forward_host(xrt_plan p, const float* img_host, float* sino_host,
             p->launches += 1;
             if (e == cudaSuccess) e = cudaEventRecord(evb[b], c);
             if (e == cudaSuccess) e = cudaStreamWaitEvent(d, evb[b], 0);
-            const int r0 = 64 * b, r1 = std::min(top, 64 * (b + 1));
+            const int mr = xrt::fd_mirror_band_rows();
+            const int r0 = mr * b, r1 = std::min(top, mr * (b + 1));
             const int q0[2] = {r0, rows - r1};
             for (int h = 0; h < 2 && e == cudaSuccess; ++h)
                 e = cudaMemcpy2DAsync(sino_host + (int64_t)q0[h] * p->det.cols, pitch,

@@ -1879,7 +1879,11 @@ static cudaError_t launch_fd(const xrt_plan_s* p, const float2* fd, float* sino,
 }
 
 int fd_mirror_bands(const xrt_plan_s* p);
-// mirrored forward (k_fwd_fd<1, true>): read per launch, XRT_FWD_MIRROR=0 disables (A/B)
+#ifndef XRT_FD_MIRROR_NP
+#define XRT_FD_MIRROR_NP 1   // walked ray pairs per lane of the z-mirror forward (rows per band 64 NP)
+#endif
+constexpr int kMirNP = XRT_FD_MIRROR_NP;
+// mirrored forward (k_fwd_fd<kMirNP, true>): read per launch, XRT_FWD_MIRROR=0 disables (A/B)
 static bool fd_mirror_on(const xrt_plan_s* p) {
     const char* e = std::getenv("XRT_FWD_MIRROR");
     return p->fd_mirror && !(e && std::atoi(e) == 0);
@@ -1913,7 +1917,7 @@ cudaError_t launch_forward_fd_bands(const xrt_plan_s* p, const float2* fd, float
         L.band0 = 0;
         if (cudaError_t e2 = set_dbg_range(fd, 16ull * (size_t)p->grid.nxy * (size_t)p->nzp, s); e2 != cudaSuccess)
             return e2;
-        k_fwd_fd<1, true><<<L.n_items * fd_mirror_bands(p), kFdWarps * 32, 0, s>>>(
+        k_fwd_fd<kMirNP, true><<<L.n_items * fd_mirror_bands(p), kFdWarps * 32, 0, s>>>(
             p->d_views, p->det, p->grid, fd, sino, 0, (const ColDesc*)p->d_coldesc, L);
         return cudaGetLastError();
     }
@@ -1922,7 +1926,8 @@ cudaError_t launch_forward_fd_bands(const xrt_plan_s* p, const float2* fd, float
 }
 
 bool fd_mirror_active(const xrt_plan_s* p) { return fd_mirror_on(p); }
-int fd_mirror_bands(const xrt_plan_s* p) { return ((p->det.rows + 1) / 2 + 63) / 64; }
+int fd_mirror_bands(const xrt_plan_s* p) { return ((p->det.rows + 1) / 2 + 64 * kMirNP - 1) / (64 * kMirNP); }
+int fd_mirror_band_rows() { return 64 * kMirNP; }
 
 // mirror bands [b0, b1) (upper rows [64 b0, 64 b1) and their mirrors; those sinogram rows zeroed first)
 cudaError_t launch_forward_fd_mirror_bands(const xrt_plan_s* p, const float2* fd, float* sino, int b0, int b1,
@@ -1941,7 +1946,7 @@ cudaError_t launch_forward_fd_mirror_bands(const xrt_plan_s* p, const float2* fd
         L.n_items = (int)((p->n_views + kFdViews - 1) / kFdViews) * L.n_cgroups;
     }
     const int rows = p->det.rows, top = (rows + 1) / 2;
-    const int r0 = 64 * b0, r1 = std::min(top, 64 * b1);
+    const int r0 = 64 * kMirNP * b0, r1 = std::min(top, 64 * kMirNP * b1);
     if (r1 <= r0) return cudaSuccess;
     const size_t pitch = sizeof(float) * (size_t)p->det.per_view;
     cudaError_t e = cudaMemset2DAsync(sino + (int64_t)r0 * p->det.cols, pitch, 0,
@@ -1952,7 +1957,7 @@ cudaError_t launch_forward_fd_mirror_bands(const xrt_plan_s* p, const float2* fd
     if (e != cudaSuccess) return e;
     if (cudaError_t e2 = set_dbg_range(fd, 16ull * (size_t)p->grid.nxy * (size_t)p->nzp, s); e2 != cudaSuccess) return e2;
     L.band0 = b0;
-    k_fwd_fd<1, true><<<L.n_items * (b1 - b0), kFdWarps * 32, 0, s>>>(p->d_views, p->det, p->grid, fd, sino, 0,
+    k_fwd_fd<kMirNP, true><<<L.n_items * (b1 - b0), kFdWarps * 32, 0, s>>>(p->d_views, p->det, p->grid, fd, sino, 0,
                                                                      (const ColDesc*)p->d_coldesc, L);
     return cudaGetLastError();
 }

@@ -362,6 +362,7 @@ cudaError_t launch_forward_fd_bands(const xrt_plan_s* p, const float2* fd, float
 int fd_view_block();                 // views per CTA of the fd forward (kFdViews)
 bool fd_mirror_active(const xrt_plan_s* p);
 int fd_mirror_bands(const xrt_plan_s* p);
+int fd_mirror_band_rows();           // upper-half rows per z-mirror band
 cudaError_t launch_forward_fd_mirror_bands(const xrt_plan_s* p, const float2* fd, float* sino, int b0, int b1,
                                            cudaStream_t s);
 cudaError_t launch_adjoint_column_band_part(const xrt_plan_s* p, const float* sino, float* vol_zfast, int b,
