@@ -410,6 +410,7 @@ struct ColumnLaunch {
     int band0;            // first band of this launch (bands band0 .. band0 + grid / n_items - 1)
     int tile, n_tx;       // tile side in cells, tiles along x
     int nzp, pad;
+    unsigned eight;       // 8 as a launch value: a cell address by IMAD.WIDE.U32 (ptxas turns a literal 8 into LEA pairs)
 };
 
 // z state of two rays of one lane (rows lane + 32 q), packed so the per-segment arithmetic of the
@@ -1234,10 +1235,27 @@ __device__ __forceinline__ float2 ldg_f2(unsigned long long a) {
 #ifndef XRT_FD_UNROLL
 #define XRT_FD_UNROLL 0   // 0: by NP
 #endif
-// mirrored ray (kM): the cell z -> -z of the walked ray's, address = ptr + K8 - 8 bits(kpf) (see
-// k_fwd_fd); one IMAD.WIDE with a negative multiplier
-__device__ __forceinline__ unsigned long long fd_addr_m(unsigned long long mptr, float kpf) {
-    return mptr + (unsigned long long)((long long)(int)__float_as_uint(kpf) * -8ll);
+// mirrored ray (kM): the cell z -> -z of the walked ray's, bits(kpf') = Kb - bits(kpf) (see k_fwd_fd),
+// address = ptr + 8 bits(kpf'): IADD3 + IMAD.WIDE.U32
+#ifndef XRT_FD_ADDR_MODE
+#define XRT_FD_ADDR_MODE 0   // z-mirror forward addresses (cfg 4: 94.7 / 100.3 / 111.2 ms): 0 walked LEA pairs / mirrored IADD3 + LEA pair,
+#endif                       // 1 walked LEA pairs / mirrored IADD3 + IMAD.WIDE.U32, 2 both IMAD.WIDE.U32
+__device__ __forceinline__ unsigned long long fd_addr_m(unsigned long long ptr, float kpf, unsigned Kb,
+                                                        unsigned eight) {
+    unsigned long long a;
+    if (XRT_FD_ADDR_MODE == 0)
+        asm("mad.wide.u32 %0, %1, 8, %2;" : "=l"(a) : "r"(Kb - __float_as_uint(kpf)), "l"(ptr));
+    else
+        asm("mad.wide.u32 %0, %1, %2, %3;" : "=l"(a) : "r"(Kb - __float_as_uint(kpf)), "r"(eight), "l"(ptr));
+    return a;
+}
+__device__ __forceinline__ unsigned long long fd_addr_w(unsigned long long ptr, float kpf, unsigned eight) {
+    if (XRT_FD_ADDR_MODE == 2) {
+        unsigned long long a;
+        asm("mad.wide.u32 %0, %1, %2, %3;" : "=l"(a) : "r"(__float_as_uint(kpf)), "r"(eight), "l"(ptr));
+        return a;
+    }
+    return fd_addr(ptr, kpf);
 }
 
 struct FdMirror {
@@ -1246,17 +1264,17 @@ struct FdMirror {
 
 template <int NP, bool kM = false>
 __device__ __forceinline__ void fd_segments(unsigned seg, int total, FdPair (&P)[NP], FdMirror (&Mr)[NP],
-                                            unsigned long long K8) {
+                                            unsigned Kb, unsigned eight) {
     constexpr int kFdUnroll = XRT_FD_UNROLL > 0 ? XRT_FD_UNROLL : (NP == 1 && !kM ? 4 : 2);
     uint4 raw = lds128(seg);
     float2 va[NP], vb[NP], wa[NP], wb[NP];
 #pragma unroll
     for (int p = 0; p < NP; ++p) {
-        va[p] = ldg_f2(fd_addr(seg_ptr(raw), P[p].kpf.x));
-        vb[p] = ldg_f2(fd_addr(seg_ptr(raw), P[p].kpf.y));
+        va[p] = ldg_f2(kM ? fd_addr_w(seg_ptr(raw), P[p].kpf.x, eight) : fd_addr(seg_ptr(raw), P[p].kpf.x));
+        vb[p] = ldg_f2(kM ? fd_addr_w(seg_ptr(raw), P[p].kpf.y, eight) : fd_addr(seg_ptr(raw), P[p].kpf.y));
         if (kM) {
-            wa[p] = ldg_f2(fd_addr_m(seg_ptr(raw) + K8, P[p].kpf.x));
-            wb[p] = ldg_f2(fd_addr_m(seg_ptr(raw) + K8, P[p].kpf.y));
+            wa[p] = ldg_f2(fd_addr_m(seg_ptr(raw), P[p].kpf.x, Kb, eight));
+            wb[p] = ldg_f2(fd_addr_m(seg_ptr(raw), P[p].kpf.y, Kb, eight));
         }
     }
 #pragma unroll kFdUnroll
@@ -1264,7 +1282,6 @@ __device__ __forceinline__ void fd_segments(unsigned seg, int total, FdPair (&P)
         const float qse = __uint_as_float(raw.z), qds = __uint_as_float(raw.w);
         const float2 se2 = make_float2(qse, qse);
         const uint4 nraw = lds128(seg + 16u * (unsigned)(s + 1));   // record `total` repeats the last one
-        const unsigned long long mptr = kM ? seg_ptr(nraw) + K8 : 0ull;
 #pragma unroll
         for (int p = 0; p < NP; ++p) {
             const float2 le = __fadd2_rn(se2, P[p].ntz);                 // sigma_e - tau
@@ -1273,12 +1290,12 @@ __device__ __forceinline__ void fd_segments(unsigned seg, int total, FdPair (&P)
             const float lma = lm.x, lmb = lm.y;
             P[p].kpf = __ffma2_rn(cr, P[p].dkf, P[p].kpf);
             P[p].ntz = __ffma2_rn(cr, P[p].ndtz, P[p].ntz);
-            const float2 na = ldg_f2(fd_addr(seg_ptr(nraw), P[p].kpf.x));
-            const float2 nb = ldg_f2(fd_addr(seg_ptr(nraw), P[p].kpf.y));
+            const float2 na = ldg_f2(kM ? fd_addr_w(seg_ptr(nraw), P[p].kpf.x, eight) : fd_addr(seg_ptr(nraw), P[p].kpf.x));
+            const float2 nb = ldg_f2(kM ? fd_addr_w(seg_ptr(nraw), P[p].kpf.y, eight) : fd_addr(seg_ptr(nraw), P[p].kpf.y));
             float2 ma = make_float2(0.f, 0.f), mb = make_float2(0.f, 0.f);
             if (kM) {
-                ma = ldg_f2(fd_addr_m(mptr, P[p].kpf.x));
-                mb = ldg_f2(fd_addr_m(mptr, P[p].kpf.y));
+                ma = ldg_f2(fd_addr_m(seg_ptr(nraw), P[p].kpf.x, Kb, eight));
+                mb = ldg_f2(fd_addr_m(seg_ptr(nraw), P[p].kpf.y, Kb, eight));
             }
             P[p].acc0a = fmaf(va[p].x, qds, P[p].acc0a);                  // f_s d_sigma
             P[p].acc1a = fmaf(va[p].y, lma, P[p].acc1a);                  // (f_e - f_s) l_e
@@ -1387,9 +1404,8 @@ k_fwd_fd(const ViewRec* __restrict__ views, DetC dc, GridC g, const float2* __re
         Mr[p].acc0a = Mr[p].acc0b = Mr[p].acc1a = Mr[p].acc1b = 0.f;
         any_live |= (Za.active && ra < rows_top) | (Zb.active && rb < rows_top);
     }
-    // mirrored address offset: 8 (2 kMagicBits + NzP + N_z - 1 + 2 pad)
-    const unsigned long long K8 =
-        8ull * (2ull * kMagicBits + (unsigned long long)L.nzp + (unsigned long long)(g.n[2] - 1 + 2 * L.pad));
+    // mirrored cell: bits(kpf') = Kb - bits(kpf), Kb = 2 kMagicBits + NzP + N_z - 1 + 2 pad (< 2^32)
+    const unsigned Kb = 2u * kMagicBits + (unsigned)L.nzp + (unsigned)(g.n[2] - 1 + 2 * L.pad);
     if (!__any_sync(0xffffffffu, any_live)) return;
     Seg* seg = s_seg[warp];
     const unsigned seg_s = (unsigned)__cvta_generic_to_shared(seg);
@@ -1439,7 +1455,7 @@ k_fwd_fd(const ViewRec* __restrict__ views, DetC dc, GridC g, const float2* __re
             }
 #pragma unroll
             for (int p = 0; p < NP; ++p) fd_anchor(P[p], sc);
-            fd_segments<NP, kM>(seg_s, total, P, Mr, K8);
+            fd_segments<NP, kM>(seg_s, total, P, Mr, Kb, L.eight);
         }
         __syncwarp();  // the next chunk overwrites the segments
     }
@@ -1757,6 +1773,7 @@ ColumnLaunch make_launch(const xrt_plan_s* p, int64_t v0, int64_t v1, int& nblk,
     L.n_bands = (p->det.rows + rows_per_band - 1) / rows_per_band;
     L.nzp = (int)p->nzp;
     L.pad = (int)p->zpad;
+    L.eight = 8u;
     static const xrt_plan_s::ColTiling kUntiled{};
     const xrt_plan_s::ColTiling& T = untiled ? kUntiled : p->ct[adj ? 1 : 0];
     L.tile = T.tile;
