@@ -1265,7 +1265,7 @@ struct FdMirror {
 template <int NP, bool kM = false>
 __device__ __forceinline__ void fd_segments(unsigned seg, int total, FdPair (&P)[NP], FdMirror (&Mr)[NP],
                                             unsigned Kb, unsigned eight) {
-    constexpr int kFdUnroll = XRT_FD_UNROLL > 0 ? XRT_FD_UNROLL : (NP == 1 && !kM ? 4 : 2);
+    constexpr int kFdUnroll = XRT_FD_UNROLL > 0 ? XRT_FD_UNROLL : (NP == 1 ? 4 : 2);   // z-mirror (NP 1): 92.6 ms at 4 vs 94.7 at 2
     uint4 raw = lds128(seg);
     float2 va[NP], vb[NP], wa[NP], wb[NP];
 #pragma unroll
@@ -1321,8 +1321,12 @@ __device__ __forceinline__ void fd_segments(unsigned seg, int total, FdPair (&P)
 #define XRT_FD_THREADS 1024  // resident threads per SM targeted by the launch bounds (2 pairs per lane):
 #endif                       // cfg 4 124.0 ms vs 136.0 (768), 138.9 (512); 4 x 4 CTAs 126.6
 #ifndef XRT_FD_THREADS1
-#define XRT_FD_THREADS1 1024 // ... 1 pair per lane (cfg 5: 18.2 ms vs 18.4 at 768, 19.6 at 512)
+#define XRT_FD_THREADS1 1280 // ... 1 pair per lane (cfg 5: 15.55 ms at 1280 vs 16.20 at 1024, 16.0 at 768)
 #endif
+#ifndef XRT_FD_THREADSM
+#define XRT_FD_THREADSM 1024 // ... the z-mirror forward (cfg 4: 92.6 ms vs 98.4 at 1280, 102.7 at 768)
+#endif
+#define XRT_FD_MINBM (XRT_FD_THREADSM / (32 * kFdWarps) > 0 ? XRT_FD_THREADSM / (32 * kFdWarps) : 1)
 #define XRT_FD_MINB (XRT_FD_THREADS / (32 * kFdWarps) > 0 ? XRT_FD_THREADS / (32 * kFdWarps) : 1)
 
 #define XRT_FD_MINB1 (XRT_FD_THREADS1 / (32 * kFdWarps) > 0 ? XRT_FD_THREADS1 / (32 * kFdWarps) : 1)
@@ -1340,7 +1344,7 @@ __device__ __forceinline__ void fd_segments(unsigned seg, int total, FdPair (&P)
 // decisions, not an independent fp32 walk of row r'); the self-mirror middle row (odd rows) is walked
 // only.  Saves the z-state arithmetic of half the rays.
 template <int NP, bool kM>
-__global__ void __launch_bounds__(kFdWarps * 32, NP == 1 ? XRT_FD_MINB1 : XRT_FD_MINB)
+__global__ void __launch_bounds__(kFdWarps * 32, kM ? XRT_FD_MINBM : (NP == 1 ? XRT_FD_MINB1 : XRT_FD_MINB))
 k_fwd_fd(const ViewRec* __restrict__ views, DetC dc, GridC g, const float2* __restrict__ fd,
          float* __restrict__ sino_out, int view0, const ColDesc* __restrict__ desc, ColumnLaunch L) {
     constexpr int R = 2 * NP;
