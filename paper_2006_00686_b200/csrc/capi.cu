@@ -1039,9 +1039,10 @@ xrt_status xrt_forward_host(xrt_plan p, const float* img_host, float* sino_host,
             dhi = dlo;
         }
         const int nst = (int)steps.size();
-        std::vector<cudaEvent_t> evc((size_t)nst), evb((size_t)nbm);
+        std::vector<cudaEvent_t> evc((size_t)nst), evb((size_t)nbm), evp((size_t)xrt_plan_s::kFwdParts);
         for (auto& x : evc) XRT_CUDA(cudaEventCreateWithFlags(&x, cudaEventDisableTiming));
         for (auto& x : evb) XRT_CUDA(cudaEventCreateWithFlags(&x, cudaEventDisableTiming));
+        for (auto& x : evp) XRT_CUDA(cudaEventCreateWithFlags(&x, cudaEventDisableTiming));
         cudaEvent_t ev0, ev_end;
         XRT_CUDA(cudaEventCreateWithFlags(&ev0, cudaEventDisableTiming));
         XRT_CUDA(cudaEventCreateWithFlags(&ev_end, cudaEventDisableTiming));
@@ -1083,15 +1084,35 @@ xrt_status xrt_forward_host(xrt_plan p, const float* img_host, float* sino_host,
                 }
                 if (ok) { need = i; break; }
             }
+            const int mr = xrt::fd_mirror_band_rows();
+            const int r0 = mr * b, r1 = std::min(top, mr * (b + 1));
+            const int q0[2] = {r0, rows - r1};
+            if (b == nbm - 1 && p->d_fd_part_items) {
+                // the last band part by part (view ranges): each part's rows go down while the next
+                // part computes, so only the last part's copy is exposed
+                for (int q = 0; q < xrt_plan_s::kFwdParts && e == cudaSuccess; ++q) {
+                    const int64_t v0 = p->fd_part_view[q], v1 = p->fd_part_view[q + 1];
+                    cudaStream_t c = cs[(b + q) & 1];
+                    e = cudaStreamWaitEvent(c, evc[need], 0);
+                    if (e == cudaSuccess)
+                        e = xrt::launch_forward_fd_mirror_band_part(p, p->d_work_fd, p->d_stage_sino, b, q, c);
+                    p->launches += 1;
+                    if (e == cudaSuccess) e = cudaEventRecord(evp[q], c);
+                    if (e == cudaSuccess) e = cudaStreamWaitEvent(d, evp[q], 0);
+                    for (int h = 0; h < 2 && e == cudaSuccess && v1 > v0; ++h)
+                        e = cudaMemcpy2DAsync(sino_host + v0 * p->det.per_view + (int64_t)q0[h] * p->det.cols, pitch,
+                                              p->d_stage_sino + v0 * p->det.per_view + (int64_t)q0[h] * p->det.cols,
+                                              pitch, sizeof(float) * (size_t)(r1 - r0) * p->det.cols, (size_t)(v1 - v0),
+                                              cudaMemcpyDeviceToHost, d);
+                }
+                continue;
+            }
             cudaStream_t c = cs[b & 1];
             e = cudaStreamWaitEvent(c, evc[need], 0);
             if (e == cudaSuccess) e = xrt::launch_forward_fd_mirror_bands(p, p->d_work_fd, p->d_stage_sino, b, b + 1, c);
             p->launches += 1;
             if (e == cudaSuccess) e = cudaEventRecord(evb[b], c);
             if (e == cudaSuccess) e = cudaStreamWaitEvent(d, evb[b], 0);
-            const int mr = xrt::fd_mirror_band_rows();
-            const int r0 = mr * b, r1 = std::min(top, mr * (b + 1));
-            const int q0[2] = {r0, rows - r1};
             for (int h = 0; h < 2 && e == cudaSuccess; ++h)
                 e = cudaMemcpy2DAsync(sino_host + (int64_t)q0[h] * p->det.cols, pitch,
                                       p->d_stage_sino + (int64_t)q0[h] * p->det.cols, pitch,
@@ -1108,6 +1129,7 @@ xrt_status xrt_forward_host(xrt_plan p, const float* img_host, float* sino_host,
         if (e3 == cudaSuccess) e3 = e4;
         for (auto& x : evc) cudaEventDestroy(x);
         for (auto& x : evb) cudaEventDestroy(x);
+        for (auto& x : evp) cudaEventDestroy(x);
         cudaEventDestroy(ev0);
         cudaEventDestroy(ev_end);
         if (e != cudaSuccess) return cuda_fail(e, "forward_host mirrored pipeline");

@@ -2008,6 +2008,35 @@ cudaError_t launch_forward_fd_band_part(const xrt_plan_s* p, const float2* fd, f
     return launch_fd(p, fd, sino, L, L.n_items, s);
 }
 
+// z-mirror band b, views [fd_part_view[part], fd_part_view[part + 1]) only (tiled plans)
+cudaError_t launch_forward_fd_mirror_band_part(const xrt_plan_s* p, const float2* fd, float* sino, int b, int part,
+                                               cudaStream_t s) {
+    if (!p->d_fd_part_items || part < 0 || part >= xrt_plan_s::kFwdParts) return cudaErrorInvalidValue;
+    int nblk = 0;
+    ColumnLaunch L = make_launch(p, 0, p->n_views, nblk, false);
+    L.n_cgroups = (p->det.cols + kFdCols - 1) / kFdCols;
+    L.tile = p->ct_fd.tile;
+    L.n_tx = p->ct_fd.n_tx;
+    L.items = (const uint2*)p->d_fd_part_items + p->fd_part_off[part];
+    L.n_items = (int)(p->fd_part_off[part + 1] - p->fd_part_off[part]);
+    const int rows = p->det.rows, top = (rows + 1) / 2;
+    const int r0 = 64 * kMirNP * b, r1 = std::min(top, 64 * kMirNP * (b + 1));
+    const int64_t v0 = p->fd_part_view[part], v1 = p->fd_part_view[part + 1];
+    if (r1 <= r0 || v1 <= v0 || L.n_items <= 0) return cudaSuccess;
+    const size_t pitch = sizeof(float) * (size_t)p->det.per_view;
+    cudaError_t e = cudaMemset2DAsync(sino + v0 * p->det.per_view + (int64_t)r0 * p->det.cols, pitch, 0,
+                                      sizeof(float) * (size_t)(r1 - r0) * p->det.cols, (size_t)(v1 - v0), s);
+    if (e == cudaSuccess)
+        e = cudaMemset2DAsync(sino + v0 * p->det.per_view + (int64_t)(rows - r1) * p->det.cols, pitch, 0,
+                              sizeof(float) * (size_t)(r1 - r0) * p->det.cols, (size_t)(v1 - v0), s);
+    if (e != cudaSuccess) return e;
+    if (cudaError_t e2 = set_dbg_range(fd, 16ull * (size_t)p->grid.nxy * (size_t)p->nzp, s); e2 != cudaSuccess) return e2;
+    L.band0 = b;
+    k_fwd_fd<kMirNP, true><<<L.n_items, kFdWarps * 32, 0, s>>>(p->d_views, p->det, p->grid, fd, sino, 0,
+                                                              (const ColDesc*)p->d_coldesc, L);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_forward_column_bands(const xrt_plan_s* p, const float* vol_zfast, float* sino, int b0,
                                         int b1, cudaStream_t s) {
     int nblk = 0;

@@ -365,6 +365,8 @@ int fd_mirror_bands(const xrt_plan_s* p);
 int fd_mirror_band_rows();           // upper-half rows per z-mirror band
 cudaError_t launch_forward_fd_mirror_bands(const xrt_plan_s* p, const float2* fd, float* sino, int b0, int b1,
                                            cudaStream_t s);
+cudaError_t launch_forward_fd_mirror_band_part(const xrt_plan_s* p, const float2* fd, float* sino, int b, int part,
+                                               cudaStream_t s);
 cudaError_t launch_adjoint_column_band_part(const xrt_plan_s* p, const float* sino, float* vol_zfast, int b,
                                             int part, cudaStream_t s);
 cudaError_t launch_forward_fd_band_part(const xrt_plan_s* p, const float2* fd, float* sino, int b, int part,
