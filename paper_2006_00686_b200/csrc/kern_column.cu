@@ -1221,6 +1221,10 @@ __device__ __forceinline__ float2 ldg_f2(unsigned long long a) {
     asm("ld.global.nc.L2::256B.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "l"(a));
 #elif XRT_FD_LDHINT == 3
     asm("ld.global.nc.L1::evict_first.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "l"(a));
+#elif XRT_FD_LDHINT == 4
+    asm("ld.global.nc.L1::no_allocate.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "l"(a));
+#elif XRT_FD_LDHINT == 5
+    asm("ld.global.nc.L1::evict_normal.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "l"(a));
 #else
     asm("ld.global.nc.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "l"(a));
 #endif
