@@ -293,6 +293,17 @@ xrt_status fwd_prepare(xrt_plan p, const float* img, cudaStream_t s) {
         if (e != cudaSuccess) return cuda_fail(e, "transpose launch");
         return XRT_OK;
     }
+    if (p->fd_forward && xrt::fd_f4_on(p)) {
+        if (!p->d_work_fd4) {   // first use: the interleaved z-mirror volume (same size as the fd volume), zeroed
+            const size_t b4 = sizeof(float4) * (size_t)(p->grid.nxy * p->nzp);
+            XRT_CUDA(cudaMalloc(&p->d_work_fd4, b4));
+            XRT_CUDA(cudaMemsetAsync(p->d_work_fd4, 0, b4, s));
+        }
+        cudaError_t e = xrt::launch_to_fd4(p, img, p->d_work_fd4, s);
+        p->launches += 1;
+        if (e != cudaSuccess) return cuda_fail(e, "transpose launch");
+        return XRT_OK;
+    }
     cudaError_t e = p->fd_forward ? xrt::launch_to_fd(p, img, p->d_work_fd, s) : xrt::launch_to_zfast(p, img, p->d_work_fwd, s);
     p->launches += 1;
     if (e != cudaSuccess) return cuda_fail(e, "transpose launch");
@@ -789,6 +800,7 @@ xrt_status xrt_plan_destroy(xrt_plan p) {
     cudaFree(p->d_raydesc2d);
     cudaFree(p->d_ray2d_walk);
     cudaFree(p->d_fwd_t);
+    cudaFree(p->d_work_fd4);
     cudaFree(p->d_fd2d);
     cudaFree(p->d_img_t);
     cudaFree(p->d_stage_img);

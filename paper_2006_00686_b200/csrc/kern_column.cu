@@ -1266,10 +1266,59 @@ struct FdMirror {
     float acc0a, acc0b, acc1a, acc1b;   // the mirrored rays of the pair's rays a / b
 };
 
-template <int NP, bool kM = false>
+// interleaved z-mirror layout (kF4): one 16-byte load gives the walked ray's (f, f[k+1] - f[k]) and its
+// mirror's (f', f'[k'-1] - f'), k' = N_z - 1 + 2 pad - k: address = ptr + 16 bits(kpf)
+__device__ __forceinline__ float4 ldg_f4(unsigned long long ptr, float kpf) {
+    unsigned long long a;
+    asm("{ .reg .u64 t; cvt.u64.u32 t, %1; shl.b64 t, t, 4; add.s64 %0, %2, t; }" : "=l"(a) : "r"(__float_as_uint(kpf)), "l"(ptr));
+    dbg_chk((const void*)a, 16);
+    float4 v;
+    asm("ld.global.nc.L1::evict_last.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(a));
+    return v;
+}
+
+template <int NP, bool kM = false, bool kF4 = false>
 __device__ __forceinline__ void fd_segments(unsigned seg, int total, FdPair (&P)[NP], FdMirror (&Mr)[NP],
                                             unsigned Kb, unsigned eight) {
     constexpr int kFdUnroll = XRT_FD_UNROLL > 0 ? XRT_FD_UNROLL : (NP == 1 ? 4 : 2);   // z-mirror (NP 1): 92.6 ms at 4 vs 94.7 at 2
+    if constexpr (kF4) {
+        uint4 raw = lds128(seg);
+        float4 qa[NP], qb[NP];
+#pragma unroll
+        for (int p = 0; p < NP; ++p) {
+            qa[p] = ldg_f4(seg_ptr(raw), P[p].kpf.x);
+            qb[p] = ldg_f4(seg_ptr(raw), P[p].kpf.y);
+        }
+#pragma unroll kFdUnroll
+        for (int s = 0; s < total; ++s) {
+            const float qse = __uint_as_float(raw.z), qds = __uint_as_float(raw.w);
+            const float2 se2 = make_float2(qse, qse);
+            const uint4 nraw = lds128(seg + 16u * (unsigned)(s + 1));
+#pragma unroll
+            for (int p = 0; p < NP; ++p) {
+                const float2 le = __fadd2_rn(se2, P[p].ntz);
+                const float2 cr = make_float2(fd_cr(le.x), fd_cr(le.y));
+                const float2 lm = __fmul2_rn(le, cr);
+                const float lma = lm.x, lmb = lm.y;
+                P[p].kpf = __ffma2_rn(cr, P[p].dkf, P[p].kpf);
+                P[p].ntz = __ffma2_rn(cr, P[p].ndtz, P[p].ntz);
+                const float4 na = ldg_f4(seg_ptr(nraw), P[p].kpf.x);
+                const float4 nb = ldg_f4(seg_ptr(nraw), P[p].kpf.y);
+                P[p].acc0a = fmaf(qa[p].x, qds, P[p].acc0a);
+                P[p].acc1a = fmaf(qa[p].y, lma, P[p].acc1a);
+                P[p].acc0b = fmaf(qb[p].x, qds, P[p].acc0b);
+                P[p].acc1b = fmaf(qb[p].y, lmb, P[p].acc1b);
+                Mr[p].acc0a = fmaf(qa[p].z, qds, Mr[p].acc0a);
+                Mr[p].acc1a = fmaf(qa[p].w, lma, Mr[p].acc1a);
+                Mr[p].acc0b = fmaf(qb[p].z, qds, Mr[p].acc0b);
+                Mr[p].acc1b = fmaf(qb[p].w, lmb, Mr[p].acc1b);
+                qa[p] = na;
+                qb[p] = nb;
+            }
+            raw = nraw;
+        }
+        return;
+    }
     uint4 raw = lds128(seg);
     float2 va[NP], vb[NP], wa[NP], wb[NP];
 #pragma unroll
@@ -1347,7 +1396,11 @@ __device__ __forceinline__ void fd_segments(unsigned seg, int total, FdPair (&P)
 // Each mirrored ray's units and C_up - C_low are those of its walked ray mirrored (the fp32 walk's
 // decisions, not an independent fp32 walk of row r'); the self-mirror middle row (odd rows) is walked
 // only.  Saves the z-state arithmetic of half the rays.
-template <int NP, bool kM>
+//
+// kF4 (with kM): the interleaved layout fd4[cell][k_p] = (f[k], f[k+1] - f[k], f[k'], f[k'-1] - f[k']) of
+// k_to_fd4 (k' the mirrored cell): the walked ray (its z steps +1: the upper rows of the z-symmetric
+// cone) and its mirror from ONE 16-byte load.
+template <int NP, bool kM, bool kF4 = false>
 __global__ void __launch_bounds__(kFdWarps * 32, kM ? XRT_FD_MINBM : (NP == 1 ? XRT_FD_MINB1 : XRT_FD_MINB))
 k_fwd_fd(const ViewRec* __restrict__ views, DetC dc, GridC g, const float2* __restrict__ fd,
          float* __restrict__ sino_out, int view0, const ColDesc* __restrict__ desc, ColumnLaunch L) {
@@ -1406,8 +1459,9 @@ k_fwd_fd(const ViewRec* __restrict__ views, DetC dc, GridC g, const float2* __re
     for (int p = 0; p < NP; ++p) {
         RayZ Za, Zb;
         const int ra = (band * R + 2 * p) * 32 + lane, rb = ra + 32;
-        ray_z(V, dc, g, Pth, ca, ra, L.pad, Za);
-        ray_z(V, dc, g, Pth, ca, rb, L.pad, Zb);
+        // z-mirror: rows past the upper half (last band) walk as inactive rays (flat, in the zero padding)
+        ray_z(V, dc, g, Pth, ca, (!kM || ra < rows_top) ? ra : dc.rows, L.pad, Za);
+        ray_z(V, dc, g, Pth, ca, (!kM || rb < rows_top) ? rb : dc.rows, L.pad, Zb);
         fd_init(P[p], Za, Zb, L.nzp);
         Mr[p].acc0a = Mr[p].acc0b = Mr[p].acc1a = Mr[p].acc1b = 0.f;
         any_live |= (Za.active && ra < rows_top) | (Zb.active && rb < rows_top);
@@ -1418,7 +1472,8 @@ k_fwd_fd(const ViewRec* __restrict__ views, DetC dc, GridC g, const float2* __re
     Seg* seg = s_seg[warp];
     const unsigned seg_s = (unsigned)__cvta_generic_to_shared(seg);
     // segment pointers pre-offset by -8 kMagicBits bytes: address = ptr + 8 bits(kpf)
-    const unsigned long long base = (unsigned long long)fd - 8ull * kMagicBits;
+    // (kF4: 16-byte cells, nzp of them per column -- the same column stride)
+    const unsigned long long base = (unsigned long long)fd - (kF4 ? 16ull : 8ull) * kMagicBits;
     const unsigned long long cstride = 16ull * (unsigned long long)L.nzp;
     bool zinit = !tiled;  // untiled: the z state at sigma = 0 is the initial one
     const ColDesc* dsc = desc + ((int64_t)v * dc.cols + c);
@@ -1463,7 +1518,7 @@ k_fwd_fd(const ViewRec* __restrict__ views, DetC dc, GridC g, const float2* __re
             }
 #pragma unroll
             for (int p = 0; p < NP; ++p) fd_anchor(P[p], sc);
-            fd_segments<NP, kM>(seg_s, total, P, Mr, Kb, L.eight);
+            fd_segments<NP, kM, kF4>(seg_s, total, P, Mr, Kb, L.eight);
         }
         __syncwarp();  // the next chunk overwrites the segments
     }
@@ -1889,6 +1944,49 @@ cudaError_t launch_to_fd(const xrt_plan_s* p, const float* img, float2* fd, cuda
     return launch_to_fd_rows(p, img, fd, -1, p->grid.n[2] + 1, s);
 }
 
+// interleaved z-mirror layout: fd4[cell][j] = (F[j], F[j+1] - F[j], F[C-j], F[C-j-1] - F[C-j]), F the
+// zero-padded column (F[j] = f[j - pad]), C = N_z - 1 + 2 pad; rows j = pad - 1 .. pad + N_z hold data
+// (the rest of the buffer stays zero from its allocation)
+__global__ void __launch_bounds__(256) k_to_fd4(const float* __restrict__ img, float4* __restrict__ fd4, int64_t nxy,
+                                                int nz, int64_t nzp, int pad, int j_lo) {
+    __shared__ float t[33][33], u[33][33];
+    const int64_t c0 = (int64_t)blockIdx.y * 32;
+    const int j0 = j_lo + (int)blockIdx.x * 32;
+    const int C = nz - 1 + 2 * pad;
+    for (int r = threadIdx.y; r < 33; r += 8) {
+        const int64_t c = c0 + threadIdx.x;
+        const int k1 = j0 + r - pad, k2 = C - j0 - r - pad;
+        t[r][threadIdx.x] = (k1 >= 0 && k1 < nz && c < nxy) ? img[(int64_t)k1 * nxy + c] : 0.f;
+        u[r][threadIdx.x] = (k2 >= 0 && k2 < nz && c < nxy) ? img[(int64_t)k2 * nxy + c] : 0.f;
+    }
+    __syncthreads();
+    const int j_hi = pad + nz + 1;
+    for (int cc = threadIdx.y; cc < 32; cc += 8) {
+        const int64_t c = c0 + cc;
+        const int j = j0 + (int)threadIdx.x;
+        if (c >= nxy || j >= j_hi) continue;
+        const float f = t[threadIdx.x][cc], fn = t[threadIdx.x + 1][cc];
+        const float g = u[threadIdx.x][cc], gn = u[threadIdx.x + 1][cc];
+        fd4[c * nzp + j] = make_float4(f, fn - f, g, gn - g);
+    }
+}
+
+#ifndef XRT_FD_F4
+#define XRT_FD_F4 1   // device-path z-mirror forward on the interleaved layout (XRT_FD_F4=0 per launch: two halves)
+#endif
+bool fd_f4_on(const xrt_plan_s* p) {
+    if (!fd_mirror_on_x(p)) return false;
+    const char* e = std::getenv("XRT_FD_F4");
+    return e ? std::atoi(e) != 0 : XRT_FD_F4 != 0;
+}
+
+cudaError_t launch_to_fd4(const xrt_plan_s* p, const float* img, float4* fd4, cudaStream_t s) {
+    const int j_lo = std::max(0, (int)p->zpad - 1), j_hi = (int)(p->zpad + p->grid.n[2] + 1);
+    dim3 grid((unsigned)((j_hi - j_lo + 31) / 32), (unsigned)((p->grid.nxy + 31) / 32));
+    k_to_fd4<<<grid, dim3(32, 8), 0, s>>>(img, fd4, p->grid.nxy, p->grid.n[2], p->nzp, (int)p->zpad, j_lo);
+    return cudaGetLastError();
+}
+
 static cudaError_t launch_fd(const xrt_plan_s* p, const float2* fd, float* sino, const ColumnLaunch& L, int nblk,
                              cudaStream_t s) {
     if (nblk <= 0) return cudaSuccess;
@@ -1904,6 +2002,7 @@ static cudaError_t launch_fd(const xrt_plan_s* p, const float2* fd, float* sino,
 }
 
 int fd_mirror_bands(const xrt_plan_s* p);
+bool fd_f4_on(const xrt_plan_s* p);
 #ifndef XRT_FD_MIRROR_NP
 #define XRT_FD_MIRROR_NP 1   // walked ray pairs per lane of the z-mirror forward (rows per band 64 NP)
 #endif
@@ -1936,6 +2035,16 @@ cudaError_t launch_forward_fd_bands(const xrt_plan_s* p, const float2* fd, float
     cudaError_t e = cudaMemset2DAsync(sino + (int64_t)r0 * p->det.cols, pitch, 0,
                                       sizeof(float) * (size_t)(r1 - r0) * p->det.cols, (size_t)p->n_views, s);
     if (e != cudaSuccess) return e;
+    if (fd_f4_on(p)) {
+        // the interleaved layout (built by fwd_prepare's launch_to_fd4) serves only the full-range call
+        if (!(r0 == 0 && r1 == p->det.rows) || !p->d_work_fd4) return cudaErrorInvalidValue;
+        L.band0 = 0;
+        if (cudaError_t e2 = set_dbg_range(p->d_work_fd4, 16ull * (size_t)p->grid.nxy * (size_t)p->nzp, s); e2 != cudaSuccess)
+            return e2;
+        k_fwd_fd<kMirNP, true, true><<<L.n_items * fd_mirror_bands(p), kFdWarps * 32, 0, s>>>(
+            p->d_views, p->det, p->grid, (const float2*)p->d_work_fd4, sino, 0, (const ColDesc*)p->d_coldesc, L);
+        return cudaGetLastError();
+    }
     if (fd_mirror_on(p) && r0 == 0 && r1 == p->det.rows) {
         // all rows: bands of 64 upper-half rows, each with its mirrored rows (same L2 slab budget:
         // two 64-row slabs per band instead of one 128-row slab)
@@ -1951,6 +2060,7 @@ cudaError_t launch_forward_fd_bands(const xrt_plan_s* p, const float2* fd, float
 }
 
 bool fd_mirror_active(const xrt_plan_s* p) { return fd_mirror_on(p); }
+bool fd_mirror_on_x(const xrt_plan_s* p) { return fd_mirror_on(p); }
 int fd_mirror_bands(const xrt_plan_s* p) { return ((p->det.rows + 1) / 2 + 64 * kMirNP - 1) / (64 * kMirNP); }
 int fd_mirror_band_rows() { return 64 * kMirNP; }
 

@@ -225,6 +225,7 @@ struct xrt_plan_s {
     float* d_work_fwd = nullptr;       // z-fastest, z-padded copy of the forward input (COLUMN)
     float* d_work_adj = nullptr;       // z-fastest, z-padded adjoint accumulator (COLUMN)
     float2* d_work_fd = nullptr;       // forward (COLUMN): per cell 2 x NzP (f, f[k+-1] - f[k]) cells
+    float4* d_work_fd4 = nullptr;      // z-mirror forward, device path: interleaved (f, df, f', df') cells (first use)
     bool fd_forward = true;            // AUTO forward on the (f, delta f) volume (XRT_FWD_LEGACY=1: k_column)
     bool flat_z = false;               // every ray keeps one z cell (par3d, tilt 0): flat column kernels
     bool fd_mirror = false;            // circular cone symmetric in z: the fd forward walks the upper rows and their mirrors
@@ -361,6 +362,9 @@ cudaError_t launch_forward_fd_bands(const xrt_plan_s* p, const float2* fd, float
                                     cudaStream_t s);
 int fd_view_block();                 // views per CTA of the fd forward (kFdViews)
 bool fd_mirror_active(const xrt_plan_s* p);
+bool fd_mirror_on_x(const xrt_plan_s* p);
+bool fd_f4_on(const xrt_plan_s* p);
+cudaError_t launch_to_fd4(const xrt_plan_s* p, const float* img, float4* fd4, cudaStream_t s);
 int fd_mirror_bands(const xrt_plan_s* p);
 int fd_mirror_band_rows();           // upper-half rows per z-mirror band
 cudaError_t launch_forward_fd_mirror_bands(const xrt_plan_s* p, const float2* fd, float* sino, int b0, int b1,
