@@ -1062,40 +1062,53 @@ xrt_status xrt_forward_host(xrt_plan p, const float* img_host, float* sino_host,
         XRT_CUDA(cudaStreamWaitEvent(a, ev0, 0));
         XRT_CUDA(cudaStreamWaitEvent(cs[1], ev0, 0));
         cudaError_t e = cudaSuccess;
-        int built_hi = -1, built_lo = nz + 1;     // fd rows [-1, built_hi) and [built_lo, nz] built
-        std::vector<int> done_hi((size_t)nst), done_lo((size_t)nst);
+        // interleaved layout (device-path layout, also here when on): fd4 row k needs image rows k, k + 1
+        // and their mirrors N_z - 1 - k, N_z - 2 - k; two halves: fd row k needs k - 1, k, k + 1.
+        // After every upload step, the rows (k = -1 .. N_z) whose image rows are all present are built
+        // (runs of consecutive rows per launch); built_at[k] = the step after which row k exists.
+        const bool f4 = xrt::fd_f4_on(p);
+        if (f4 && !p->d_work_fd4) {
+            const size_t b4 = sizeof(float4) * (size_t)(nxy * p->nzp);
+            XRT_CUDA(cudaMalloc(&p->d_work_fd4, b4));
+            XRT_CUDA(cudaMemsetAsync(p->d_work_fd4, 0, b4, a));
+        }
+        std::vector<char> up((size_t)nz, 0);
+        std::vector<int> built_at((size_t)nz + 2, -1);   // index k + 1
+        auto present = [&](int k) { return k < 0 || k >= nz || up[(size_t)k]; };
         for (int i = 0; i < nst && e == cudaSuccess; ++i) {
             const Step& S = steps[i];
             e = cudaMemcpyAsync(p->d_stage_img + S.lo * nxy, img_host + S.lo * nxy,
                                 sizeof(float) * (size_t)((S.hi - S.lo) * nxy), cudaMemcpyHostToDevice, a);
-            if (i == nst - 1) {                   // the fronts met: every remaining row has its neighbours
-                if (e == cudaSuccess) e = xrt::launch_to_fd_rows(p, p->d_stage_img, p->d_work_fd, built_hi, built_lo, a);
-                built_hi = nz + 1; built_lo = -1;
-            } else if (S.asc) {
-                const int kb = S.hi - 1;          // row hi - 1 waits for its upper neighbour
-                if (e == cudaSuccess) e = xrt::launch_to_fd_rows(p, p->d_stage_img, p->d_work_fd, built_hi, kb, a);
-                built_hi = std::max(built_hi, kb);
-            } else {
-                const int ka = S.lo + 1;          // row lo waits for its lower neighbour
-                if (e == cudaSuccess) e = xrt::launch_to_fd_rows(p, p->d_stage_img, p->d_work_fd, ka, built_lo, a);
-                built_lo = std::min(built_lo, ka);
+            for (int k = S.lo; k < S.hi; ++k) up[(size_t)k] = 1;
+            int run0 = -2;
+            for (int k = -1; k <= nz + 1 && e == cudaSuccess; ++k) {
+                bool ready = false;
+                if (k <= nz && built_at[(size_t)k + 1] < 0)
+                    ready = f4 ? (present(k) && present(k + 1) && present(nz - 1 - k) && present(nz - 2 - k))
+                               : (present(k - 1) && present(k) && present(k + 1));
+                if (ready) {
+                    built_at[(size_t)k + 1] = i;
+                    if (run0 == -2) run0 = k;
+                } else if (run0 != -2) {
+                    e = f4 ? xrt::launch_to_fd4_rows(p, p->d_stage_img, p->d_work_fd4, run0, k, a)
+                           : xrt::launch_to_fd_rows(p, p->d_stage_img, p->d_work_fd, run0, k, a);
+                    p->launches += 1;
+                    run0 = -2;
+                }
             }
-            p->launches += 1;
-            done_hi[i] = built_hi;
-            done_lo[i] = built_lo;
             if (e == cudaSuccess) e = cudaEventRecord(evc[i], a);
         }
         const size_t pitch = sizeof(float) * (size_t)p->det.per_view;
         for (int b = 0; b < nbm && e == cudaSuccess; ++b) {
-            int need = nst - 1;
-            for (int i = 0; i < nst; ++i) {
-                bool ok = true;
-                for (int h = 0; h < 2; ++h) {
-                    const int x0 = (int)p->fwdm_band_k[4 * b + 2 * h] - 1, x1 = (int)p->fwdm_band_k[4 * b + 2 * h + 1] + 1;
-                    ok = ok && (x1 <= done_hi[i] || x0 >= done_lo[i] || done_hi[i] >= done_lo[i]);
-                }
-                if (ok) { need = i; break; }
+            // the step after which every row the band reads is built (f4: the walked rows' range only,
+            // their mirrors sit in the same fd4 rows)
+            int need = 0;
+            for (int h = 0; h < (f4 ? 1 : 2); ++h) {
+                const int x0 = std::max(-1, (int)p->fwdm_band_k[4 * b + 2 * h] - 1);
+                const int x1 = std::min(nz + 1, (int)p->fwdm_band_k[4 * b + 2 * h + 1] + 1);
+                for (int k = x0; k < x1; ++k) need = std::max(need, built_at[(size_t)k + 1]);
             }
+            if (need < 0) need = nst - 1;
             const int mr = xrt::fd_mirror_band_rows();
             const int r0 = mr * b, r1 = std::min(top, mr * (b + 1));
             const int q0[2] = {r0, rows - r1};

@@ -1948,7 +1948,7 @@ cudaError_t launch_to_fd(const xrt_plan_s* p, const float* img, float2* fd, cuda
 // zero-padded column (F[j] = f[j - pad]), C = N_z - 1 + 2 pad; rows j = pad - 1 .. pad + N_z hold data
 // (the rest of the buffer stays zero from its allocation)
 __global__ void __launch_bounds__(256) k_to_fd4(const float* __restrict__ img, float4* __restrict__ fd4, int64_t nxy,
-                                                int nz, int64_t nzp, int pad, int j_lo) {
+                                                int nz, int64_t nzp, int pad, int j_lo, int j_hi) {
     __shared__ float t[33][33], u[33][33];
     const int64_t c0 = (int64_t)blockIdx.y * 32;
     const int j0 = j_lo + (int)blockIdx.x * 32;
@@ -1960,7 +1960,6 @@ __global__ void __launch_bounds__(256) k_to_fd4(const float* __restrict__ img, f
         u[r][threadIdx.x] = (k2 >= 0 && k2 < nz && c < nxy) ? img[(int64_t)k2 * nxy + c] : 0.f;
     }
     __syncthreads();
-    const int j_hi = pad + nz + 1;
     for (int cc = threadIdx.y; cc < 32; cc += 8) {
         const int64_t c = c0 + cc;
         const int j = j0 + (int)threadIdx.x;
@@ -1980,11 +1979,17 @@ bool fd_f4_on(const xrt_plan_s* p) {
     return e ? std::atoi(e) != 0 : XRT_FD_F4 != 0;
 }
 
-cudaError_t launch_to_fd4(const xrt_plan_s* p, const float* img, float4* fd4, cudaStream_t s) {
-    const int j_lo = std::max(0, (int)p->zpad - 1), j_hi = (int)(p->zpad + p->grid.n[2] + 1);
+// image rows k in [ka, kb) (ka >= -1, kb <= N_z + 1), i.e. padded rows j = pad + k
+cudaError_t launch_to_fd4_rows(const xrt_plan_s* p, const float* img, float4* fd4, int ka, int kb, cudaStream_t s) {
+    const int j_lo = std::max(0, (int)p->zpad + ka), j_hi = (int)p->zpad + kb;
+    if (j_hi <= j_lo) return cudaSuccess;
     dim3 grid((unsigned)((j_hi - j_lo + 31) / 32), (unsigned)((p->grid.nxy + 31) / 32));
-    k_to_fd4<<<grid, dim3(32, 8), 0, s>>>(img, fd4, p->grid.nxy, p->grid.n[2], p->nzp, (int)p->zpad, j_lo);
+    k_to_fd4<<<grid, dim3(32, 8), 0, s>>>(img, fd4, p->grid.nxy, p->grid.n[2], p->nzp, (int)p->zpad, j_lo, j_hi);
     return cudaGetLastError();
+}
+
+cudaError_t launch_to_fd4(const xrt_plan_s* p, const float* img, float4* fd4, cudaStream_t s) {
+    return launch_to_fd4_rows(p, img, fd4, -1, p->grid.n[2] + 1, s);
 }
 
 static cudaError_t launch_fd(const xrt_plan_s* p, const float2* fd, float* sino, const ColumnLaunch& L, int nblk,
@@ -2090,8 +2095,15 @@ cudaError_t launch_forward_fd_mirror_bands(const xrt_plan_s* p, const float2* fd
         e = cudaMemset2DAsync(sino + (int64_t)(rows - r1) * p->det.cols, pitch, 0,
                               sizeof(float) * (size_t)(r1 - r0) * p->det.cols, (size_t)p->n_views, s);
     if (e != cudaSuccess) return e;
-    if (cudaError_t e2 = set_dbg_range(fd, 16ull * (size_t)p->grid.nxy * (size_t)p->nzp, s); e2 != cudaSuccess) return e2;
     L.band0 = b0;
+    if (fd_f4_on(p) && p->d_work_fd4) {   // host pipeline on the interleaved layout
+        if (cudaError_t e2 = set_dbg_range(p->d_work_fd4, 16ull * (size_t)p->grid.nxy * (size_t)p->nzp, s); e2 != cudaSuccess)
+            return e2;
+        k_fwd_fd<kMirNP, true, true><<<L.n_items * (b1 - b0), kFdWarps * 32, 0, s>>>(
+            p->d_views, p->det, p->grid, (const float2*)p->d_work_fd4, sino, 0, (const ColDesc*)p->d_coldesc, L);
+        return cudaGetLastError();
+    }
+    if (cudaError_t e2 = set_dbg_range(fd, 16ull * (size_t)p->grid.nxy * (size_t)p->nzp, s); e2 != cudaSuccess) return e2;
     k_fwd_fd<kMirNP, true><<<L.n_items * (b1 - b0), kFdWarps * 32, 0, s>>>(p->d_views, p->det, p->grid, fd, sino, 0,
                                                                      (const ColDesc*)p->d_coldesc, L);
     return cudaGetLastError();
@@ -2144,8 +2156,15 @@ cudaError_t launch_forward_fd_mirror_band_part(const xrt_plan_s* p, const float2
         e = cudaMemset2DAsync(sino + v0 * p->det.per_view + (int64_t)(rows - r1) * p->det.cols, pitch, 0,
                               sizeof(float) * (size_t)(r1 - r0) * p->det.cols, (size_t)(v1 - v0), s);
     if (e != cudaSuccess) return e;
-    if (cudaError_t e2 = set_dbg_range(fd, 16ull * (size_t)p->grid.nxy * (size_t)p->nzp, s); e2 != cudaSuccess) return e2;
     L.band0 = b;
+    if (fd_f4_on(p) && p->d_work_fd4) {
+        if (cudaError_t e2 = set_dbg_range(p->d_work_fd4, 16ull * (size_t)p->grid.nxy * (size_t)p->nzp, s); e2 != cudaSuccess)
+            return e2;
+        k_fwd_fd<kMirNP, true, true><<<L.n_items, kFdWarps * 32, 0, s>>>(
+            p->d_views, p->det, p->grid, (const float2*)p->d_work_fd4, sino, 0, (const ColDesc*)p->d_coldesc, L);
+        return cudaGetLastError();
+    }
+    if (cudaError_t e2 = set_dbg_range(fd, 16ull * (size_t)p->grid.nxy * (size_t)p->nzp, s); e2 != cudaSuccess) return e2;
     k_fwd_fd<kMirNP, true><<<L.n_items, kFdWarps * 32, 0, s>>>(p->d_views, p->det, p->grid, fd, sino, 0,
                                                               (const ColDesc*)p->d_coldesc, L);
     return cudaGetLastError();

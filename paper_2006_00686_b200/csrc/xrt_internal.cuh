@@ -365,6 +365,7 @@ bool fd_mirror_active(const xrt_plan_s* p);
 bool fd_mirror_on_x(const xrt_plan_s* p);
 bool fd_f4_on(const xrt_plan_s* p);
 cudaError_t launch_to_fd4(const xrt_plan_s* p, const float* img, float4* fd4, cudaStream_t s);
+cudaError_t launch_to_fd4_rows(const xrt_plan_s* p, const float* img, float4* fd4, int ka, int kb, cudaStream_t s);
 int fd_mirror_bands(const xrt_plan_s* p);
 int fd_mirror_band_rows();           // upper-half rows per z-mirror band
 cudaError_t launch_forward_fd_mirror_bands(const xrt_plan_s* p, const float2* fd, float* sino, int b0, int b1,
