@@ -16,7 +16,7 @@ for c in 1 2 3 5; do
 done
 CMD="python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu --no-attenuated"
 timeout 600 $CMD > $out/plain_$tag.log 2>&1 && \
-timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"k_(column|fwd_fd|to_fd|transpose)" -s 12 -c 4 --csv \
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"k_(column|fwd_fd|to_fd|transpose|slice|forward_ray|fd2d)" -s 12 -c 4 --csv \
     --log-file $out/launches_$tag.csv $CMD > $out/ncu_launches_$tag.log 2>&1
 echo "launches exit $?" >> $out/plain_$tag.log
 timeout 1200 ncu --set full --clock-control none --import-source on -k regex:k_fwd_fd -s 1 -c 1 \
