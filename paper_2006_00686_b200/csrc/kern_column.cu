@@ -410,7 +410,6 @@ struct ColumnLaunch {
     int band0;            // first band of this launch (bands band0 .. band0 + grid / n_items - 1)
     int tile, n_tx;       // tile side in cells, tiles along x
     int nzp, pad;
-    unsigned eight;       // 8 as a launch value: a cell address by IMAD.WIDE.U32 (ptxas turns a literal 8 into LEA pairs)
 };
 
 // z state of two rays of one lane (rows lane + 32 q), packed so the per-segment arithmetic of the
@@ -1241,25 +1240,13 @@ __device__ __forceinline__ float2 ldg_f2(unsigned long long a) {
 #endif
 // mirrored ray (kM): the cell z -> -z of the walked ray's, bits(kpf') = Kb - bits(kpf) (see k_fwd_fd),
 // address = ptr + 8 bits(kpf'): IADD3 + IMAD.WIDE.U32
-#ifndef XRT_FD_ADDR_MODE
-#define XRT_FD_ADDR_MODE 0   // z-mirror forward addresses (cfg 4: 94.7 / 100.3 / 111.2 ms): 0 walked LEA pairs / mirrored IADD3 + LEA pair,
-#endif                       // 1 walked LEA pairs / mirrored IADD3 + IMAD.WIDE.U32, 2 both IMAD.WIDE.U32
-__device__ __forceinline__ unsigned long long fd_addr_m(unsigned long long ptr, float kpf, unsigned Kb,
-                                                        unsigned eight) {
+// mirrored cell of the two-half layout: bits(kpf') = Kb - bits(kpf), address = ptr + 8 bits(kpf') by
+// IADD3 + shift-and-add (ALU pipe).  Measured on cfg 4 (profiles/r2_forward_fd.md): 94.7 ms, vs 100.3 ms
+// with IMAD.WIDE.U32 for the mirrored address and 111.2 ms with IMAD.WIDE.U32 for both (FMA-heavy pipe)
+__device__ __forceinline__ unsigned long long fd_addr_m(unsigned long long ptr, float kpf, unsigned Kb) {
     unsigned long long a;
-    if (XRT_FD_ADDR_MODE == 0)
-        asm("mad.wide.u32 %0, %1, 8, %2;" : "=l"(a) : "r"(Kb - __float_as_uint(kpf)), "l"(ptr));
-    else
-        asm("mad.wide.u32 %0, %1, %2, %3;" : "=l"(a) : "r"(Kb - __float_as_uint(kpf)), "r"(eight), "l"(ptr));
+    asm("mad.wide.u32 %0, %1, 8, %2;" : "=l"(a) : "r"(Kb - __float_as_uint(kpf)), "l"(ptr));
     return a;
-}
-__device__ __forceinline__ unsigned long long fd_addr_w(unsigned long long ptr, float kpf, unsigned eight) {
-    if (XRT_FD_ADDR_MODE == 2) {
-        unsigned long long a;
-        asm("mad.wide.u32 %0, %1, %2, %3;" : "=l"(a) : "r"(__float_as_uint(kpf)), "r"(eight), "l"(ptr));
-        return a;
-    }
-    return fd_addr(ptr, kpf);
 }
 
 struct FdMirror {
@@ -1279,7 +1266,7 @@ __device__ __forceinline__ float4 ldg_f4(unsigned long long ptr, float kpf) {
 
 template <int NP, bool kM = false, bool kF4 = false>
 __device__ __forceinline__ void fd_segments(unsigned seg, int total, FdPair (&P)[NP], FdMirror (&Mr)[NP],
-                                            unsigned Kb, unsigned eight) {
+                                            unsigned Kb) {
     constexpr int kFdUnroll = XRT_FD_UNROLL > 0 ? XRT_FD_UNROLL : (NP == 1 ? 4 : 2);   // z-mirror (NP 1): 92.6 ms at 4 vs 94.7 at 2
     if constexpr (kF4) {
         uint4 raw = lds128(seg);
@@ -1323,11 +1310,11 @@ __device__ __forceinline__ void fd_segments(unsigned seg, int total, FdPair (&P)
     float2 va[NP], vb[NP], wa[NP], wb[NP];
 #pragma unroll
     for (int p = 0; p < NP; ++p) {
-        va[p] = ldg_f2(kM ? fd_addr_w(seg_ptr(raw), P[p].kpf.x, eight) : fd_addr(seg_ptr(raw), P[p].kpf.x));
-        vb[p] = ldg_f2(kM ? fd_addr_w(seg_ptr(raw), P[p].kpf.y, eight) : fd_addr(seg_ptr(raw), P[p].kpf.y));
+        va[p] = ldg_f2(fd_addr(seg_ptr(raw), P[p].kpf.x));
+        vb[p] = ldg_f2(fd_addr(seg_ptr(raw), P[p].kpf.y));
         if (kM) {
-            wa[p] = ldg_f2(fd_addr_m(seg_ptr(raw), P[p].kpf.x, Kb, eight));
-            wb[p] = ldg_f2(fd_addr_m(seg_ptr(raw), P[p].kpf.y, Kb, eight));
+            wa[p] = ldg_f2(fd_addr_m(seg_ptr(raw), P[p].kpf.x, Kb));
+            wb[p] = ldg_f2(fd_addr_m(seg_ptr(raw), P[p].kpf.y, Kb));
         }
     }
 #pragma unroll kFdUnroll
@@ -1343,12 +1330,12 @@ __device__ __forceinline__ void fd_segments(unsigned seg, int total, FdPair (&P)
             const float lma = lm.x, lmb = lm.y;
             P[p].kpf = __ffma2_rn(cr, P[p].dkf, P[p].kpf);
             P[p].ntz = __ffma2_rn(cr, P[p].ndtz, P[p].ntz);
-            const float2 na = ldg_f2(kM ? fd_addr_w(seg_ptr(nraw), P[p].kpf.x, eight) : fd_addr(seg_ptr(nraw), P[p].kpf.x));
-            const float2 nb = ldg_f2(kM ? fd_addr_w(seg_ptr(nraw), P[p].kpf.y, eight) : fd_addr(seg_ptr(nraw), P[p].kpf.y));
+            const float2 na = ldg_f2(fd_addr(seg_ptr(nraw), P[p].kpf.x));
+            const float2 nb = ldg_f2(fd_addr(seg_ptr(nraw), P[p].kpf.y));
             float2 ma = make_float2(0.f, 0.f), mb = make_float2(0.f, 0.f);
             if (kM) {
-                ma = ldg_f2(fd_addr_m(seg_ptr(nraw), P[p].kpf.x, Kb, eight));
-                mb = ldg_f2(fd_addr_m(seg_ptr(nraw), P[p].kpf.y, Kb, eight));
+                ma = ldg_f2(fd_addr_m(seg_ptr(nraw), P[p].kpf.x, Kb));
+                mb = ldg_f2(fd_addr_m(seg_ptr(nraw), P[p].kpf.y, Kb));
             }
             P[p].acc0a = fmaf(va[p].x, qds, P[p].acc0a);                  // f_s d_sigma
             P[p].acc1a = fmaf(va[p].y, lma, P[p].acc1a);                  // (f_e - f_s) l_e
@@ -1518,7 +1505,7 @@ k_fwd_fd(const ViewRec* __restrict__ views, DetC dc, GridC g, const float2* __re
             }
 #pragma unroll
             for (int p = 0; p < NP; ++p) fd_anchor(P[p], sc);
-            fd_segments<NP, kM, kF4>(seg_s, total, P, Mr, Kb, L.eight);
+            fd_segments<NP, kM, kF4>(seg_s, total, P, Mr, Kb);
         }
         __syncwarp();  // the next chunk overwrites the segments
     }
@@ -1836,7 +1823,6 @@ ColumnLaunch make_launch(const xrt_plan_s* p, int64_t v0, int64_t v1, int& nblk,
     L.n_bands = (p->det.rows + rows_per_band - 1) / rows_per_band;
     L.nzp = (int)p->nzp;
     L.pad = (int)p->zpad;
-    L.eight = 8u;
     static const xrt_plan_s::ColTiling kUntiled{};
     const xrt_plan_s::ColTiling& T = untiled ? kUntiled : p->ct[adj ? 1 : 0];
     L.tile = T.tile;
